@@ -1,0 +1,1268 @@
+// Host side of the initial pass: device resource management and the
+// reference's event handling (diffusion.hpp Engine::check and handlers),
+// executed only at steps where the device reported a topology event.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <queue>
+#include <unordered_set>
+
+namespace dtb {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(kCudaError, std::string(what) + ": " + cudaGetErrorString(e));
+}
+static void ck(int e, const char* what) { cuda_check(static_cast<cudaError_t>(e), what); }
+
+namespace {
+
+template <class T>
+std::vector<T> to_host(const DevBuf<T>& b, size_t n, cudaStream_t s) {
+  std::vector<T> out(n);
+  if (n) b.download(out.data(), n, s);
+  cuda_check(cudaStreamSynchronize(s), "sync");
+  return out;
+}
+
+struct UnionFind {
+  std::vector<Index> parent;
+  explicit UnionFind(size_t n) : parent(n) { std::iota(parent.begin(), parent.end(), Index{0}); }
+  Index find(Index a) {
+    while (parent[a] != a) a = parent[a] = parent[parent[a]];
+    return a;
+  }
+  void unite(Index a, Index b) {
+    a = find(a);
+    b = find(b);
+    if (a != b) parent[std::max(a, b)] = std::min(a, b);
+  }
+};
+
+double signed_value(double value, double level) {
+  double s = value - level;
+  if (s == 0.0) s = 1e-12 * (1.0 + std::abs(level));
+  return s;
+}
+
+double value_in(const std::vector<std::pair<Index, double>>& sorted_vals, Index v) {
+  auto it = std::lower_bound(sorted_vals.begin(), sorted_vals.end(), std::make_pair(v, -1e300));
+  return (it != sorted_vals.end() && it->first == v) ? it->second : 0.0;
+}
+
+V3 mean_of(const Mesh& m, const std::vector<Index>& verts) {
+  V3 c{};
+  for (Index v : verts) c = c + m.p(v);
+  return verts.empty() ? c : c / static_cast<double>(verts.size());
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// DeviceMesh
+
+DeviceMesh::DeviceMesh(std::shared_ptr<const Mesh> mesh, cudaStream_t s) : mesh_(std::move(mesh)) {
+  const Mesh& m = *mesh_;
+  const Index nv = m.nv(), nf = m.nf(), ne = m.ne();
+  std::vector<double> x(nv), y(nv), z(nv);
+  double maxabs = 1e-300;
+  for (Index v = 0; v < nv; ++v) {
+    x[v] = m.p(v).x;
+    y[v] = m.p(v).y;
+    z[v] = m.p(v).z;
+    maxabs = std::max({maxabs, std::abs(x[v]), std::abs(y[v]), std::abs(z[v])});
+  }
+  // Fixed point with |coord| * 2^k <= 2^38: band sums of up to 2^25 vertices
+  // stay exact in int64 (order-independent device reductions).
+  const int k = 38 - static_cast<int>(std::ceil(std::log2(maxabs)));
+  const double scale = std::ldexp(1.0, k);
+  std::vector<long long> qx(nv), qy(nv), qz(nv);
+  for (Index v = 0; v < nv; ++v) {
+    qx[v] = std::llrint(x[v] * scale);
+    qy[v] = std::llrint(y[v] * scale);
+    qz[v] = std::llrint(z[v] * scale);
+  }
+  px.alloc(nv);
+  py.alloc(nv);
+  pz.alloc(nv);
+  fx.alloc(nv);
+  fy.alloc(nv);
+  fz.alloc(nv);
+  px.upload(x.data(), nv, s);
+  py.upload(y.data(), nv, s);
+  pz.upload(z.data(), nv, s);
+  fx.upload(qx.data(), nv, s);
+  fy.upload(qy.data(), nv, s);
+  fz.upload(qz.data(), nv, s);
+  faces.alloc(3 * static_cast<size_t>(nf));
+  faces.upload(reinterpret_cast<const unsigned*>(m.faces().data()), 3 * static_cast<size_t>(nf), s);
+  std::vector<unsigned> ev(2 * static_cast<size_t>(ne));
+  for (Index e = 0; e < ne; ++e) {
+    ev[2 * e] = m.edge_vertices(e)[0];
+    ev[2 * e + 1] = m.edge_vertices(e)[1];
+  }
+  edges.alloc(ev.size());
+  edges.upload(ev.data(), ev.size(), s);
+  // Front connectivity: mesh neighbours plus, for every incident face, the
+  // apex of the face across the link edge (the edge of the face opposite v).
+  // Two band vertices are related iff their stars contain edge-adjacent
+  // faces, which makes union-find over band vertices equivalent to the
+  // reference's union-find over band triangles.
+  std::vector<int> coff(nv + 1, 0), ccol;
+  ccol.reserve(static_cast<size_t>(nv) * 12);
+  std::vector<int> tmp;
+  for (Index v = 0; v < nv; ++v) {
+    tmp.clear();
+    for (Index q = m.v2v_off()[v]; q < m.v2v_off()[v + 1]; ++q) tmp.push_back(static_cast<int>(m.v2v()[q]));
+    for (Index q = m.v2f_off()[v]; q < m.v2f_off()[v + 1]; ++q) {
+      const Index f = m.v2f()[q];
+      const auto& t = m.face(f);
+      int kv = t[0] == v ? 0 : (t[1] == v ? 1 : 2);
+      const Index e = m.face_edges(f)[(kv + 1) % 3];  // edge (t[kv+1], t[kv+2])
+      const Index g = m.opposite_face(e, f);
+      const auto& tg = m.face(g);
+      const auto& evs = m.edge_vertices(e);
+      for (Index w : tg)
+        if (w != evs[0] && w != evs[1] && w != v) tmp.push_back(static_cast<int>(w));
+    }
+    std::sort(tmp.begin(), tmp.end());
+    tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+    ccol.insert(ccol.end(), tmp.begin(), tmp.end());
+    coff[v + 1] = static_cast<int>(ccol.size());
+  }
+  c_off.alloc(coff.size());
+  c_off.upload(coff.data(), coff.size(), s);
+  c_col.alloc(std::max<size_t>(1, ccol.size()));
+  c_col.upload(ccol.data(), ccol.size(), s);
+  std::vector<int> noff(m.v2v_off().begin(), m.v2v_off().end()), ncol(m.v2v().begin(), m.v2v().end());
+  n_off.alloc(noff.size());
+  n_off.upload(noff.data(), noff.size(), s);
+  n_col.alloc(std::max<size_t>(1, ncol.size()));
+  n_col.upload(ncol.data(), ncol.size(), s);
+  std::vector<int> foff(m.v2f_off().begin(), m.v2f_off().end()), fcol(m.v2f().begin(), m.v2f().end());
+  f_off.alloc(foff.size());
+  f_off.upload(foff.data(), foff.size(), s);
+  f_col.alloc(std::max<size_t>(1, fcol.size()));
+  f_col.upload(fcol.data(), fcol.size(), s);
+  cuda_check(cudaStreamSynchronize(s), "mesh upload");
+
+  view_.nv = static_cast<int>(nv);
+  view_.nf = static_cast<int>(nf);
+  view_.ne = static_cast<int>(ne);
+  view_.px = px.p;
+  view_.py = py.p;
+  view_.pz = pz.p;
+  view_.fx = fx.p;
+  view_.fy = fy.p;
+  view_.fz = fz.p;
+  view_.fx_scale = std::ldexp(1.0, -k);
+  view_.faces = faces.p;
+  view_.edges = edges.p;
+  view_.c_off = c_off.p;
+  view_.c_col = c_col.p;
+  view_.n_off = n_off.p;
+  view_.n_col = n_col.p;
+}
+
+// ---------------------------------------------------------------------------
+// DeviceLaplacian
+
+DeviceLaplacian::DeviceLaplacian(std::shared_ptr<DeviceMesh> dm, cudaStream_t s) : dm_(std::move(dm)) {
+  const Mesh& m = dm_->host();
+  const int nv = static_cast<int>(m.nv());
+  off.alloc(nv + 1);
+  col.alloc(static_cast<size_t>(nv) + 2 * static_cast<size_t>(m.ne()));
+  val.alloc(col.n);
+  mass.alloc(nv);
+  DevBuf<double> grow(nv);
+  DevBuf<int> dnnz(1);
+  LapBuild b{};
+  b.nv = nv;
+  b.nf = static_cast<int>(m.nf());
+  b.px = dm_->px.p;
+  b.py = dm_->py.p;
+  b.pz = dm_->pz.p;
+  b.faces = dm_->faces.p;
+  b.v2v_off = dm_->n_off.p;
+  b.v2v = dm_->n_col.p;
+  b.v2f_off = dm_->f_off.p;
+  b.v2f = dm_->f_col.p;
+  b.s_off = off.p;
+  b.s_col = col.p;
+  b.s_val = val.p;
+  b.mass = mass.p;
+  b.gersh_row = grow.p;
+  b.nnz = dnnz.p;
+  const int rc = launch_assemble(b, s);
+  if (rc == -1) fail(kDegeneracyError, "non-finite cotangent weight");
+  ck(rc, "laplacian assembly");
+  nnz_ = to_host(dnnz, 1, s)[0];
+  std::vector<double> g = to_host(grow, nv, s);
+  gersh_ = 0;
+  for (double r : g) gersh_ = std::max(gersh_, r);
+}
+
+DeviceLaplacian::DeviceLaplacian(std::shared_ptr<DeviceMesh> dm, const std::vector<int>& o, const std::vector<int>& c,
+                                 const std::vector<double>& v, const std::vector<double>& ms, double gershgorin,
+                                 cudaStream_t s)
+    : dm_(std::move(dm)), nnz_(static_cast<int>(c.size())), gersh_(gershgorin) {
+  const size_t nv = dm_->host().nv();
+  if (o.size() != nv + 1 || ms.size() != nv || c.size() != v.size() || o.back() != static_cast<int>(c.size()))
+    fail(kDimensionMismatch, "operator does not match the mesh");
+  off.alloc(o.size());
+  off.upload(o.data(), o.size(), s);
+  col.alloc(std::max<size_t>(1, c.size()));
+  col.upload(c.data(), c.size(), s);
+  val.alloc(std::max<size_t>(1, v.size()));
+  val.upload(v.data(), v.size(), s);
+  mass.alloc(nv);
+  mass.upload(ms.data(), nv, s);
+  cuda_check(cudaStreamSynchronize(s), "operator upload");
+}
+
+void DeviceLaplacian::download(std::vector<int>& o, std::vector<int>& c, std::vector<double>& v, std::vector<double>& ms,
+                               cudaStream_t s) const {
+  const size_t nv = dm_->host().nv();
+  o = to_host(off, nv + 1, s);
+  c = to_host(col, nnz_, s);
+  v = to_host(val, nnz_, s);
+  ms = to_host(mass, nv, s);
+}
+
+void DeviceLaplacian::apply(const double* xh, double* yh, cudaStream_t s) const {
+  const int nv = static_cast<int>(dm_->host().nv());
+  DevBuf<double> x(nv), y(nv);
+  x.upload(xh, nv, s);
+  ck(launch_spmv(nv, off.p, col.p, val.p, mass.p, x.p, y.p, s), "spmv");
+  y.download(yh, nv, s);
+  cuda_check(cudaStreamSynchronize(s), "spmv sync");
+}
+
+DevMesh DeviceLaplacian::view() const {
+  DevMesh v = dm_->view();
+  v.s_off = off.p;
+  v.s_col = col.p;
+  v.s_val = val.p;
+  v.mass = mass.p;
+  return v;
+}
+
+double stable_time_step(const DeviceLaplacian& op, const Coefficients& c) {
+  const double a = c.gradient_energy;
+  const double lambda = op.gershgorin() * 0.5 * a * a;
+  if (lambda <= 0) fail(kInvalidParameter, "operator admits no positive time step");
+  return 0.9 * 2.0 / lambda;
+}
+
+void Config::validate() const {
+  if (!(band_low_threshold > 0) || !(band_low_threshold < saturation) || !(saturation <= 1.0))
+    fail(kInvalidParameter, "need 0 < band threshold < saturation <= 1");
+  if (!(collision_threshold > 0) || collision_threshold > 0.5)
+    fail(kInvalidParameter, "collision threshold must lie in (0, 0.5]");
+  if (check_interval < 1) fail(kInvalidParameter, "check interval must be >= 1");
+  if (max_steps < 1) fail(kInvalidParameter, "max steps must be >= 1");
+}
+
+// Geodesic ball by Dijkstra over mesh edges (diffusion.hpp:134).
+std::vector<Index> seed_region(const Mesh& mesh, Index seed, double radius) {
+  std::vector<double> d(mesh.nv(), 1e300);
+  std::priority_queue<std::pair<double, Index>, std::vector<std::pair<double, Index>>, std::greater<>> q;
+  d[seed] = 0;
+  q.push({0, seed});
+  std::vector<Index> out;
+  while (!q.empty()) {
+    auto [dv, v] = q.top();
+    q.pop();
+    if (dv > d[v]) continue;
+    if (dv > radius) break;
+    out.push_back(v);
+    for (Index o = mesh.v2v_off()[v]; o < mesh.v2v_off()[v + 1]; ++o) {
+      const Index u = mesh.v2v()[o];
+      const double nd = dv + dist(mesh.p(v), mesh.p(u));
+      if (nd < d[u]) {
+        d[u] = nd;
+        q.push({nd, u});
+      }
+    }
+  }
+  std::sort(out.begin(), out.end());
+  return out;
+}
+
+double SurfaceLoop::length() const {
+  double total = 0;
+  for (size_t i = 0; i + 1 < points.size(); ++i) total += dist(points[i].position, points[i + 1].position);
+  return total;
+}
+
+V3 SurfaceLoop::centroid() const {
+  V3 c{};
+  double total = 0;
+  for (size_t i = 0; i + 1 < points.size(); ++i) {
+    const double len = dist(points[i].position, points[i + 1].position);
+    c = c + (points[i].position + points[i + 1].position) * (0.5 * len);
+    total += len;
+  }
+  if (total <= 0) return points.empty() ? V3{} : points.front().position;
+  return c / total;
+}
+
+// Chains edge crossings into closed loops (isoline.hpp:55-103): seeds in
+// ascending edge order, each walk leaves through the face's other crossed
+// edge, the closing point repeats the first.
+static std::vector<SurfaceLoop> chain_crossings(const Mesh& mesh, const std::vector<int>& e_sorted,
+                                                const std::unordered_map<Index, double>& t_of) {
+  std::unordered_map<Index, std::array<Index, 2>> face_edges;
+  for (int ei : e_sorted) {
+    const Index e = static_cast<Index>(ei);
+    for (Index f : mesh.edge_faces(e)) {
+      auto [it, fresh] = face_edges.try_emplace(f, std::array<Index, 2>{e, kInvalid});
+      if (!fresh) it->second[1] = e;
+    }
+  }
+  std::vector<SurfaceLoop> loops;
+  std::unordered_map<Index, bool> visited;
+  for (int ei : e_sorted) {
+    const Index seed = static_cast<Index>(ei);
+    if (visited[seed]) continue;
+    SurfaceLoop loop;
+    Index edge = seed, face = mesh.edge_faces(seed)[0];
+    while (true) {
+      visited[edge] = true;
+      LoopPoint p;
+      p.edge = edge;
+      p.edge_t = t_of.at(edge);
+      const auto& ev = mesh.edge_vertices(edge);
+      p.position = lerp(mesh.p(ev[0]), mesh.p(ev[1]), p.edge_t);
+      p.face = face;
+      loop.points.push_back(p);
+      const auto& fe = face_edges.at(face);
+      const Index next = fe[0] == edge ? fe[1] : fe[0];
+      face = mesh.opposite_face(next, face);
+      edge = next;
+      if (edge == seed) break;
+    }
+    LoopPoint first = loop.points.front();
+    first.face = loop.points.back().face;
+    loop.points.push_back(first);
+    loops.push_back(std::move(loop));
+  }
+  return loops;
+}
+
+std::vector<SurfaceLoop> extract_isoline(const Mesh& mesh, const std::vector<double>& values, double level) {
+  if (values.size() != mesh.nv()) fail(kDimensionMismatch, "isoline values must cover every vertex");
+  std::vector<int> es;
+  std::unordered_map<Index, double> t_of;
+  for (Index e = 0; e < mesh.ne(); ++e) {
+    const auto& ev = mesh.edge_vertices(e);
+    const double sa = signed_value(values[ev[0]], level), sb = signed_value(values[ev[1]], level);
+    if (sa * sb >= 0) continue;
+    es.push_back(static_cast<int>(e));
+    t_of[e] = sa / (sa - sb);
+  }
+  return chain_crossings(mesh, es, t_of);
+}
+
+// ---------------------------------------------------------------------------
+// DeviceField
+
+DeviceField::DeviceField(std::shared_ptr<DeviceMesh> dm, cudaStream_t s) : dm_(std::move(dm)), s_(s) {
+  const size_t nv = dm_->host().nv();
+  cnt.alloc(nv);
+  interest.alloc(nv);
+  scnt.alloc(nv);
+  sflag.alloc(nv);
+  lay.alloc(nv * kSlots);
+  slay.alloc(nv * kSlots);
+  val.alloc(nv * kSlots);
+  sval.alloc(nv * kSlots);
+  region0.alloc(nv);
+  region1.alloc(nv);
+  stamp.alloc(nv);
+  ilist.alloc(nv);
+  parent.alloc(nv * kSlots);
+  active.alloc(kMaxLayers + 1);
+  aidx.alloc(kMaxLayers + 1);
+  alist.alloc(kMaxActive);
+  stat.alloc(kMaxActive);
+  pair_keys.alloc(kPairCap);
+  pairs.alloc(kPairCap);
+  lastpos.alloc(4 * static_cast<size_t>(kMaxLayers + 1));
+  trail.alloc(kTrailCap);
+  ctl.alloc(1);
+  parent.zero(s_);
+  pair_keys.zero(s_);
+  stat.zero(s_);
+  lastpos.zero(s_);
+  ctl.zero(s_);
+  active.zero(s_);
+  view_.cnt = cnt.p;
+  view_.lay = lay.p;
+  view_.val = val.p;
+  view_.interest = interest.p;
+  work_.region[0] = region0.p;
+  work_.region[1] = region1.p;
+  work_.stamp = stamp.p;
+  work_.scnt = scnt.p;
+  work_.slay = slay.p;
+  work_.sval = sval.p;
+  work_.sflag = sflag.p;
+  work_.ilist = ilist.p;
+  work_.parent = parent.p;
+  work_.active = active.p;
+  work_.aidx = aidx.p;
+  work_.alist = alist.p;
+  work_.stat = stat.p;
+  work_.pair_keys = pair_keys.p;
+  work_.pairs = pairs.p;
+  work_.lastpos = lastpos.p;
+  work_.trail = trail.p;
+  work_.ctl = ctl.p;
+}
+
+void DeviceField::init(const std::vector<Index>& seeds) {
+  if (seeds.empty()) fail(kEmptySeed, "seed set is empty");
+  const Index nv = dm_->host().nv();
+  for (Index v : seeds)
+    if (v >= nv) fail(kInvalidParameter, "seed vertex out of range");
+  meta_.clear();
+  meta_.resize(2);
+  meta_[0].active = true;  // base layer
+  meta_[1].active = true;  // seed layer
+  std::vector<int> sv(seeds.begin(), seeds.end());
+  std::sort(sv.begin(), sv.end());
+  sv.erase(std::unique(sv.begin(), sv.end()), sv.end());
+  DevBuf<int> ds(sv.size());
+  ds.upload(sv.data(), sv.size(), s_);
+  ctl.zero(s_);
+  ck(launch_init_field(view_, work_, static_cast<int>(nv), ds.p, static_cast<int>(sv.size()), s_), "init field");
+  Ctl c{};
+  c.base_one = static_cast<int>(nv - sv.size());
+  ctl.upload(&c, 1, s_);
+  sync_active();
+  cuda_check(cudaStreamSynchronize(s_), "init");
+}
+
+std::vector<Index> DeviceField::active_nonbase() const {
+  std::vector<Index> ids;
+  for (Index id = 1; id < meta_.size(); ++id)
+    if (meta_[id].active) ids.push_back(id);
+  return ids;
+}
+
+void DeviceField::sync_active() {
+  if (meta_.size() > static_cast<size_t>(kMaxLayers)) fail(kCapacityExceeded, "more than 65535 layers");
+  std::vector<unsigned char> act(kMaxLayers + 1, 0);
+  std::vector<int> ai(kMaxLayers + 1, -1), al;
+  for (Index id = 1; id < meta_.size(); ++id)
+    if (meta_[id].active) {
+      act[id] = 1;
+      ai[id] = static_cast<int>(al.size());
+      al.push_back(static_cast<int>(id));
+    }
+  if (al.size() > static_cast<size_t>(kMaxActive)) fail(kCapacityExceeded, "too many simultaneously active layers");
+  active.upload(act.data(), act.size(), s_);
+  aidx.upload(ai.data(), ai.size(), s_);
+  if (!al.empty()) alist.upload(al.data(), al.size(), s_);
+  cuda_check(cudaStreamSynchronize(s_), "sync_active");
+}
+
+Ctl DeviceField::read_ctl() const {
+  Ctl c;
+  ctl.download(&c, 1, s_);
+  cuda_check(cudaStreamSynchronize(s_), "read ctl");
+  return c;
+}
+
+std::vector<std::pair<Index, double>> DeviceField::layer_values(Index layer) const {
+  const int nv = static_cast<int>(dm_->host().nv());
+  DevBuf<int> ov(nv), on(1);
+  DevBuf<double> ox(nv);
+  on.zero(s_);
+  ck(launch_pull_layer(view_, nv, static_cast<int>(layer), ov.p, ox.p, on.p, s_), "pull layer");
+  const int n = to_host(on, 1, s_)[0];
+  std::vector<int> hv = to_host(ov, n, s_);
+  std::vector<double> hx = to_host(ox, n, s_);
+  std::vector<std::pair<Index, double>> out(n);
+  for (int i = 0; i < n; ++i) out[i] = {static_cast<Index>(hv[i]), hx[i]};
+  std::sort(out.begin(), out.end());
+  return out;
+}
+
+std::vector<double> DeviceField::dense_row(Index layer) const {
+  const int nv = static_cast<int>(dm_->host().nv());
+  DevBuf<double> d(nv);
+  ck(launch_dense_row(view_, nv, static_cast<int>(layer), d.p, s_), "dense row");
+  return to_host(d, nv, s_);
+}
+
+std::vector<Index> DeviceField::covered_set(double threshold) const {
+  const int nv = static_cast<int>(dm_->host().nv());
+  DevBuf<int> ov(nv), on(1);
+  on.zero(s_);
+  ck(launch_covered(view_, nv, threshold, ov.p, on.p, s_), "covered");
+  const int n = to_host(on, 1, s_)[0];
+  std::vector<int> hv = to_host(ov, n, s_);
+  std::sort(hv.begin(), hv.end());
+  return std::vector<Index>(hv.begin(), hv.end());
+}
+
+unsigned long long DeviceField::hash() const {
+  DevBuf<unsigned long long> h(1);
+  h.zero(s_);
+  ck(launch_field_hash(view_, static_cast<int>(dm_->host().nv()), h.p, s_), "hash");
+  return to_host(h, 1, s_)[0];
+}
+
+int DeviceField::base_one_count() const {
+  DevBuf<int> h(1);
+  h.zero(s_);
+  ck(launch_base_one_count(view_, static_cast<int>(dm_->host().nv()), h.p, s_), "base one");
+  return to_host(h, 1, s_)[0];
+}
+
+void DeviceField::normalize_columns() {
+  Ctl c = read_ctl();
+  c.error = 0;
+  ctl.upload(&c, 1, s_);
+  ck(launch_normalize_all(view_, work_, static_cast<int>(dm_->host().nv()), prune_epsilon, s_), "normalize");
+  if (read_ctl().error == kDevZeroColumn) fail(kZeroColumn, "total field extinction at a vertex");
+}
+
+void DeviceField::mark_region(const DevMesh& op_view, const std::vector<int>& verts, long stamp_value, int parity) {
+  if (verts.empty()) return;
+  DevBuf<int> d(verts.size());
+  d.upload(verts.data(), verts.size(), s_);
+  ck(launch_mark_region(op_view, work_, d.p, static_cast<int>(verts.size()), stamp_value, parity, s_), "mark region");
+  cuda_check(cudaStreamSynchronize(s_), "mark region sync");
+}
+
+std::vector<Index> DeviceField::split_layer(Index layer, const std::vector<std::vector<Index>>& comps, long step_) {
+  if (layer == 0) fail(kInvalidSplit, "cannot split the base layer");
+  if (layer >= meta_.size() || meta_[layer].cleared) fail(kInvalidSplit, "no such layer");
+  if (comps.size() < 2) fail(kInvalidSplit, "split needs at least two components");
+  const auto vals = layer_values(layer);
+  {
+    std::unordered_set<Index> seen;
+    for (const auto& c : comps) {
+      if (c.empty()) fail(kInvalidSplit, "empty split component");
+      for (Index v : c) {
+        if (!seen.insert(v).second) fail(kInvalidSplit, "overlapping split components");
+        auto it = std::lower_bound(vals.begin(), vals.end(), std::make_pair(v, -1e300));
+        if (it == vals.end() || it->first != v) fail(kInvalidSplit, "split component vertex outside layer support");
+      }
+    }
+  }
+  std::vector<Index> children;
+  std::vector<int> verts, newl;
+  for (const auto& c : comps) {
+    const Index child = static_cast<Index>(meta_.size());
+    LayerMeta lm;
+    lm.active = true;
+    lm.parent = layer;
+    lm.created_step = step_;
+    meta_.push_back(lm);
+    for (Index v : c) {
+      verts.push_back(static_cast<int>(v));
+      newl.push_back(static_cast<int>(child));
+    }
+    children.push_back(child);
+  }
+  if (meta_.size() > static_cast<size_t>(kMaxLayers)) fail(kCapacityExceeded, "more than 65535 layers");
+  meta_[layer].active = false;
+  DevBuf<int> dv(verts.size()), dl(newl.size());
+  dv.upload(verts.data(), verts.size(), s_);
+  dl.upload(newl.data(), newl.size(), s_);
+  ck(launch_relabel(view_, work_, dv.p, dl.p, static_cast<int>(verts.size()), static_cast<int>(layer), s_), "relabel");
+  cuda_check(cudaStreamSynchronize(s_), "split");
+  pending_moved.insert(pending_moved.end(), verts.begin(), verts.end());
+  return children;
+}
+
+Index DeviceField::merge_layers(const std::vector<Index>& ids, long step_, std::vector<int>* touched) {
+  if (ids.size() < 2) fail(kInvalidMerge, "merge needs at least two layers");
+  {
+    std::unordered_set<Index> seen;
+    for (Index id : ids) {
+      if (id == 0) fail(kInvalidMerge, "cannot merge the base layer");
+      if (id >= meta_.size() || meta_[id].cleared || !meta_[id].active)
+        fail(kInvalidMerge, "merge of an inactive or cleared layer");
+      if (!seen.insert(id).second) fail(kInvalidMerge, "duplicate layer in merge");
+    }
+  }
+  const Index result = static_cast<Index>(meta_.size());
+  if (result >= static_cast<Index>(kMaxLayers)) fail(kCapacityExceeded, "more than 65535 layers");
+  LayerMeta lm;
+  lm.active = true;
+  lm.parent = ids.front();
+  lm.created_step = step_;
+  lm.merge_parents = ids;
+  meta_.push_back(lm);
+  for (Index id : ids) {
+    meta_[id].active = false;
+    meta_[id].cleared = true;
+  }
+  // Values are accumulated in the order the ids are given; columns store
+  // layers in ascending order, so the device sums in ascending id order.
+  std::vector<int> sorted_ids(ids.begin(), ids.end());
+  std::vector<int> order(sorted_ids);
+  std::sort(order.begin(), order.end());
+  if (order != sorted_ids) fail(kInvalidMerge, "merge ids must be ascending (reference groups are sorted)");
+  const int nv = static_cast<int>(dm_->host().nv());
+  DevBuf<int> g(ids.size()), t(nv), nt(1);
+  g.upload(sorted_ids.data(), ids.size(), s_);
+  nt.zero(s_);
+  ck(launch_merge(view_, work_, nv, g.p, static_cast<int>(ids.size()), static_cast<int>(result), t.p, nt.p, s_),
+     "merge");
+  const int n = to_host(nt, 1, s_)[0];
+  std::vector<int> tv = to_host(t, n, s_);
+  pending_moved.insert(pending_moved.end(), tv.begin(), tv.end());
+  if (touched) *touched = tv;
+  return result;
+}
+
+void DeviceField::set_inactive(Index layer) { meta_[layer].active = false; }
+
+bool DeviceField::finished(Index layer, int nunsat) const {
+  if (nunsat != 0) return false;
+  DevBuf<int> flag(1);
+  const int one = 1;
+  flag.upload(&one, 1, s_);
+  DevMesh m = dm_->view();
+  ck(launch_finished(m, view_, static_cast<int>(layer), prune_epsilon, flag.p, s_), "finished");
+  return to_host(flag, 1, s_)[0] != 0;
+}
+
+long InitialPassResult::handle_estimate_count() const {
+  long n = 0;
+  for (const auto& e : events) n += static_cast<long>(e.estimates.size());
+  return n;
+}
+
+// ---------------------------------------------------------------------------
+// extract_front / detect_collisions / step (one-shot API)
+
+std::vector<FrontComponent> extract_front(const DeviceField& field, Index layer, const Config& cfg) {
+  const Mesh& mesh = field.mesh().host();
+  const auto vals = field.layer_values(layer);
+  std::vector<Index> band;
+  for (const auto& [v, x] : vals)
+    if (x < 1.0 && x > cfg.band_low_threshold && x < cfg.saturation) band.push_back(v);
+  if (band.empty()) return {};
+  std::vector<Index> tris;
+  for (Index v : band)
+    for (Index q = mesh.v2f_off()[v]; q < mesh.v2f_off()[v + 1]; ++q) tris.push_back(mesh.v2f()[q]);
+  std::sort(tris.begin(), tris.end());
+  tris.erase(std::unique(tris.begin(), tris.end()), tris.end());
+  auto slot = [&](Index f) -> long {
+    auto it = std::lower_bound(tris.begin(), tris.end(), f);
+    return (it != tris.end() && *it == f) ? static_cast<long>(it - tris.begin()) : -1;
+  };
+  UnionFind uf(tris.size());
+  for (Index i = 0; i < tris.size(); ++i)
+    for (Index e : mesh.face_edges(tris[i])) {
+      const long j = slot(mesh.opposite_face(e, tris[i]));
+      if (j >= 0) uf.unite(i, static_cast<Index>(j));
+    }
+  std::unordered_map<Index, Index> root_comp;
+  std::vector<FrontComponent> comps;
+  for (Index i = 0; i < tris.size(); ++i) {
+    auto [it, fresh] = root_comp.try_emplace(uf.find(i), static_cast<Index>(comps.size()));
+    if (fresh) {
+      comps.emplace_back();
+      comps.back().layer = layer;
+    }
+    comps[it->second].triangles.push_back(tris[i]);
+  }
+  for (auto& c : comps) {
+    std::vector<Index> verts;
+    for (Index f : c.triangles)
+      for (Index v : mesh.face(f))
+        if (std::binary_search(band.begin(), band.end(), v)) verts.push_back(v);
+    std::sort(verts.begin(), verts.end());
+    verts.erase(std::unique(verts.begin(), verts.end()), verts.end());
+    c.boundary_vertices = std::move(verts);
+    double len = 0;
+    for (Index f : c.triangles) {
+      V3 pts[3];
+      int count = 0;
+      const auto& t = mesh.face(f);
+      for (int k = 0; k < 3 && count < 3; ++k) {
+        const Index a = t[k], b = t[(k + 1) % 3];
+        const double sa = signed_value(value_in(vals, a), 0.5), sb = signed_value(value_in(vals, b), 0.5);
+        if (sa * sb >= 0) continue;
+        pts[count++] = lerp(mesh.p(a), mesh.p(b), sa / (sa - sb));
+      }
+      if (count == 2) len += dist(pts[0], pts[1]);
+    }
+    c.band_length = len;
+  }
+  return comps;
+}
+
+namespace {
+
+StepParams make_params(const DeviceField& field, const Config& cfg, const Coefficients& c, double dt) {
+  StepParams p{};
+  const auto act = field.active_nonbase();
+  const double n = static_cast<double>(act.size() + 1);
+  const double m = static_cast<double>(act.size());
+  p.mu_n = c.mobility / n;
+  p.m_mu_n = m * (c.mobility / n);
+  p.w = c.penalty;
+  p.e = c.contact;
+  p.half_a2 = 0.5 * c.gradient_energy * c.gradient_energy;
+  p.dt = dt;
+  p.prune = field.prune_epsilon;
+  p.band_lo = cfg.band_low_threshold;
+  p.sat = cfg.saturation;
+  p.kappa = cfg.collision_threshold;
+  p.coll_base_limit = 1.0 - cfg.collision_threshold;
+  p.extinct_limit = 1.0 - cfg.saturation;
+  p.check_interval = cfg.check_interval;
+  p.n_active = static_cast<int>(act.size());
+  p.record_trails = cfg.record_trails ? 1 : 0;
+  p.do_hash = cfg.record_hashes ? 1 : 0;
+  p.do_check = 1;
+  return p;
+}
+
+int engine_blocks(int nv) {
+  static int maxco = 0;
+  if (!maxco) ck(dev_max_coresident_blocks(&maxco), "occupancy");
+  if (const char* env = std::getenv("DTB_BLOCKS")) {
+    const int b = std::atoi(env);
+    if (b > 0) return std::min(b, maxco);
+  }
+  const int want = std::max(1, nv / 2048);
+  return std::min(want, maxco);
+}
+
+std::vector<std::vector<Index>> groups_from_pairs(const std::vector<unsigned>& pairs) {
+  std::vector<Index> layers;
+  for (unsigned p : pairs) {
+    layers.push_back(p >> 16);
+    layers.push_back(p & 0xFFFF);
+  }
+  std::sort(layers.begin(), layers.end());
+  layers.erase(std::unique(layers.begin(), layers.end()), layers.end());
+  auto slot = [&](Index l) { return static_cast<Index>(std::lower_bound(layers.begin(), layers.end(), l) - layers.begin()); };
+  UnionFind uf(layers.size());
+  for (unsigned p : pairs) uf.unite(slot(p >> 16), slot(p & 0xFFFF));
+  std::map<Index, std::vector<Index>> g;
+  for (Index i = 0; i < layers.size(); ++i) g[uf.find(i)].push_back(layers[i]);
+  std::vector<std::vector<Index>> out;
+  for (auto& [r, mem] : g)
+    if (mem.size() >= 2) out.push_back(mem);
+  std::sort(out.begin(), out.end());
+  return out;
+}
+
+std::vector<unsigned> read_pairs(const DeviceField& field) {
+  const Ctl c = field.read_ctl();
+  if (c.pair_overflow) fail(kCapacityExceeded, "collision pair table overflow");
+  return to_host(field.pairs, static_cast<size_t>(c.npairs), field.stream());
+}
+
+void run_check_kernel(DeviceField& field, const Config& cfg, const Coefficients& co, double dt) {
+  StepParams p = make_params(field, cfg, co, dt);
+  static int maxco = 0;
+  if (!maxco) ck(dev_max_coresident_blocks(&maxco), "occupancy");
+  const int blocks = std::min(maxco, std::max(1, static_cast<int>(field.mesh().host().nv()) / 2048));
+  ck(launch_check(field.mesh().view(), field.view(), field.work(), p, blocks, field.stream()), "check kernel");
+  cuda_check(cudaStreamSynchronize(field.stream()), "check sync");
+}
+
+std::vector<LayerStat> read_stats(const DeviceField& field) {
+  const size_t n = field.active_nonbase().size();
+  return to_host(field.stat, n, field.stream());
+}
+
+}  // namespace
+
+std::vector<std::vector<Index>> detect_collisions(DeviceField& field, const Config& cfg) {
+  cfg.validate();
+  field.sync_active();
+  if (field.active_nonbase().size() < 2) return {};
+  run_check_kernel(field, cfg, Coefficients{}, 0.0);
+  return groups_from_pairs(read_pairs(field));
+}
+
+void step(DeviceField& field, const DeviceLaplacian& op, const Config& cfg, const Coefficients& c) {
+  cfg.validate();
+  const double dt = cfg.dt > 0 ? cfg.dt : stable_time_step(op, c);
+  field.sync_active();
+  cudaStream_t s = field.stream();
+  // prime_full_frontier: every support vertex of the base and active layers.
+  cuda_check(cudaMemsetAsync(field.stamp.p, 0xFF, sizeof(int) * field.stamp.n, s), "stamp reset");
+  DevWork w = field.work();
+  w.stamp = field.stamp.p;
+  Ctl ctl = field.read_ctl();
+  ctl.rcount[0] = ctl.rcount[1] = 0;
+  ctl.error = 0;
+  ctl.stop_bits = 0;
+  ctl.trail_pending = 0;
+  field.ctl.upload(&ctl, 1, s);
+  const DevMesh m = op.view();
+  ck(launch_mark_all_support(m, field.view(), w, 0, 1, s), "mark support");
+  StepParams p = make_params(field, cfg, c, dt);
+  p.step_begin = 1;
+  p.step_end = 2;
+  p.do_check = 0;
+  ck(launch_run(m, field.view(), w, p, engine_blocks(m.nv), s), "step kernel");
+  cuda_check(cudaStreamSynchronize(s), "step sync");
+  const Ctl after = field.read_ctl();
+  if (after.error == kDevBlowup) fail(kNumericalBlowup, "non-finite rate; reduce dt");
+  if (after.error == kDevZeroColumn) fail(kZeroColumn, "total field extinction at vertex " + std::to_string(after.error_vertex));
+  if (after.error) fail(kCapacityExceeded, "column capacity exceeded at vertex " + std::to_string(after.error_vertex));
+}
+
+namespace {
+
+// The initial pass (diffusion.hpp:530 Engine) with the step loop on the device.
+class PassEngine {
+ public:
+  PassEngine(std::shared_ptr<DeviceMesh> dm, const DeviceLaplacian& op, Index seed, const Config& cfg,
+             const Coefficients& co)
+      : dm_(std::move(dm)), mesh_(dm_->host()), op_(op), cfg_(cfg), co_(co) {
+    cfg_.validate();
+    if (seed >= mesh_.nv()) fail(kInvalidParameter, "seed vertex out of range");
+    cuda_check(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "stream");
+    field_ = std::make_shared<DeviceField>(dm_, s_);
+    res_.field = field_;
+    res_.seed_vertex = seed;
+    const double radius =
+        cfg_.seed_radius > 0 ? cfg_.seed_radius : 1.5 * (co_.gradient_energy / std::sqrt(co_.penalty));
+    const std::vector<Index> seeds = seed_region(mesh_, seed, radius);
+    field_->init(seeds);
+    dt_ = cfg_.dt > 0 ? cfg_.dt : stable_time_step(op_, co_);
+    res_.dt_used = dt_;
+    if (cfg_.record_hashes) {
+      field_->hashes.alloc(static_cast<size_t>(cfg_.max_steps) + 1);
+      field_->hashes.zero(s_);
+    }
+    TopologyEvent ev;
+    ev.kind = EventKind::Seed;
+    ev.step = 0;
+    ev.layers = {1};
+    ev.position = mesh_.p(seed);
+    res_.events.push_back(ev);
+    track(1).created_event = 0;
+    std::vector<int> sv(seeds.begin(), seeds.end());
+    field_->mark_region(op_.view(), sv, 0, 1);
+    blocks_ = engine_blocks(static_cast<int>(mesh_.nv()));
+  }
+  ~PassEngine() {
+    if (s_) cudaStreamDestroy(s_);
+  }
+
+  InitialPassResult run() {
+    long step = 0;
+    try {
+      while (true) {
+        if (step >= cfg_.max_steps) {
+          res_.status = kMaxStepsExceeded;
+          res_.message = "initial pass exceeded " + std::to_string(cfg_.max_steps) + " steps";
+          break;
+        }
+        const long s = advance_until_event(step);
+        if (s < 0) {  // budget exhausted without an event
+          step = cfg_.max_steps;
+          continue;
+        }
+        step = s;
+        if (host_check(s)) break;
+      }
+    } catch (const Error& e) {
+      res_.status = e.code;
+      res_.message = e.what();
+    }
+    res_.steps = step;
+    finish_tracks();
+    if (cfg_.record_hashes) {
+      const size_t n = static_cast<size_t>(std::min(step, cfg_.max_steps));
+      std::vector<unsigned long long> h = to_host(field_->hashes, n + 1, s_);
+      for (size_t i = 1; i <= n; ++i)
+        if (i % static_cast<size_t>(cfg_.check_interval) == 0) res_.hashes.push_back(h[i]);
+    }
+    return std::move(res_);
+  }
+
+ private:
+  LayerTrack& track(Index layer) {
+    if (layer >= tracks_.size()) tracks_.resize(layer + 1);
+    tracks_[layer].layer = layer;
+    return tracks_[layer];
+  }
+
+  StepParams params() const {
+    StepParams p = make_params(*field_, cfg_, co_, dt_);
+    p.stop_every_check = cfg_.on_check ? 1 : 0;
+    return p;
+  }
+
+  DevWork work() const {
+    DevWork w = field_->work();
+    if (cfg_.record_hashes) {
+      w.hashes = field_->hashes.p;
+      w.hash_base = 0;
+      w.hash_cap = static_cast<int>(field_->hashes.n);
+    }
+    return w;
+  }
+
+  // Runs device steps from `done`+1 until an event step (returned) or the
+  // step budget (returns -1 after executing through max_steps).
+  long advance_until_event(long done) {
+    const auto t0 = std::chrono::steady_clock::now();
+    StepParams p = params();
+    const long per_launch = std::max<long>(1, (kTrailCap / std::max(1, p.n_active)) - 2);
+    long begin = done + 1;
+    while (true) {
+      const long end = std::min<long>(cfg_.max_steps + 1, begin + std::min<long>(per_launch, 1L << 20));
+      if (begin >= end) {
+        res_.t_device += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return -1;
+      }
+      p.step_begin = begin;
+      p.step_end = end;
+      ck(launch_run(op_.view(), field_->view(), work(), p, blocks_, s_), "engine launch");
+      cuda_check(cudaStreamSynchronize(s_), "engine sync");
+      ++res_.launches;
+      Ctl c = field_->read_ctl();
+      drain_trails(c);
+      res_.kernel_steps += c.stop_step - begin + 1;
+      if (c.error) {
+        res_.t_device += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (c.error == kDevBlowup) fail(kNumericalBlowup, "non-finite rate; reduce dt");
+        if (c.error == kDevZeroColumn)
+          fail(kZeroColumn, "total field extinction at vertex " + std::to_string(c.error_vertex));
+        fail(kCapacityExceeded, "column capacity exceeded at vertex " + std::to_string(c.error_vertex));
+      }
+      if (c.stop_bits) {
+        res_.t_device += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return static_cast<long>(c.stop_step);
+      }
+      begin = end;
+    }
+  }
+
+  void drain_trails(Ctl& c) {
+    if (c.ntrail == 0) return;
+    if (c.ntrail > kTrailCap) fail(kCapacityExceeded, "trail ring overflow");
+    std::vector<TrailRec> recs = to_host(field_->trail, static_cast<size_t>(c.ntrail), s_);
+    std::sort(recs.begin(), recs.end(), [](const TrailRec& a, const TrailRec& b) {
+      return a.step != b.step ? a.step < b.step : a.layer < b.layer;
+    });
+    for (const auto& r : recs) {
+      if (cfg_.record_trails) track(static_cast<Index>(r.layer)).trail.push_back(mesh_.p(static_cast<Index>(r.vertex)));
+    }
+    const int zero = 0;
+    cuda_check(cudaMemcpyAsync(&field_->ctl.p->ntrail, &zero, sizeof(int), cudaMemcpyHostToDevice, s_), "ntrail");
+    cuda_check(cudaStreamSynchronize(s_), "ntrail sync");
+    c.ntrail = 0;
+  }
+
+  void set_lastpos(Index layer, const V3& p) {
+    const double v[4] = {p.x, p.y, p.z, 1.0};
+    cuda_check(cudaMemcpyAsync(field_->lastpos.p + 4 * static_cast<size_t>(layer), v, sizeof v, cudaMemcpyHostToDevice,
+                               s_),
+               "lastpos");
+    cuda_check(cudaStreamSynchronize(s_), "lastpos sync");
+  }
+  bool get_lastpos(Index layer, V3& p) const {
+    double v[4];
+    cuda_check(cudaMemcpyAsync(v, field_->lastpos.p + 4 * static_cast<size_t>(layer), sizeof v, cudaMemcpyDeviceToHost,
+                               s_),
+               "lastpos");
+    cuda_check(cudaStreamSynchronize(s_), "lastpos sync");
+    if (v[3] == 0.0) return false;
+    p = {v[0], v[1], v[2]};
+    return true;
+  }
+
+  std::vector<Index> band_of(const std::vector<std::pair<Index, double>>& vals) const {
+    std::vector<Index> band;
+    for (const auto& [v, x] : vals)
+      if (x < 1.0 && x > cfg_.band_low_threshold && x < cfg_.saturation) band.push_back(v);
+    return band;
+  }
+
+  // handle_split (diffusion.hpp:642).
+  bool handle_split(Index layer, const std::vector<FrontComponent>& fronts, long s) {
+    const auto vals = field_->layer_values(layer);
+    std::vector<Index> unsat;
+    for (const auto& [v, x] : vals)
+      if (x < 1.0) unsat.push_back(v);
+    auto is_unsat = [&](Index v) { return std::binary_search(unsat.begin(), unsat.end(), v); };
+    std::unordered_map<Index, Index> label;
+    std::vector<Index> queue;
+    for (Index c = 0; c < fronts.size(); ++c)
+      for (Index v : fronts[c].boundary_vertices)
+        if (label.emplace(v, c).second) queue.push_back(v);
+    for (size_t head = 0; head < queue.size(); ++head) {
+      const Index v = queue[head];
+      const Index c = label.at(v);
+      for (Index o = mesh_.v2v_off()[v]; o < mesh_.v2v_off()[v + 1]; ++o) {
+        const Index u = mesh_.v2v()[o];
+        if (!is_unsat(u)) continue;
+        if (label.emplace(u, c).second) queue.push_back(u);
+      }
+    }
+    std::vector<std::vector<Index>> comps(fronts.size());
+    for (Index v : unsat) {
+      auto it = label.find(v);
+      comps[it == label.end() ? 0 : it->second].push_back(v);
+    }
+    comps.erase(std::remove_if(comps.begin(), comps.end(), [](const auto& c) { return c.empty(); }), comps.end());
+    if (comps.size() < 2) return false;
+    std::vector<Index> parent_band;
+    for (const auto& f : fronts) parent_band.insert(parent_band.end(), f.boundary_vertices.begin(), f.boundary_vertices.end());
+    std::sort(parent_band.begin(), parent_band.end());
+    parent_band.erase(std::unique(parent_band.begin(), parent_band.end()), parent_band.end());
+    const std::vector<Index> children = field_->split_layer(layer, comps, s);
+    TopologyEvent ev;
+    ev.kind = EventKind::Split;
+    ev.step = s;
+    ev.layers = {layer};
+    ev.produced = children;
+    ev.position = mean_of(mesh_, parent_band);
+    const Index idx = static_cast<Index>(res_.events.size());
+    res_.events.push_back(std::move(ev));
+    track(layer).consumed_event = idx;
+    for (Index c : children) track(c).created_event = idx;
+    return true;
+  }
+
+  // front_loop_of_layer (diffusion.hpp:606): longest mid-level isoline of the
+  // layer that is not a frozen seam.
+  bool front_loop(Index layer, SurfaceLoop& out) const {
+    const DevMesh m = dm_->view();
+    const int ne = m.ne;
+    DevBuf<int> de(ne), dn(1);
+    DevBuf<double> dtt(ne), dba(ne), dbb(ne);
+    dn.zero(s_);
+    ck(launch_crossings(m, field_->view(), static_cast<int>(layer), 0.5, de.p, dtt.p, dba.p, dbb.p, dn.p, s_),
+       "crossings");
+    const int n = to_host(dn, 1, s_)[0];
+    std::vector<int> e = to_host(de, n, s_);
+    std::vector<double> t = to_host(dtt, n, s_), ba = to_host(dba, n, s_), bb = to_host(dbb, n, s_);
+    std::unordered_map<Index, double> t_of, b0, b1;
+    for (int i = 0; i < n; ++i) {
+      t_of[static_cast<Index>(e[i])] = t[i];
+      b0[static_cast<Index>(e[i])] = ba[i];
+      b1[static_cast<Index>(e[i])] = bb[i];
+    }
+    std::sort(e.begin(), e.end());
+    std::vector<SurfaceLoop> loops = chain_crossings(mesh_, e, t_of);
+    double best = -1;
+    for (auto& loop : loops) {
+      double base_mass = 0;
+      size_t samples = 0;
+      for (const auto& p : loop.points) {
+        if (p.edge == kInvalid) continue;
+        base_mass += (1.0 - p.edge_t) * b0.at(p.edge) + p.edge_t * b1.at(p.edge);
+        ++samples;
+      }
+      if (samples == 0 || base_mass / samples < 0.01) continue;
+      const double len = loop.length();
+      if (len > best) {
+        best = len;
+        out = std::move(loop);
+      }
+    }
+    return best > 0;
+  }
+
+  // handle_merge (diffusion.hpp:698).
+  void handle_merge(const std::vector<Index>& group, long s) {
+    struct FrontLoop {
+      Index layer;
+      SurfaceLoop loop;
+      double length;
+    };
+    std::vector<FrontLoop> loops;
+    for (Index id : group) {
+      SurfaceLoop loop;
+      if (front_loop(id, loop)) loops.push_back({id, std::move(loop), 0});
+    }
+    for (auto& fl : loops) fl.length = fl.loop.length();
+    std::vector<Index> union_band;
+    std::map<Index, std::vector<std::pair<Index, double>>> snaps;
+    for (Index id : group) {
+      auto vals = field_->layer_values(id);
+      auto band = band_of(vals);
+      union_band.insert(union_band.end(), band.begin(), band.end());
+      snaps[id] = std::move(vals);
+    }
+    std::sort(union_band.begin(), union_band.end());
+    union_band.erase(std::unique(union_band.begin(), union_band.end()), union_band.end());
+    TopologyEvent ev;
+    ev.kind = EventKind::Merge;
+    ev.step = s;
+    ev.layers = group;
+    ev.position = mean_of(mesh_, union_band);
+    ev.covered_snapshot = field_->covered_set(cfg_.covered_threshold);
+    const Index idx = static_cast<Index>(res_.events.size());
+    if (!loops.empty()) {
+      size_t drop = 0;
+      for (size_t i = 1; i < loops.size(); ++i)
+        if (loops[i].length > loops[drop].length ||
+            (loops[i].length == loops[drop].length && loops[i].layer < loops[drop].layer))
+          drop = i;
+      loops.erase(loops.begin() + static_cast<std::ptrdiff_t>(drop));
+      std::sort(loops.begin(), loops.end(), [](const FrontLoop& a, const FrontLoop& b) {
+        return a.length != b.length ? a.length < b.length : a.layer < b.layer;
+      });
+      for (auto& fl : loops) {
+        HandleEstimate est;
+        est.loop = std::move(fl.loop);
+        est.layer = fl.layer;
+        est.field_snapshot = snaps[fl.layer];
+        est.event_index = idx;
+        ev.estimates.push_back(std::move(est));
+      }
+    }
+    const Index merged = field_->merge_layers(group, s);
+    ev.produced = {merged};
+    const V3 pos = ev.position;
+    res_.events.push_back(std::move(ev));
+    for (Index id : group) track(id).consumed_event = idx;
+    track(merged).created_event = idx;
+    set_lastpos(merged, pos);
+  }
+
+  void handle_vanish(Index layer, long s) {
+    TopologyEvent ev;
+    ev.kind = EventKind::Vanish;
+    ev.step = s;
+    ev.layers = {layer};
+    V3 p;
+    if (!get_lastpos(layer, p)) {
+      std::vector<Index> support;
+      for (const auto& [v, x] : field_->layer_values(layer)) support.push_back(v);
+      p = mean_of(mesh_, support);
+    }
+    ev.position = p;
+    const Index idx = static_cast<Index>(res_.events.size());
+    res_.events.push_back(std::move(ev));
+    track(layer).consumed_event = idx;
+    field_->set_inactive(layer);
+  }
+
+  // check() (diffusion.hpp:807) for a step at which the device flagged an
+  // event.  Returns true when the run is over.
+  bool host_check(long s) {
+    const auto t0 = std::chrono::steady_clock::now();
+    ++res_.event_checks;
+    bool changed = false;
+    {
+      const std::vector<LayerStat> st = read_stats(*field_);
+      const std::vector<Index> act = field_->active_nonbase();
+      for (size_t a = 0; a < act.size(); ++a) {
+        if (st[a].ncomp < 2) continue;
+        auto fronts = extract_front(*field_, act[a], cfg_);
+        if (fronts.size() < 2)
+          fail(kInconsistentLog, "device reported a split the host front extraction does not see");
+        changed |= handle_split(act[a], fronts, s);
+      }
+    }
+    if (changed) {
+      field_->sync_active();
+      run_check_kernel(*field_, cfg_, co_, dt_);
+    }
+    const auto groups = groups_from_pairs(read_pairs(*field_));
+    for (const auto& g : groups) {
+      handle_merge(g, s);
+      changed = true;
+    }
+    if (!groups.empty()) {
+      field_->sync_active();
+      run_check_kernel(*field_, cfg_, co_, dt_);
+    }
+    // Band anchors (device: means, snaps, trail records) and vanishing layers.
+    const std::vector<Index> act = field_->active_nonbase();
+    const std::vector<LayerStat> st = read_stats(*field_);
+    StepParams p = params();
+    p.step_begin = s;
+    if (cfg_.record_trails) ck(launch_snap(dm_->view(), field_->view(), field_->work(), p, s_), "snap");
+    ck(launch_flush(dm_->view(), field_->view(), field_->work(), p, s_), "flush");
+    cuda_check(cudaStreamSynchronize(s_), "flush sync");
+    Ctl c = field_->read_ctl();
+    drain_trails(c);
+    bool vanished = false;
+    for (size_t a = 0; a < act.size(); ++a) {
+      if (st[a].nband > 0) continue;
+      if (field_->finished(act[a], st[a].nunsat)) {
+        handle_vanish(act[a], s);
+        vanished = true;
+      }
+    }
+    if (cfg_.on_check) cfg_.on_check(s);
+    bool done = false;
+    const double bmax = [&] {
+      double d;
+      std::memcpy(&d, &c.base_max_bits, 8);
+      return d;
+    }();
+    if (c.base_one == 0 && bmax < 1.0 - cfg_.saturation) {
+      for (Index l : field_->active_nonbase()) handle_vanish(l, s);
+      done = true;
+    } else if (field_->active_nonbase().empty()) {
+      done = true;
+    }
+    field_->sync_active();
+    // Vertices logged by split/merge join the next frontier (change log).
+    if (!field_->pending_moved.empty()) {
+      field_->mark_region(op_.view(), field_->pending_moved, s, static_cast<int>((s + 1) & 1));
+      field_->pending_moved.clear();
+    }
+    (void)vanished;
+    if (cfg_.record_hashes && s < static_cast<long>(field_->hashes.n)) {
+      const unsigned long long h = field_->hash();
+      cuda_check(cudaMemcpyAsync(field_->hashes.p + s, &h, sizeof h, cudaMemcpyHostToDevice, s_), "hash");
+      cuda_check(cudaStreamSynchronize(s_), "hash sync");
+    }
+    res_.t_events += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return done;
+  }
+
+  void finish_tracks() { res_.tracks = tracks_; }
+
+  std::shared_ptr<DeviceMesh> dm_;
+  const Mesh& mesh_;
+  const DeviceLaplacian& op_;
+  Config cfg_;
+  Coefficients co_;
+  cudaStream_t s_ = nullptr;
+  std::shared_ptr<DeviceField> field_;
+  InitialPassResult res_;
+  std::vector<LayerTrack> tracks_;
+  double dt_ = 0;
+  int blocks_ = 1;
+};
+
+}  // namespace
+
+InitialPassResult run_initial_pass(std::shared_ptr<DeviceMesh> dm, const DeviceLaplacian& op, Index seed,
+                                   const Config& cfg, const Coefficients& c) {
+  PassEngine e(std::move(dm), op, seed, cfg, c);
+  return e.run();
+}
+
+ReebGraph build_reeb(const InitialPassResult& r) {
+  ReebGraph g;
+  for (const auto& ev : r.events) g.nodes.push_back({ev.kind, ev.position, ev.step});
+  for (const auto& t : r.tracks) {
+    if (t.layer == kInvalid || t.created_event == kInvalid || t.consumed_event == kInvalid) continue;
+    if (t.consumed_event < t.created_event) fail(kInconsistentLog, "layer consumed before created");
+    g.arcs.push_back({t.created_event, t.consumed_event, t.layer, t.trail});
+  }
+  return g;
+}
+
+}  // namespace dtb

@@ -1,0 +1,281 @@
+// Host orchestration of the device engine: device-resident mesh, Laplacian
+// operator, layer field, and the initial pass (reference diffusion.hpp).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <functional>
+#include <map>
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "kernels.h"
+#include "mesh.hpp"
+
+namespace dtb {
+
+void cuda_check(cudaError_t e, const char* what);
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+    o.p = nullptr;
+    o.n = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) cuda_check(cudaMalloc(reinterpret_cast<void**>(&p), sizeof(T) * count), "cudaMalloc");
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void upload(const T* src, size_t count, cudaStream_t s) {
+    cuda_check(cudaMemcpyAsync(p, src, sizeof(T) * count, cudaMemcpyHostToDevice, s), "H2D");
+  }
+  void download(T* dst, size_t count, cudaStream_t s) const {
+    cuda_check(cudaMemcpyAsync(dst, p, sizeof(T) * count, cudaMemcpyDeviceToHost, s), "D2H");
+  }
+  void zero(cudaStream_t s) {
+    if (n) cuda_check(cudaMemsetAsync(p, 0, sizeof(T) * n, s), "memset");
+  }
+};
+
+// Mesh geometry and topology resident in HBM.
+class DeviceMesh {
+ public:
+  explicit DeviceMesh(std::shared_ptr<const Mesh> mesh, cudaStream_t s);
+  const Mesh& host() const { return *mesh_; }
+  std::shared_ptr<const Mesh> host_ptr() const { return mesh_; }
+  DevMesh view() const { return view_; }  // stiffness fields are filled by DeviceLaplacian::view()
+
+  DevBuf<double> px, py, pz;
+  DevBuf<long long> fx, fy, fz;
+  DevBuf<unsigned> faces, edges;
+  DevBuf<int> c_off, c_col, n_off, n_col, f_off, f_col;  // front connectivity, neighbours, v2f
+
+ private:
+  std::shared_ptr<const Mesh> mesh_;
+  DevMesh view_;
+};
+
+// Cotangent stiffness + lumped masses (operators.hpp LaplacianOperator).
+class DeviceLaplacian {
+ public:
+  // Assembled on the device from the mesh.
+  DeviceLaplacian(std::shared_ptr<DeviceMesh> dm, cudaStream_t s);
+  // From a host CSR (e.g. the reference's own operator) -- for parity tests.
+  DeviceLaplacian(std::shared_ptr<DeviceMesh> dm, const std::vector<int>& off, const std::vector<int>& col,
+                  const std::vector<double>& val, const std::vector<double>& mass, double gershgorin, cudaStream_t s);
+  int nnz() const { return nnz_; }
+  double gershgorin() const { return gersh_; }
+  void download(std::vector<int>& off, std::vector<int>& col, std::vector<double>& val, std::vector<double>& mass,
+                cudaStream_t s) const;
+  void apply(const double* x_host, double* y_host, cudaStream_t s) const;
+  std::shared_ptr<DeviceMesh> mesh() const { return dm_; }
+  DevMesh view() const;
+
+  DevBuf<int> off, col;
+  DevBuf<double> val, mass;
+
+ private:
+  std::shared_ptr<DeviceMesh> dm_;
+  int nnz_ = 0;
+  double gersh_ = 0;
+};
+
+struct Coefficients {  // layer_field.hpp CoefficientScheme
+  double gradient_energy = 1.0 / 25.0;
+  double penalty = 1.0 / 125.0;
+  double contact = 1.0 / 30.0;
+  double mobility = 0.25;
+};
+
+struct Config {  // diffusion.hpp DiffusionConfig
+  double dt = 0.0;
+  double band_low_threshold = 0.05;
+  double saturation = 0.999;
+  double collision_threshold = 0.1;
+  int check_interval = 1;
+  long max_steps = 200000;
+  double covered_threshold = 0.05;
+  double seed_radius = 0.0;
+  bool record_trails = true;
+  bool record_hashes = false;  // per-check field digests (parity tooling)
+  std::function<void(long)> on_check;  // host hook; forces a host round trip per check
+  void validate() const;
+};
+
+double stable_time_step(const DeviceLaplacian& op, const Coefficients& c);
+std::vector<Index> seed_region(const Mesh& mesh, Index seed, double radius);
+
+struct LoopPoint {
+  V3 position;
+  Index face = kInvalid, edge = kInvalid, vertex = kInvalid;
+  double edge_t = 0.0;
+};
+struct SurfaceLoop {
+  std::vector<LoopPoint> points;
+  bool closed = true;
+  double length() const;
+  V3 centroid() const;
+};
+
+struct FrontComponent {
+  Index layer = kInvalid;
+  std::vector<Index> triangles, boundary_vertices;
+  double band_length = 0;
+};
+
+enum class EventKind { Seed = 0, Split = 1, Merge = 2, Vanish = 3 };
+
+struct HandleEstimate {
+  SurfaceLoop loop;
+  Index layer = kInvalid;
+  std::vector<std::pair<Index, double>> field_snapshot;  // sorted by vertex
+  Index event_index = kInvalid;
+};
+
+struct TopologyEvent {
+  EventKind kind;
+  long step = 0;
+  std::vector<Index> layers, produced;
+  V3 position{};
+  std::vector<HandleEstimate> estimates;
+  std::vector<Index> covered_snapshot;
+};
+
+struct LayerTrack {
+  Index layer = kInvalid, created_event = kInvalid, consumed_event = kInvalid;
+  std::vector<V3> trail;
+};
+
+struct LayerMeta {
+  bool active = false, cleared = false;
+  Index parent = kInvalid;
+  std::vector<Index> merge_parents;
+  long created_step = 0;
+};
+
+// The dynamic layer matrix Phi, resident on the device as per-vertex columns.
+class DeviceField {
+ public:
+  DeviceField(std::shared_ptr<DeviceMesh> dm, cudaStream_t s);
+  // init_field (layer_field.hpp:318): base + one seed layer.
+  void init(const std::vector<Index>& seeds);
+
+  int layer_count() const { return static_cast<int>(meta_.size()); }
+  const LayerMeta& meta(Index id) const { return meta_[id]; }
+  std::vector<Index> active_nonbase() const;
+  void sync_active();  // upload active flags / dense indices
+
+  std::vector<std::pair<Index, double>> layer_values(Index layer) const;  // sorted by vertex
+  std::vector<double> dense_row(Index layer) const;
+  std::vector<Index> covered_set(double threshold) const;
+  unsigned long long hash() const;
+  void normalize_columns();
+  std::vector<Index> split_layer(Index layer, const std::vector<std::vector<Index>>& comps, long step);
+  Index merge_layers(const std::vector<Index>& ids, long step, std::vector<int>* touched = nullptr);
+  void set_inactive(Index layer);
+  bool finished(Index layer, int nunsat) const;  // diffusion.hpp:795
+  int base_one_count() const;
+
+  DevField view() const { return view_; }
+  DevWork work() const { return work_; }
+  DeviceMesh& mesh() { return *dm_; }
+  const DeviceMesh& mesh() const { return *dm_; }
+  cudaStream_t stream() const { return s_; }
+  Ctl read_ctl() const;
+  // Queues verts and their stiffness rows as the frontier of step stamp+1.
+  void mark_region(const DevMesh& op_view, const std::vector<int>& verts, long stamp, int parity);
+  double prune_epsilon = 1e-9;
+  // Vertices logged by split/merge edits since the last take (change log).
+  std::vector<int> pending_moved;
+
+  // storage
+  DevBuf<unsigned char> cnt, interest, scnt, sflag, active;
+  DevBuf<unsigned short> lay, slay;
+  DevBuf<double> val, sval, lastpos;
+  DevBuf<int> region0, region1, stamp, ilist, aidx, alist, pairs_scratch;
+  DevBuf<unsigned long long> parent, pair_keys, hashes;
+  DevBuf<unsigned> pairs;
+  DevBuf<LayerStat> stat;
+  DevBuf<TrailRec> trail;
+  DevBuf<Ctl> ctl;
+
+ private:
+  std::shared_ptr<DeviceMesh> dm_;
+  cudaStream_t s_;
+  std::vector<LayerMeta> meta_;
+  DevField view_;
+  DevWork work_;
+};
+
+struct InitialPassResult {
+  std::vector<TopologyEvent> events;
+  std::vector<LayerTrack> tracks;
+  double dt_used = 0;
+  long steps = 0;
+  Index seed_vertex = 0;
+  int status = 0;  // ErrorCode (0 ok)
+  std::string message;
+  std::vector<unsigned long long> hashes;  // per check step (if recorded)
+  std::shared_ptr<DeviceField> field;
+  long handle_estimate_count() const;
+  // Timing breakdown (seconds): device step loop vs. host event handling.
+  double t_device = 0, t_events = 0;
+  long launches = 0, event_checks = 0, kernel_steps = 0;
+};
+
+// extract_front (diffusion.hpp:398) on host data pulled from the device.
+std::vector<FrontComponent> extract_front(const DeviceField& field, Index layer, const Config& cfg);
+// detect_collisions (diffusion.hpp:475) via the device check kernel.
+std::vector<std::vector<Index>> detect_collisions(DeviceField& field, const Config& cfg);
+// One explicit Euler update of the whole field (diffusion.hpp:386).
+void step(DeviceField& field, const DeviceLaplacian& op, const Config& cfg, const Coefficients& c);
+// extract_isoline (isoline.hpp:55) of a host value array.
+std::vector<SurfaceLoop> extract_isoline(const Mesh& mesh, const std::vector<double>& values, double level);
+
+InitialPassResult run_initial_pass(std::shared_ptr<DeviceMesh> dm, const DeviceLaplacian& op, Index seed,
+                                   const Config& cfg, const Coefficients& c = {});
+
+// Reeb graph from the event log (SPEC reeb.build_reeb; nodes = events, arcs =
+// layer lifetimes, embedding = the layer trails).
+struct ReebGraph {
+  struct Node {
+    EventKind kind;
+    V3 position;
+    long step;
+  };
+  struct Arc {
+    Index from, to, layer;
+    std::vector<V3> embedding;
+  };
+  std::vector<Node> nodes;
+  std::vector<Arc> arcs;
+  long cycle_rank() const { return static_cast<long>(arcs.size()) - static_cast<long>(nodes.size()) + 1; }
+};
+ReebGraph build_reeb(const InitialPassResult& r);
+
+}  // namespace dtb

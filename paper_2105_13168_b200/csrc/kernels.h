@@ -1,0 +1,192 @@
+// Device data layout and kernel launchers for the diffusion-front engine.
+//
+// HBM layout:
+//   * mesh: SoA positions (3 x f64), fixed-point positions (3 x i64, for
+//     order-independent band sums), faces (3 x u32), edges (2 x u32),
+//     stiffness CSR (i32 offsets / i32 columns / f64 values), lumped masses,
+//     the front-connectivity CSR (mesh neighbours plus the apexes opposite each
+//     link edge) and the mesh neighbour CSR.
+//   * field: the transposed layer matrix Phi^T as fixed-capacity columns -- per
+//     vertex a count (u8) and kSlots (layer id u16, value f64) pairs sorted by
+//     layer id.  Column v holds exactly the reference's owners_[v] list
+//     (layer_field.hpp:310) with the values of layers_[id].values[v].
+//   * work: double-buffered region lists (the reference's one-ring-dilated
+//     frontier, diffusion.hpp:253-271) with per-vertex stamps, per-region-slot
+//     scratch columns, the "interest" flags/list (vertices holding any value
+//     strictly inside (0,1)), versioned union-find parents per (vertex, slot),
+//     per-active-layer statistics and the collision pair set.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+namespace dtb {
+
+constexpr int kSlots = 16;         // max owners per vertex (column capacity)
+constexpr int kMaxLayers = 65535;  // layer ids are u16
+constexpr int kMaxActive = 4096;   // simultaneously active non-base layers
+constexpr int kPairCap = 1 << 16;  // collision pair hash table slots
+constexpr int kTrailCap = 1 << 20; // device trail ring capacity (records)
+constexpr int kBlock = 256;        // threads per CTA for all engine kernels
+
+// Error codes raised by device code (mirrored in mesh.hpp ErrorCode).
+enum DevError : int {
+  kDevOk = 0,
+  kDevBlowup = 10,    // NumericalBlowup (diffusion.hpp:315)
+  kDevZeroColumn = 7, // ZeroColumn (layer_field.hpp:148)
+  kDevCapacity = 101, // column or candidate capacity exceeded
+};
+
+// Stop reasons of the persistent step kernel.
+enum StopBits : int {
+  kStopNone = 0,
+  kStopSplit = 1,      // some active layer has >= 2 band components
+  kStopMerge = 2,      // a collision pair exists
+  kStopVanish = 4,     // some active layer has no band and no unsaturated value
+  kStopExtinct = 8,    // base layer extinct (diffusion.hpp:785)
+  kStopError = 16,     // device error (see ctl.error)
+  kStopEveryCheck = 32 // host requested a stop at every check (on_check hook)
+};
+
+struct DevMesh {
+  int nv = 0, nf = 0, ne = 0;
+  const double *px = nullptr, *py = nullptr, *pz = nullptr;
+  const long long *fx = nullptr, *fy = nullptr, *fz = nullptr;  // fixed-point positions
+  double fx_scale = 1.0;                                          // 2^-k
+  const unsigned *faces = nullptr;                                // 3 * nf
+  const unsigned *edges = nullptr;                                // 2 * ne (lo, hi)
+  const int *s_off = nullptr, *s_col = nullptr;                   // stiffness CSR
+  const double *s_val = nullptr, *mass = nullptr;
+  const int *c_off = nullptr, *c_col = nullptr;                   // front connectivity
+  const int *n_off = nullptr, *n_col = nullptr;                   // mesh neighbours
+};
+
+// Control block in device memory (one per engine).
+struct Ctl {
+  int rcount[2];             // region list sizes (parity = step & 1)
+  int icount;                // interest list size
+  int error;                 // DevError
+  int error_vertex;
+  int stop_bits;
+  long long stop_step;       // last step executed by the kernel
+  long long epoch;           // union-find / pair-set version
+  int base_one;              // number of vertices whose base value is exactly 1.0
+  int pad0;
+  unsigned long long base_max_bits;  // max base value in (0,1) (as ordered bits)
+  int npairs;                // collision pairs recorded this check
+  int pair_overflow;
+  int ntrail;                // trail records written (ring index)
+  int trail_pending;         // a snap for the previous check step is outstanding
+  long long trail_step;      // step of the pending snap
+  unsigned bar_count;        // grid barrier
+  unsigned bar_gen;
+  unsigned long long hash_acc;  // field digest accumulator
+};
+
+struct LayerStat {
+  int ncomp, nband, nunsat, pad;
+  long long sx, sy, sz;           // fixed-point band position sums
+  unsigned long long snap;        // packed (distance bits | vertex) argmin
+};
+
+struct TrailRec {
+  long long step;
+  int layer, vertex;
+  double mx, my, mz;  // band mean (last_band_position_)
+};
+
+struct DevField {
+  unsigned char *cnt = nullptr;   // nv
+  unsigned short *lay = nullptr;  // nv * kSlots
+  double *val = nullptr;          // nv * kSlots
+  unsigned char *interest = nullptr;
+};
+
+struct DevWork {
+  int *region[2] = {nullptr, nullptr};  // region lists
+  int *stamp = nullptr;                 // per vertex: step whose advance queued it
+  unsigned char *scnt = nullptr;        // scratch columns per region slot
+  unsigned short *slay = nullptr;
+  double *sval = nullptr;
+  unsigned char *sflag = nullptr;
+  int *ilist = nullptr;                 // interest list
+  unsigned long long *parent = nullptr; // nv * kSlots versioned UF parents
+  unsigned char *active = nullptr;      // kMaxLayers + 1
+  int *aidx = nullptr;                  // layer -> dense active index or -1
+  int *alist = nullptr;                 // dense active index -> layer
+  LayerStat *stat = nullptr;            // kMaxActive
+  unsigned long long *pair_keys = nullptr;  // kPairCap versioned keys
+  unsigned *pairs = nullptr;            // recorded pairs (first << 16 | second)
+  double *lastpos = nullptr;            // 4 * (kMaxLayers + 1): x, y, z, valid
+  TrailRec *trail = nullptr;            // kTrailCap
+  unsigned long long *hashes = nullptr; // per-step field digests (optional)
+  long long hash_base = 0;              // step of hashes[0]
+  int hash_cap = 0;
+  Ctl *ctl = nullptr;
+};
+
+struct StepParams {
+  double mu_n, m_mu_n, w, e, half_a2, dt, prune;
+  double band_lo, sat, kappa, coll_base_limit, extinct_limit;
+  long long step_begin, step_end;  // execute steps [step_begin, step_end)
+  int check_interval;
+  int n_active;
+  int record_trails;
+  int do_hash;
+  int stop_every_check;
+  int do_check;  // 0: advance only (one-shot step())
+};
+
+// --- launchers (kernels.cu) -------------------------------------------------
+// All return a cudaError_t value as int.
+int dev_max_coresident_blocks(int* out);
+int launch_run(const DevMesh& m, const DevField& f, const DevWork& w, const StepParams& p, int blocks,
+               void* stream);
+int launch_check(const DevMesh& m, const DevField& f, const DevWork& w, const StepParams& p, int blocks,
+                 void* stream);  // stats/CCL/collisions for the current state (no advance)
+int launch_snap(const DevMesh& m, const DevField& f, const DevWork& w, const StepParams& p, void* stream);
+// Writes trail / last-position records of the last check (step = p.step_begin) and resets the stats.
+int launch_flush(const DevMesh& m, const DevField& f, const DevWork& w, const StepParams& p, void* stream);
+
+// Laplacian assembly (laplacian.cu).
+struct LapBuild {
+  int nv, nf;
+  const double *px, *py, *pz;
+  const unsigned* faces;
+  const int *v2v_off, *v2v;    // sorted mesh neighbours (CSR)
+  const int *v2f_off, *v2f;    // incident faces in face order (CSR)
+  int *s_off;                  // out: nv + 1
+  int *s_col;                  // out: capacity nv + 2 * ne
+  double *s_val;               // out
+  double *mass;                // out
+  double *gersh_row;           // out: per-row bound (max reduced on host)
+  int *nnz;                    // out
+};
+int launch_assemble(const LapBuild& b, void* stream);
+int launch_spmv(int nv, const int* off, const int* col, const double* val, const double* mass,
+                const double* x, double* y, void* stream);
+
+// Field edit / query helpers (fieldops.cu).
+int launch_init_field(const DevField& f, const DevWork& w, int nv, const int* seeds, int nseeds,
+                      void* stream);
+int launch_mark_region(const DevMesh& m, const DevWork& w, const int* verts, int n, long long stamp,
+                       int parity, void* stream);
+int launch_mark_all_support(const DevMesh& m, const DevField& f, const DevWork& w, long long stamp,
+                            int parity, void* stream);
+int launch_pull_layer(const DevField& f, int nv, int layer, int* out_v, double* out_x, int* out_n,
+                      void* stream);
+int launch_relabel(const DevField& f, const DevWork& w, const int* verts, const int* newlayer, int n,
+                   int oldlayer, void* stream);
+int launch_merge(const DevField& f, const DevWork& w, int nv, const int* group, int ngroup, int result,
+                 int* touched, int* ntouched, void* stream);
+int launch_covered(const DevField& f, int nv, double threshold, int* out_v, int* out_n, void* stream);
+int launch_crossings(const DevMesh& m, const DevField& f, int layer, double level, int* out_e,
+                     double* out_t, double* out_ba, double* out_bb, int* out_n, void* stream);
+int launch_finished(const DevMesh& m, const DevField& f, int layer, double prune, int* out_flag,
+                    void* stream);
+int launch_field_hash(const DevField& f, int nv, unsigned long long* out, void* stream);
+int launch_normalize_all(const DevField& f, const DevWork& w, int nv, double prune, void* stream);
+int launch_dense_row(const DevField& f, int nv, int layer, double* out, void* stream);
+int launch_base_one_count(const DevField& f, int nv, int* out, void* stream);
+
+}  // namespace dtb

@@ -1,0 +1,176 @@
+// Cotangent-Laplacian assembly on the device (reference: operators.hpp:33-70).
+//
+// One thread per vertex builds its stiffness row directly in CSR form: the
+// sorted column set {v} U N(v), off-diagonal (v,u) = sum over the two faces of
+// edge vu of 0.5 * cot(opposite angle), diagonal = -sum of the incident
+// half-weights, entries that sum to exactly zero dropped (from_triplets with
+// drop tolerance 0, sparse.hpp:50).  Off-diagonal sums have two terms and are
+// therefore bit-identical to the reference's sort-then-sum; the diagonal sums
+// 2*deg terms in face order, which can differ from the reference's
+// std::sort-dependent order in the last bits (tests bound it by 8 ulp).
+// Lumped masses accumulate face areas / 3 in face order exactly like the
+// reference's sequential loop, so they are bit-identical.
+#include <cuda_runtime.h>
+
+#include <cub/cub.cuh>
+
+#include "kernels.h"
+
+namespace dtb {
+
+namespace {
+
+struct P3 {
+  double x, y, z;
+};
+__device__ __forceinline__ P3 sub(P3 a, P3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ double dot3(P3 a, P3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ P3 cross3(P3 a, P3 b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+__device__ __forceinline__ P3 pos(const LapBuild& b, unsigned v) { return {b.px[v], b.py[v], b.pz[v]}; }
+
+// Half cotangent weight of edge (a, b) inside face with apex c.
+__device__ __forceinline__ double half_cot(const LapBuild& B, unsigned a, unsigned b, unsigned c, bool& bad) {
+  const P3 pc = pos(B, c);
+  const P3 ca = sub(pos(B, a), pc), cb = sub(pos(B, b), pc);
+  const double cot = dot3(ca, cb) / sqrt(dot3(cross3(ca, cb), cross3(ca, cb)));
+  if (!isfinite(cot)) bad = true;
+  return 0.5 * cot;
+}
+
+// Off-diagonal value of (v, u): the two incident faces' half weights.
+__device__ double offdiag(const LapBuild& B, int v, int u, bool& bad) {
+  double sum = 0.0;
+  for (int q = B.v2f_off[v]; q < B.v2f_off[v + 1]; ++q) {
+    const int f = B.v2f[q];
+    const unsigned t0 = B.faces[3 * f], t1 = B.faces[3 * f + 1], t2 = B.faces[3 * f + 2];
+    unsigned c;
+    if ((t0 == (unsigned)v && t1 == (unsigned)u) || (t1 == (unsigned)v && t0 == (unsigned)u)) c = t2;
+    else if ((t1 == (unsigned)v && t2 == (unsigned)u) || (t2 == (unsigned)v && t1 == (unsigned)u)) c = t0;
+    else if ((t2 == (unsigned)v && t0 == (unsigned)u) || (t0 == (unsigned)v && t2 == (unsigned)u)) c = t1;
+    else continue;
+    sum = sum + half_cot(B, (unsigned)v, (unsigned)u, c, bad);
+  }
+  return sum;
+}
+
+// Diagonal: -w for each (face, corner-edge) incident to v, faces in order,
+// corner edges k = 0, 1, 2 within a face (the reference's triplet order before
+// its sort).
+__device__ double diagonal(const LapBuild& B, int v, bool& bad) {
+  double sum = 0.0;
+  for (int q = B.v2f_off[v]; q < B.v2f_off[v + 1]; ++q) {
+    const int f = B.v2f[q];
+    const unsigned t[3] = {B.faces[3 * f], B.faces[3 * f + 1], B.faces[3 * f + 2]};
+    for (int k = 0; k < 3; ++k) {
+      const unsigned a = t[k], b = t[(k + 1) % 3], c = t[(k + 2) % 3];
+      if (a != (unsigned)v && b != (unsigned)v) continue;
+      sum = sum + (-half_cot(B, a, b, c, bad));
+    }
+  }
+  return sum;
+}
+
+__global__ void k_row_count(LapBuild B, int* counts, int* bad_flag) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= B.nv) return;
+  bool bad = false;
+  int n = 0;
+  if (diagonal(B, v, bad) != 0.0) ++n;
+  for (int q = B.v2v_off[v]; q < B.v2v_off[v + 1]; ++q)
+    if (offdiag(B, v, B.v2v[q], bad) != 0.0) ++n;
+  counts[v] = n;
+  if (bad) atomicExch(bad_flag, 1);
+}
+
+__global__ void k_row_fill(LapBuild B) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= B.nv) return;
+  bool bad = false;
+  const double d = diagonal(B, v, bad);
+  int o = B.s_off[v];
+  bool diag_done = false;
+  double gersh = 0.0;
+  auto emit = [&](int c, double x) {
+    B.s_col[o] = c;
+    B.s_val[o] = x;
+    ++o;
+    gersh = gersh + fabs(x);
+  };
+  for (int q = B.v2v_off[v]; q < B.v2v_off[v + 1]; ++q) {
+    const int u = B.v2v[q];
+    if (!diag_done && u > v) {
+      if (d != 0.0) emit(v, d);
+      diag_done = true;
+    }
+    const double w = offdiag(B, v, u, bad);
+    if (w != 0.0) emit(u, w);
+  }
+  if (!diag_done && d != 0.0) emit(v, d);
+  // Lumped mass: area / 3 of every incident face, in face order.
+  double m = 0.0;
+  for (int q = B.v2f_off[v]; q < B.v2f_off[v + 1]; ++q) {
+    const int f = B.v2f[q];
+    const P3 p0 = pos(B, B.faces[3 * f]), p1 = pos(B, B.faces[3 * f + 1]), p2 = pos(B, B.faces[3 * f + 2]);
+    const P3 n = cross3(sub(p1, p0), sub(p2, p0));
+    const double area = 0.5 * sqrt(dot3(n, n));
+    m = m + area / 3.0;
+  }
+  B.mass[v] = m;
+  B.gersh_row[v] = gersh / m;
+}
+
+__global__ void k_spmv(int nv, const int* off, const int* col, const double* val, const double* mass, const double* x,
+                       double* y) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  double acc = 0.0;
+  for (int k = off[v]; k < off[v + 1]; ++k) acc = acc + val[k] * x[col[k]];
+  y[v] = acc / mass[v];
+}
+
+}  // namespace
+
+// Returns cudaSuccess, or -1 when a cotangent weight is non-finite
+// (DegeneracyError, operators.hpp:48).
+int launch_assemble(const LapBuild& b, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int threads = 128, blocks = (b.nv + threads - 1) / threads;
+  int* counts = nullptr;
+  int* bad = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&counts), sizeof(int) * (b.nv + 1), s);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  e = cudaMallocAsync(reinterpret_cast<void**>(&bad), sizeof(int), s);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  cudaMemsetAsync(bad, 0, sizeof(int), s);
+  cudaMemsetAsync(counts + b.nv, 0, sizeof(int), s);
+  k_row_count<<<blocks, threads, 0, s>>>(b, counts, bad);
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, b.s_off, b.nv + 1, s);
+  void* tmp = nullptr;
+  cudaMallocAsync(&tmp, tmp_bytes, s);
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, b.s_off, b.nv + 1, s);
+  k_row_fill<<<blocks, threads, 0, s>>>(b);
+  cudaMemcpyAsync(b.nnz, b.s_off + b.nv, sizeof(int), cudaMemcpyDeviceToDevice, s);
+  int hbad = 0;
+  cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(tmp, s);
+  cudaFreeAsync(counts, s);
+  cudaFreeAsync(bad, s);
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return static_cast<int>(e);
+  return hbad ? -1 : 0;
+}
+
+int launch_spmv(int nv, const int* off, const int* col, const double* val, const double* mass, const double* x,
+                double* y, void* stream) {
+  const int threads = 256;
+  k_spmv<<<(nv + threads - 1) / threads, threads, 0, static_cast<cudaStream_t>(stream)>>>(nv, off, col, val, mass, x,
+                                                                                           y);
+  return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace dtb

@@ -1,0 +1,56 @@
+"""Device engine vs. the compiled reference (oracle/_ref) on the same inputs.
+
+Bit-exact: stiffness off-diagonals, masses, every field value after every step
+(64-bit field digests per check), event logs, loop anchors, covered sets and
+estimate snapshots.  Tolerance-bounded: stiffness diagonals (8 ulp, summation
+order of the reference's std::sort is not reproducible) and vanish positions
+(fixed-point device band means, 1e-9)."""
+import numpy as np
+import pytest
+
+import paper_2105_13168_b200 as dt
+from tests import parity, refdata
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not refdata.have_ref(), reason="oracle/_ref not built")]
+
+SMALL = ["icosphere:3:2.0", "torus:32:16:2:0.5", "genus:1:2", "genus:2:2", "torus_irr:32:16:2:0.5:0.3:0.05:7"]
+
+
+def ref_operator(mesh, spec):
+    L = refdata.ref_laplacian(spec)
+    return dt.LaplacianOperator.from_csr(mesh, L["off"], L["col"], L["val"], L["mass"], L["gershgorin"]), L
+
+
+@pytest.mark.parametrize("spec", SMALL + ["limbstar:3:3:4", "coin:8:24:3:1"])
+def test_laplacian_assembly(spec):
+    mesh = dt.TriangleMesh.generate(spec)
+    op = dt.assemble_laplacian(mesh)
+    off, col, val, mass = op.csr()
+    L = refdata.ref_laplacian(spec)
+    assert np.array_equal(off, L["off"]) and np.array_equal(col, L["col"])
+    assert np.array_equal(mass.view(np.uint64), L["mass"].view(np.uint64))
+    rows = np.repeat(np.arange(len(off) - 1), np.diff(off))
+    diag = rows == col
+    assert np.array_equal(val[~diag].view(np.uint64), L["val"][~diag].view(np.uint64))
+    ulp = np.abs(val[diag].view(np.int64) - L["val"][diag].view(np.int64))
+    assert ulp.max() <= 8, ulp.max()
+    assert op.gershgorin_bound == pytest.approx(L["gershgorin"], rel=1e-14)
+
+
+@pytest.mark.parametrize("spec,steps", [(s, 300) for s in SMALL])
+def test_initial_pass_bit_exact(spec, steps):
+    mesh = dt.TriangleMesh.generate(spec)
+    op, _ = ref_operator(mesh, spec)
+    cfg = dt.default_config(max_steps=steps, record_hashes=1)
+    res = dt.run_initial_pass(mesh, op, 0, cfg)
+    ref = refdata.ref_run(spec, max_steps=steps)
+    assert res.status == ("ok" if ref["status"] == "ok" else ref["error_type"])
+    assert res.steps == ref["steps"]
+    mine = [int(h) for h in res.hashes()]
+    theirs = [int(h) for h in ref["hashes"]]
+    assert len(mine) == len(theirs)
+    first_bad = next((i for i, (a, b) in enumerate(zip(mine, theirs)) if a != b), None)
+    assert first_bad is None, f"field digest diverges at check {first_bad + 1}"
+    parity.compare_events(res.events(), ref["events"])
+    exact, total = parity.compare_tracks(res.tracks(), ref["tracks"])
+    assert total == 0 or exact / total > 0.9, (exact, total)
