@@ -137,6 +137,14 @@ int dtb_result_field_hash(const dtb_result* r, uint64_t* hash);
 int dtb_result_hashes(const dtb_result* r, uint64_t* out, int64_t cap, int64_t* n);
 int dtb_result_timing(const dtb_result* r, double* t_device, double* t_events, int64_t* launches,
                       int64_t* event_checks, int64_t* kernel_steps);
+/* Device work counters (frontier vertices updated, band vertices checked, summed over steps) and the
+ * CUDA-event duration of the whole pass on its stream and of its step-kernel launches, in seconds. */
+int dtb_result_work(const dtb_result* r, uint64_t* sum_region, uint64_t* sum_interest, double* t_pass_device,
+                    double* t_kernel);
+/* Kernels launched by this library so far (process-wide counter). */
+unsigned long long dtb_launch_count(void);
+/* Bytes the mesh's device copy occupies (the H2D volume of uploading it). */
+int dtb_mesh_device_bytes(const dtb_mesh* m, uint64_t* bytes);
 /* build_reeb (SPEC reeb): nodes = events, arcs = layer lifetimes. */
 int dtb_result_reeb(const dtb_result* r, int64_t* n_nodes, int64_t* n_arcs, int64_t* cycle_rank);
 int dtb_result_reeb_arcs(const dtb_result* r, uint32_t* from, uint32_t* to, uint32_t* layer);

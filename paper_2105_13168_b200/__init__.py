@@ -110,6 +110,9 @@ def load_library(path: str = LIB_PATH):
         "dtb_result_hashes": (C.c_int, [P, pU64, I64, pI64]),
         "dtb_result_timing": (C.c_int, [P, pD, pD, pI64, pI64, pI64]),
         "dtb_result_reeb": (C.c_int, [P, pI64, pI64, pI64]),
+        "dtb_result_work": (C.c_int, [P, pU64, pU64, pD, pD]),
+        "dtb_launch_count": (C.c_ulonglong, []),
+        "dtb_mesh_device_bytes": (C.c_int, [P, pU64]),
         "dtb_result_reeb_arcs": (C.c_int, [P, pU32, pU32, pU32]),
         "dtb_field_init": (C.c_int, [P, pU32, U32, pP]),
         "dtb_field_free": (None, [P]),
@@ -165,6 +168,10 @@ def default_coefficients(**overrides) -> Coefficients:
     return c
 
 
+def launch_count() -> int:
+    return int(load_library().dtb_launch_count())
+
+
 def device_info():
     lib = load_library()
     n, sms, ma, mi = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
@@ -203,6 +210,11 @@ class TriangleMesh:
         h = C.c_void_p()
         _check(lib.dtb_mesh_load(path.encode(), fmt, C.byref(h)))
         return cls(h)
+
+    def device_bytes(self) -> int:
+        b = C.c_uint64()
+        _check(_lib.dtb_mesh_device_bytes(self._h, C.byref(b)))
+        return b.value
 
     def save(self, path: str):
         _check(_lib.dtb_mesh_save(self._h, path.encode()))
@@ -456,8 +468,11 @@ class InitialPassResult:
     def timing(self):
         td, te, la, ec, ks = C.c_double(), C.c_double(), C.c_int64(), C.c_int64(), C.c_int64()
         _check(_lib.dtb_result_timing(self._h, C.byref(td), C.byref(te), C.byref(la), C.byref(ec), C.byref(ks)))
+        sr, si, tp, tk = C.c_uint64(), C.c_uint64(), C.c_double(), C.c_double()
+        _check(_lib.dtb_result_work(self._h, C.byref(sr), C.byref(si), C.byref(tp), C.byref(tk)))
         return {"t_device": td.value, "t_events": te.value, "launches": la.value, "event_checks": ec.value,
-                "kernel_steps": ks.value}
+                "kernel_steps": ks.value, "sum_region": sr.value, "sum_interest": si.value,
+                "t_pass_device": tp.value, "t_kernel": tk.value}
 
     def reeb(self):
         nn, na, rank = C.c_int64(), C.c_int64(), C.c_int64()

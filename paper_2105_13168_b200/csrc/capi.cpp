@@ -518,6 +518,29 @@ int dtb_result_hashes(const dtb_result* r, uint64_t* out, int64_t cap, int64_t* 
   });
 }
 
+unsigned long long dtb_launch_count(void) { return launch_count(); }
+
+int dtb_mesh_device_bytes(const dtb_mesh* m, uint64_t* bytes) {
+  return guard([&] {
+    need(m, "mesh");
+    need(bytes, "bytes");
+    const DeviceMesh& d = m->device();
+    *bytes = 8 * (d.px.n + d.py.n + d.pz.n + d.fx.n + d.fy.n + d.fz.n) + 4 * (d.faces.n + d.edges.n) +
+             4 * (d.c_off.n + d.c_col.n + d.n_off.n + d.n_col.n + d.f_off.n + d.f_col.n);
+  });
+}
+
+int dtb_result_work(const dtb_result* r, uint64_t* sum_region, uint64_t* sum_interest, double* t_pass_device,
+                    double* t_kernel) {
+  return guard([&] {
+    need(r, "result");
+    if (t_kernel) *t_kernel = r->r.t_kernel;
+    if (t_pass_device) *t_pass_device = r->r.t_pass_device;
+    if (sum_region) *sum_region = r->r.sum_region;
+    if (sum_interest) *sum_interest = r->r.sum_interest;
+  });
+}
+
 int dtb_result_timing(const dtb_result* r, double* td, double* te, int64_t* launches, int64_t* checks,
                       int64_t* ksteps) {
   return guard([&] {

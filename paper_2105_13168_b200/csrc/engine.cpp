@@ -370,7 +370,40 @@ std::vector<SurfaceLoop> extract_isoline(const Mesh& mesh, const std::vector<dou
 // ---------------------------------------------------------------------------
 // DeviceField
 
-DeviceField::DeviceField(std::shared_ptr<DeviceMesh> dm, cudaStream_t s) : dm_(std::move(dm)), s_(s) {
+DeviceField::DeviceField(std::shared_ptr<DeviceMesh> dm, cudaStream_t s) : dm_(dm.get()), keep_(std::move(dm)), s_(s) {
+  setup();
+}
+DeviceField::DeviceField(DeviceMesh* dm, cudaStream_t s) : dm_(dm), s_(s) { setup(); }
+
+DeviceMesh::~DeviceMesh() {
+  for (DeviceField* f : pool_) delete f;
+}
+
+std::shared_ptr<DeviceField> DeviceMesh::acquire_field(cudaStream_t s) {
+  DeviceField* f = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(pool_mu_);
+    if (!pool_.empty()) {
+      f = pool_.back();
+      pool_.pop_back();
+    }
+  }
+  if (!f) f = new DeviceField(this, s);
+  f->set_stream(s);
+  f->keep_ = shared_from_this();
+  std::weak_ptr<DeviceMesh> home = f->keep_;
+  return std::shared_ptr<DeviceField>(f, [home](DeviceField* p) {
+    if (auto m = home.lock()) {
+      p->keep_.reset();  // the pool must not own its mesh
+      std::lock_guard<std::mutex> lk(m->pool_mu_);
+      m->pool_.push_back(p);
+    } else {
+      delete p;
+    }
+  });
+}
+
+void DeviceField::setup() {
   const size_t nv = dm_->host().nv();
   cnt.alloc(nv);
   interest.alloc(nv);
@@ -439,6 +472,12 @@ void DeviceField::init(const std::vector<Index>& seeds) {
   DevBuf<int> ds(sv.size());
   ds.upload(sv.data(), sv.size(), s_);
   ctl.zero(s_);
+  // Versioned union-find parents / pair keys restart at epoch 0, and a reused
+  // workspace may hold tags from an earlier pass: clear them.
+  parent.zero(s_);
+  pair_keys.zero(s_);
+  stat.zero(s_);
+  lastpos.zero(s_);
   ck(launch_init_field(view_, work_, static_cast<int>(nv), ds.p, static_cast<int>(sv.size()), s_), "init field");
   Ctl c{};
   c.base_one = static_cast<int>(nv - sv.size());
@@ -832,7 +871,12 @@ class PassEngine {
     cfg_.validate();
     if (seed >= mesh_.nv()) fail(kInvalidParameter, "seed vertex out of range");
     cuda_check(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "stream");
-    field_ = std::make_shared<DeviceField>(dm_, s_);
+    cuda_check(cudaEventCreate(&ev0_), "event");
+    cuda_check(cudaEventCreate(&ev1_), "event");
+    cuda_check(cudaEventCreate(&ev0k_), "event");
+    cuda_check(cudaEventCreate(&ev1k_), "event");
+    cuda_check(cudaEventRecord(ev0_, s_), "event record");
+    field_ = dm_->acquire_field(s_);
     res_.field = field_;
     res_.seed_vertex = seed;
     const double radius =
@@ -857,6 +901,10 @@ class PassEngine {
     blocks_ = engine_blocks(static_cast<int>(mesh_.nv()));
   }
   ~PassEngine() {
+    if (ev0_) cudaEventDestroy(ev0_);
+    if (ev1_) cudaEventDestroy(ev1_);
+    if (ev0k_) cudaEventDestroy(ev0k_);
+    if (ev1k_) cudaEventDestroy(ev1k_);
     if (s_) cudaStreamDestroy(s_);
   }
 
@@ -882,7 +930,17 @@ class PassEngine {
       res_.message = e.what();
     }
     res_.steps = step;
+    {
+      const Ctl c = field_->read_ctl();
+      res_.sum_region = c.sum_region;
+      res_.sum_interest = c.sum_interest;
+    }
     finish_tracks();
+    cuda_check(cudaEventRecord(ev1_, s_), "event record");
+    cuda_check(cudaEventSynchronize(ev1_), "event sync");
+    float ms = 0;
+    cuda_check(cudaEventElapsedTime(&ms, ev0_, ev1_), "elapsed");
+    res_.t_pass_device = ms * 1e-3;
     if (cfg_.record_hashes) {
       const size_t n = static_cast<size_t>(std::min(step, cfg_.max_steps));
       std::vector<unsigned long long> h = to_host(field_->hashes, n + 1, s_);
@@ -930,8 +988,13 @@ class PassEngine {
       }
       p.step_begin = begin;
       p.step_end = end;
+      cuda_check(cudaEventRecord(ev0k_, s_), "event record");
       ck(launch_run(op_.view(), field_->view(), work(), p, blocks_, s_), "engine launch");
+      cuda_check(cudaEventRecord(ev1k_, s_), "event record");
       cuda_check(cudaStreamSynchronize(s_), "engine sync");
+      float ms = 0;
+      cuda_check(cudaEventElapsedTime(&ms, ev0k_, ev1k_), "elapsed");
+      res_.t_kernel += ms * 1e-3;
       ++res_.launches;
       Ctl c = field_->read_ctl();
       drain_trails(c);
@@ -1239,6 +1302,7 @@ class PassEngine {
   Config cfg_;
   Coefficients co_;
   cudaStream_t s_ = nullptr;
+  cudaEvent_t ev0_ = nullptr, ev1_ = nullptr, ev0k_ = nullptr, ev1k_ = nullptr;
   std::shared_ptr<DeviceField> field_;
   InitialPassResult res_;
   std::vector<LayerTrack> tracks_;

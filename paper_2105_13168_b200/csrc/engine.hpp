@@ -7,6 +7,7 @@
 #include <functional>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -62,10 +63,16 @@ struct DevBuf {
   }
 };
 
-// Mesh geometry and topology resident in HBM.
-class DeviceMesh {
+class DeviceField;
+
+// Mesh geometry and topology resident in HBM.  Also pools the per-run field
+// workspaces (columns, frontier lists, union-find parents ...) so repeated
+// passes on one mesh do not re-allocate hundreds of MB.
+class DeviceMesh : public std::enable_shared_from_this<DeviceMesh> {
  public:
   explicit DeviceMesh(std::shared_ptr<const Mesh> mesh, cudaStream_t s);
+  ~DeviceMesh();
+  std::shared_ptr<DeviceField> acquire_field(cudaStream_t s);
   const Mesh& host() const { return *mesh_; }
   std::shared_ptr<const Mesh> host_ptr() const { return mesh_; }
   DevMesh view() const { return view_; }  // stiffness fields are filled by DeviceLaplacian::view()
@@ -78,6 +85,8 @@ class DeviceMesh {
  private:
   std::shared_ptr<const Mesh> mesh_;
   DevMesh view_;
+  std::mutex pool_mu_;
+  std::vector<DeviceField*> pool_;
 };
 
 // Cotangent stiffness + lumped masses (operators.hpp LaplacianOperator).
@@ -182,6 +191,7 @@ struct LayerMeta {
 class DeviceField {
  public:
   DeviceField(std::shared_ptr<DeviceMesh> dm, cudaStream_t s);
+  DeviceField(DeviceMesh* dm, cudaStream_t s);  // pooled (no ownership)
   // init_field (layer_field.hpp:318): base + one seed layer.
   void init(const std::vector<Index>& seeds);
 
@@ -206,6 +216,7 @@ class DeviceField {
   DeviceMesh& mesh() { return *dm_; }
   const DeviceMesh& mesh() const { return *dm_; }
   cudaStream_t stream() const { return s_; }
+  void set_stream(cudaStream_t s) { s_ = s; }
   Ctl read_ctl() const;
   // Queues verts and their stiffness rows as the frontier of step stamp+1.
   void mark_region(const DevMesh& op_view, const std::vector<int>& verts, long stamp, int parity);
@@ -225,7 +236,10 @@ class DeviceField {
   DevBuf<Ctl> ctl;
 
  private:
-  std::shared_ptr<DeviceMesh> dm_;
+  friend class DeviceMesh;
+  void setup();
+  DeviceMesh* dm_;
+  std::shared_ptr<DeviceMesh> keep_;  // keeps the mesh alive while the field is handed out
   cudaStream_t s_;
   std::vector<LayerMeta> meta_;
   DevField view_;
@@ -245,7 +259,10 @@ struct InitialPassResult {
   long handle_estimate_count() const;
   // Timing breakdown (seconds): device step loop vs. host event handling.
   double t_device = 0, t_events = 0;
+  double t_pass_device = 0;  // CUDA-event time of the whole pass on its stream
+  double t_kernel = 0;       // CUDA-event time of the persistent step-kernel launches
   long launches = 0, event_checks = 0, kernel_steps = 0;
+  unsigned long long sum_region = 0, sum_interest = 0;  // device work counters
 };
 
 // extract_front (diffusion.hpp:398) on host data pulled from the device.

@@ -271,12 +271,17 @@ __global__ void k_base_one(DevField F, int nv, int* out) {
 
 }  // namespace
 
-#define DTB_RET return static_cast<int>(cudaGetLastError())
+#define DTB_RET \
+  note_launch();  \
+  return static_cast<int>(cudaGetLastError())
 
 int launch_init_field(const DevField& f, const DevWork& w, int nv, const int* seeds, int nseeds, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   k_init<<<nblk(nv), T, 0, s>>>(f, w, nv);
-  if (nseeds) k_seed<<<nblk(nseeds), T, 0, s>>>(f, seeds, nseeds);
+  if (nseeds) {
+    k_seed<<<nblk(nseeds), T, 0, s>>>(f, seeds, nseeds);
+    note_launch();
+  }
   DTB_RET;
 }
 int launch_mark_region(const DevMesh& m, const DevWork& w, const int* verts, int n, long long stamp, int parity,

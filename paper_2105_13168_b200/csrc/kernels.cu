@@ -31,6 +31,8 @@
 
 namespace dtb {
 
+void note_launch(unsigned long long n);
+
 namespace {
 
 constexpr int kCand = 16;  // candidate layers gathered over one stiffness row
@@ -602,6 +604,7 @@ __global__ void __launch_bounds__(kBlock) k_engine(DevMesh M, DevField F, DevWor
     if (gtid == 0) {
       ctl->rcount[nxt] = 0;
       ctl->hash_acc = 0;
+      ctl->sum_region += static_cast<unsigned long long>(nR);
     }
     for (int i = gtid; i < nR; i += gsz) update_vertex(M, F, W, P, i, W.region[cur][i]);
     if (pend && P.record_trails) phase_snap(M, F, W, P);
@@ -632,6 +635,7 @@ __global__ void __launch_bounds__(kBlock) k_engine(DevMesh M, DevField F, DevWor
     // ---- E: statistics and collisions
     phase_stats(M, F, W, P, ep);
     grid_sync(ctl);
+    if (gtid == 0) ctl->sum_interest += static_cast<unsigned long long>(ctl->icount);
     if (P.do_hash && gtid == 0) {
       const long long slot = step - W.hash_base;
       if (slot >= 0 && slot < W.hash_cap) W.hashes[slot] = ctl->hash_acc;
@@ -669,11 +673,16 @@ int coop_launch(const void* fn, int blocks, const DevMesh& m, const DevField& f,
   DevWork ww = w;
   StepParams pp = p;
   void* args[] = {&mm, &ff, &ww, &pp};
+  note_launch();
   return static_cast<int>(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kBlock), args, 0,
                                                       static_cast<cudaStream_t>(stream)));
 }
 
 }  // namespace
+
+static unsigned long long g_launches = 0;
+unsigned long long launch_count() { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+void note_launch(unsigned long long n) { __atomic_fetch_add(&g_launches, n, __ATOMIC_RELAXED); }
 
 int dev_max_coresident_blocks(int* out) {
   int dev = 0, sms = 0, per = 0;
@@ -702,6 +711,7 @@ int launch_check(const DevMesh& m, const DevField& f, const DevWork& w, const St
 }
 
 int launch_snap(const DevMesh& m, const DevField& f, const DevWork& w, const StepParams& p, void* stream) {
+  note_launch();
   k_engine<2><<<148 * 4, kBlock, 0, static_cast<cudaStream_t>(stream)>>>(m, f, w, p);
   return static_cast<int>(cudaGetLastError());
 }
@@ -709,6 +719,7 @@ int launch_snap(const DevMesh& m, const DevField& f, const DevWork& w, const Ste
 int launch_flush(const DevMesh& m, const DevField& f, const DevWork& w, const StepParams& p, void* stream) {
   const int blocks = (p.n_active + kBlock - 1) / kBlock;
   if (blocks == 0) return 0;
+  note_launch();
   k_engine<3><<<blocks, kBlock, 0, static_cast<cudaStream_t>(stream)>>>(m, f, w, p);
   return static_cast<int>(cudaGetLastError());
 }

@@ -81,6 +81,8 @@ struct Ctl {
   unsigned bar_count;        // grid barrier
   unsigned bar_gen;
   unsigned long long hash_acc;  // field digest accumulator
+  unsigned long long sum_region;    // work counters: frontier vertices updated
+  unsigned long long sum_interest;  // interest (band) vertices checked
 };
 
 struct LayerStat {
@@ -138,6 +140,9 @@ struct StepParams {
 };
 
 // --- launchers (kernels.cu) -------------------------------------------------
+// Number of kernels this library has launched (all launchers increment it).
+unsigned long long launch_count();
+void note_launch(unsigned long long n = 1);
 // All return a cudaError_t value as int.
 int dev_max_coresident_blocks(int* out);
 int launch_run(const DevMesh& m, const DevField& f, const DevWork& w, const StepParams& p, int blocks,

@@ -146,6 +146,7 @@ int launch_assemble(const LapBuild& b, void* stream) {
   cudaMemsetAsync(bad, 0, sizeof(int), s);
   cudaMemsetAsync(counts + b.nv, 0, sizeof(int), s);
   k_row_count<<<blocks, threads, 0, s>>>(b, counts, bad);
+  note_launch(4);  // row count, two scan passes, row fill
   size_t tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, b.s_off, b.nv + 1, s);
   void* tmp = nullptr;
@@ -170,6 +171,7 @@ int launch_spmv(int nv, const int* off, const int* col, const double* val, const
   const int threads = 256;
   k_spmv<<<(nv + threads - 1) / threads, threads, 0, static_cast<cudaStream_t>(stream)>>>(nv, off, col, val, mass, x,
                                                                                            y);
+  note_launch();
   return static_cast<int>(cudaGetLastError());
 }
 

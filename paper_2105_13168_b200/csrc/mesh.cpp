@@ -547,7 +547,8 @@ Mesh gen_gyroid(int periods, int res, double level, double scale) {
     auto [it, fresh] = edge_vertex.try_emplace(key, static_cast<Index>(v.size()));
     if (fresh) {
       const double fa = val[a], fb = val[b];
-      const double t = fa / (fa - fb);
+      // Crossings are kept off the grid nodes so no triangle degenerates.
+      const double t = std::min(0.98, std::max(0.02, fa / (fa - fb)));
       auto coord = [&](std::size_t g) {
         const int k = static_cast<int>(g % N1), j = static_cast<int>((g / N1) % N1),
                   i = static_cast<int>(g / (static_cast<std::size_t>(N1) * N1));
