@@ -141,6 +141,9 @@ int dtb_result_timing(const dtb_result* r, double* t_device, double* t_events, i
  * CUDA-event duration of the whole pass on its stream and of its step-kernel launches, in seconds. */
 int dtb_result_work(const dtb_result* r, uint64_t* sum_region, uint64_t* sum_interest, double* t_pass_device,
                     double* t_kernel);
+/* Diagnostics: nanoseconds per grid barrier of the persistent engine (mode 0) or of
+ * cooperative_groups::grid_group::sync (mode 1) with `blocks` CTAs. */
+double dtb_bench_barrier(int blocks, int n, int mode);
 /* Kernels launched by this library so far (process-wide counter). */
 unsigned long long dtb_launch_count(void);
 /* Bytes the mesh's device copy occupies (the H2D volume of uploading it). */

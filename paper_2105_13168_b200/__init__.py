@@ -112,6 +112,7 @@ def load_library(path: str = LIB_PATH):
         "dtb_result_reeb": (C.c_int, [P, pI64, pI64, pI64]),
         "dtb_result_work": (C.c_int, [P, pU64, pU64, pD, pD]),
         "dtb_launch_count": (C.c_ulonglong, []),
+        "dtb_bench_barrier": (C.c_double, [C.c_int, C.c_int, C.c_int]),
         "dtb_mesh_device_bytes": (C.c_int, [P, pU64]),
         "dtb_result_reeb_arcs": (C.c_int, [P, pU32, pU32, pU32]),
         "dtb_field_init": (C.c_int, [P, pU32, U32, pP]),

@@ -8,6 +8,10 @@
 
 #include "engine.hpp"
 
+namespace dtb {
+double bench_barrier(int blocks, int n, int mode);
+}
+
 using namespace dtb;
 
 struct dtb_mesh {
@@ -519,6 +523,8 @@ int dtb_result_hashes(const dtb_result* r, uint64_t* out, int64_t cap, int64_t* 
 }
 
 unsigned long long dtb_launch_count(void) { return launch_count(); }
+
+double dtb_bench_barrier(int blocks, int n, int mode) { return bench_barrier(blocks, n, mode); }
 
 int dtb_mesh_device_bytes(const dtb_mesh* m, uint64_t* bytes) {
   return guard([&] {

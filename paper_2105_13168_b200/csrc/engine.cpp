@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <numeric>
 #include <queue>
@@ -67,86 +68,63 @@ V3 mean_of(const Mesh& m, const std::vector<Index>& verts) {
 DeviceMesh::DeviceMesh(std::shared_ptr<const Mesh> mesh, cudaStream_t s) : mesh_(std::move(mesh)) {
   const Mesh& m = *mesh_;
   const Index nv = m.nv(), nf = m.nf(), ne = m.ne();
-  std::vector<double> x(nv), y(nv), z(nv);
+  static_assert(sizeof(V3) == 24 && sizeof(std::array<Index, 3>) == 12 && sizeof(std::array<Index, 2>) == 8,
+                "packed host arrays are uploaded as-is");
   double maxabs = 1e-300;
-  for (Index v = 0; v < nv; ++v) {
-    x[v] = m.p(v).x;
-    y[v] = m.p(v).y;
-    z[v] = m.p(v).z;
-    maxabs = std::max({maxabs, std::abs(x[v]), std::abs(y[v]), std::abs(z[v])});
-  }
+  for (const V3& q : m.positions()) maxabs = std::max({maxabs, std::abs(q.x), std::abs(q.y), std::abs(q.z)});
   // Fixed point with |coord| * 2^k <= 2^38: band sums of up to 2^25 vertices
   // stay exact in int64 (order-independent device reductions).
   const int k = 38 - static_cast<int>(std::ceil(std::log2(maxabs)));
-  const double scale = std::ldexp(1.0, k);
-  std::vector<long long> qx(nv), qy(nv), qz(nv);
-  for (Index v = 0; v < nv; ++v) {
-    qx[v] = std::llrint(x[v] * scale);
-    qy[v] = std::llrint(y[v] * scale);
-    qz[v] = std::llrint(z[v] * scale);
-  }
+  // Host arrays go up unchanged; SoA / fixed-point positions and the
+  // front-connectivity CSR are derived on the device.
+  DevBuf<double> xyz(3 * static_cast<size_t>(nv));
+  xyz.upload(reinterpret_cast<const double*>(m.positions().data()), xyz.n, s);
   px.alloc(nv);
   py.alloc(nv);
   pz.alloc(nv);
   fx.alloc(nv);
   fy.alloc(nv);
   fz.alloc(nv);
-  px.upload(x.data(), nv, s);
-  py.upload(y.data(), nv, s);
-  pz.upload(z.data(), nv, s);
-  fx.upload(qx.data(), nv, s);
-  fy.upload(qy.data(), nv, s);
-  fz.upload(qz.data(), nv, s);
+  ck(launch_positions(xyz.p, static_cast<int>(nv), std::ldexp(1.0, k), px.p, py.p, pz.p, fx.p, fy.p, fz.p, s),
+     "positions");
   faces.alloc(3 * static_cast<size_t>(nf));
-  faces.upload(reinterpret_cast<const unsigned*>(m.faces().data()), 3 * static_cast<size_t>(nf), s);
-  std::vector<unsigned> ev(2 * static_cast<size_t>(ne));
-  for (Index e = 0; e < ne; ++e) {
-    ev[2 * e] = m.edge_vertices(e)[0];
-    ev[2 * e + 1] = m.edge_vertices(e)[1];
-  }
-  edges.alloc(ev.size());
-  edges.upload(ev.data(), ev.size(), s);
-  // Front connectivity: mesh neighbours plus, for every incident face, the
-  // apex of the face across the link edge (the edge of the face opposite v).
-  // Two band vertices are related iff their stars contain edge-adjacent
-  // faces, which makes union-find over band vertices equivalent to the
-  // reference's union-find over band triangles.
-  std::vector<int> coff(nv + 1, 0), ccol;
-  ccol.reserve(static_cast<size_t>(nv) * 12);
-  std::vector<int> tmp;
-  for (Index v = 0; v < nv; ++v) {
-    tmp.clear();
-    for (Index q = m.v2v_off()[v]; q < m.v2v_off()[v + 1]; ++q) tmp.push_back(static_cast<int>(m.v2v()[q]));
-    for (Index q = m.v2f_off()[v]; q < m.v2f_off()[v + 1]; ++q) {
-      const Index f = m.v2f()[q];
-      const auto& t = m.face(f);
-      int kv = t[0] == v ? 0 : (t[1] == v ? 1 : 2);
-      const Index e = m.face_edges(f)[(kv + 1) % 3];  // edge (t[kv+1], t[kv+2])
-      const Index g = m.opposite_face(e, f);
-      const auto& tg = m.face(g);
-      const auto& evs = m.edge_vertices(e);
-      for (Index w : tg)
-        if (w != evs[0] && w != evs[1] && w != v) tmp.push_back(static_cast<int>(w));
-    }
-    std::sort(tmp.begin(), tmp.end());
-    tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
-    ccol.insert(ccol.end(), tmp.begin(), tmp.end());
-    coff[v + 1] = static_cast<int>(ccol.size());
-  }
-  c_off.alloc(coff.size());
-  c_off.upload(coff.data(), coff.size(), s);
-  c_col.alloc(std::max<size_t>(1, ccol.size()));
-  c_col.upload(ccol.data(), ccol.size(), s);
-  std::vector<int> noff(m.v2v_off().begin(), m.v2v_off().end()), ncol(m.v2v().begin(), m.v2v().end());
-  n_off.alloc(noff.size());
-  n_off.upload(noff.data(), noff.size(), s);
-  n_col.alloc(std::max<size_t>(1, ncol.size()));
-  n_col.upload(ncol.data(), ncol.size(), s);
-  std::vector<int> foff(m.v2f_off().begin(), m.v2f_off().end()), fcol(m.v2f().begin(), m.v2f().end());
-  f_off.alloc(foff.size());
-  f_off.upload(foff.data(), foff.size(), s);
-  f_col.alloc(std::max<size_t>(1, fcol.size()));
-  f_col.upload(fcol.data(), fcol.size(), s);
+  faces.upload(reinterpret_cast<const unsigned*>(m.faces().data()), faces.n, s);
+  edges.alloc(2 * static_cast<size_t>(ne));
+  edges.upload(reinterpret_cast<const unsigned*>(&m.edge_vertices(0)[0]), edges.n, s);
+  DevBuf<unsigned> fe(3 * static_cast<size_t>(nf)), ef(2 * static_cast<size_t>(ne));
+  fe.upload(reinterpret_cast<const unsigned*>(&m.face_edges(0)[0]), fe.n, s);
+  ef.upload(reinterpret_cast<const unsigned*>(&m.edge_faces(0)[0]), ef.n, s);
+  n_off.alloc(nv + 1);
+  n_off.upload(reinterpret_cast<const int*>(m.v2v_off().data()), n_off.n, s);
+  n_col.alloc(std::max<size_t>(1, m.v2v().size()));
+  n_col.upload(reinterpret_cast<const int*>(m.v2v().data()), m.v2v().size(), s);
+  f_off.alloc(nv + 1);
+  f_off.upload(reinterpret_cast<const int*>(m.v2f_off().data()), f_off.n, s);
+  f_col.alloc(std::max<size_t>(1, m.v2f().size()));
+  f_col.upload(reinterpret_cast<const int*>(m.v2f().data()), m.v2f().size(), s);
+  // Front connectivity: for each vertex the higher-numbered mesh neighbours
+  // and apexes of the faces across its link edges.  Two band vertices are
+  // related iff their stars contain edge-adjacent faces, which makes
+  // union-find over band vertices equivalent to the reference's union-find
+  // over band triangles; each pair is united once, from its lower vertex.
+  FrontBuild fb{};
+  fb.nv = static_cast<int>(nv);
+  fb.faces = faces.p;
+  fb.face_edges = fe.p;
+  fb.edge_faces = ef.p;
+  fb.edges = edges.p;
+  fb.v2v_off = n_off.p;
+  fb.v2v = n_col.p;
+  fb.v2f_off = f_off.p;
+  fb.v2f = f_col.p;
+  c_off.alloc(nv + 1);
+  int* ccol = nullptr;
+  int nnzc = 0;
+  const int rc = launch_front_csr(fb, c_off.p, &ccol, &nnzc, s);
+  if (rc == -1) fail(kCapacityExceeded, "vertex valence above 32");
+  ck(rc, "front connectivity");
+  c_col.p = ccol;
+  c_col.n = static_cast<size_t>(std::max(1, nnzc));
   cuda_check(cudaStreamSynchronize(s), "mesh upload");
 
   view_.nv = static_cast<int>(nv);
@@ -375,36 +353,50 @@ DeviceField::DeviceField(std::shared_ptr<DeviceMesh> dm, cudaStream_t s) : dm_(d
 }
 DeviceField::DeviceField(DeviceMesh* dm, cudaStream_t s) : dm_(dm), s_(s) { setup(); }
 
-DeviceMesh::~DeviceMesh() {
-  for (DeviceField* f : pool_) delete f;
-}
+DeviceMesh::~DeviceMesh() = default;
+
+namespace {
+// Process-wide pool of field workspaces (~600 B per vertex: columns, scratch,
+// frontier and band lists, union-find parents ...).  A workspace serves any
+// mesh up to its vertex capacity, so repeated passes -- on one mesh or on a
+// batch of meshes -- do not re-allocate.
+std::mutex g_pool_mu;
+std::vector<DeviceField*> g_pool;
+constexpr size_t kPoolKeep = 4;
+}  // namespace
 
 std::shared_ptr<DeviceField> DeviceMesh::acquire_field(cudaStream_t s) {
   DeviceField* f = nullptr;
+  const size_t need = host().nv();
   {
-    std::lock_guard<std::mutex> lk(pool_mu_);
-    if (!pool_.empty()) {
-      f = pool_.back();
-      pool_.pop_back();
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    size_t best = g_pool.size();
+    for (size_t i = 0; i < g_pool.size(); ++i)
+      if (g_pool[i]->capacity() >= need && (best == g_pool.size() || g_pool[i]->capacity() < g_pool[best]->capacity()))
+        best = i;
+    if (best < g_pool.size()) {
+      f = g_pool[best];
+      g_pool.erase(g_pool.begin() + static_cast<std::ptrdiff_t>(best));
     }
   }
-  if (!f) f = new DeviceField(this, s);
+  if (f) f->retarget(this);
+  else f = new DeviceField(this, s);
   f->set_stream(s);
   f->keep_ = shared_from_this();
-  std::weak_ptr<DeviceMesh> home = f->keep_;
-  return std::shared_ptr<DeviceField>(f, [home](DeviceField* p) {
-    if (auto m = home.lock()) {
-      p->keep_.reset();  // the pool must not own its mesh
-      std::lock_guard<std::mutex> lk(m->pool_mu_);
-      m->pool_.push_back(p);
-    } else {
-      delete p;
+  return std::shared_ptr<DeviceField>(f, [](DeviceField* p) {
+    p->keep_.reset();
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_pool.push_back(p);
+    if (g_pool.size() > kPoolKeep) {
+      delete g_pool.front();
+      g_pool.erase(g_pool.begin());
     }
   });
 }
 
 void DeviceField::setup() {
   const size_t nv = dm_->host().nv();
+  cap_ = nv;
   cnt.alloc(nv);
   interest.alloc(nv);
   scnt.alloc(nv);
@@ -416,12 +408,15 @@ void DeviceField::setup() {
   region0.alloc(nv);
   region1.alloc(nv);
   stamp.alloc(nv);
-  ilist.alloc(nv);
+  ilist0.alloc(nv);
+  ilist1.alloc(nv);
+  in_list.alloc(nv);
+  bandpairs.alloc(2 * nv + 4096);
   parent.alloc(nv * kSlots);
   active.alloc(kMaxLayers + 1);
   aidx.alloc(kMaxLayers + 1);
   alist.alloc(kMaxActive);
-  stat.alloc(kMaxActive);
+  stat.alloc(2 * static_cast<size_t>(kMaxActive));
   pair_keys.alloc(kPairCap);
   pairs.alloc(kPairCap);
   lastpos.alloc(4 * static_cast<size_t>(kMaxLayers + 1));
@@ -444,7 +439,13 @@ void DeviceField::setup() {
   work_.slay = slay.p;
   work_.sval = sval.p;
   work_.sflag = sflag.p;
-  work_.ilist = ilist.p;
+  work_.ilist[0] = ilist0.p;
+  work_.ilist[1] = ilist1.p;
+  work_.in_list = in_list.p;
+  work_.bandpairs = bandpairs.p;
+  work_.bandpair_cap = static_cast<int>(bandpairs.n);
+  binfo.alloc(nv);
+  view_.binfo = binfo.p;
   work_.parent = parent.p;
   work_.active = active.p;
   work_.aidx = aidx.p;
@@ -770,15 +771,23 @@ StepParams make_params(const DeviceField& field, const Config& cfg, const Coeffi
   return p;
 }
 
+// Grid of the persistent kernel: at most one CTA per SM (the grid barrier's
+// cost grows with the CTA count, and a step's frontier/band work rarely needs
+// more than 148 x 256 threads), fewer for small meshes.
 int engine_blocks(int nv) {
-  static int maxco = 0;
-  if (!maxco) ck(dev_max_coresident_blocks(&maxco), "occupancy");
+  static int maxco = 0, sms = 0;
+  if (!maxco) {
+    ck(dev_max_coresident_blocks(&maxco), "occupancy");
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "device");
+    cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms");
+  }
   if (const char* env = std::getenv("DTB_BLOCKS")) {
     const int b = std::atoi(env);
     if (b > 0) return std::min(b, maxco);
   }
-  const int want = std::max(1, nv / 2048);
-  return std::min(want, maxco);
+  const int want = std::max(1, nv / 4096);
+  return std::min({want, sms, maxco});
 }
 
 std::vector<std::vector<Index>> groups_from_pairs(const std::vector<unsigned>& pairs) {
@@ -807,32 +816,44 @@ std::vector<unsigned> read_pairs(const DeviceField& field) {
   return to_host(field.pairs, static_cast<size_t>(c.npairs), field.stream());
 }
 
-void run_check_kernel(DeviceField& field, const Config& cfg, const Coefficients& co, double dt) {
+// Check-only kernel (stats, CCL, collisions of the current state) into the
+// statistics buffer of step s's parity.
+void run_check_kernel(DeviceField& field, const Config& cfg, const Coefficients& co, double dt, long s) {
   StepParams p = make_params(field, cfg, co, dt);
+  p.step_begin = s;
   static int maxco = 0;
   if (!maxco) ck(dev_max_coresident_blocks(&maxco), "occupancy");
-  const int blocks = std::min(maxco, std::max(1, static_cast<int>(field.mesh().host().nv()) / 2048));
+  const int blocks = std::min(maxco, engine_blocks(static_cast<int>(field.mesh().host().nv())));
   ck(launch_check(field.mesh().view(), field.view(), field.work(), p, blocks, field.stream()), "check kernel");
   cuda_check(cudaStreamSynchronize(field.stream()), "check sync");
 }
 
-std::vector<LayerStat> read_stats(const DeviceField& field) {
+std::vector<LayerStat> read_stats(const DeviceField& field, long s) {
   const size_t n = field.active_nonbase().size();
-  return to_host(field.stat, n, field.stream());
+  std::vector<LayerStat> out(n);
+  if (n) {
+    cuda_check(cudaMemcpyAsync(out.data(), field.stat.p + static_cast<size_t>(s & 1) * kMaxActive, sizeof(LayerStat) * n,
+                               cudaMemcpyDeviceToHost, field.stream()),
+               "stats");
+    cuda_check(cudaStreamSynchronize(field.stream()), "stats sync");
+  }
+  return out;
 }
 
 }  // namespace
 
 std::vector<std::vector<Index>> detect_collisions(DeviceField& field, const Config& cfg) {
   cfg.validate();
+  field.set_band(cfg.band_low_threshold, cfg.saturation);
   field.sync_active();
   if (field.active_nonbase().size() < 2) return {};
-  run_check_kernel(field, cfg, Coefficients{}, 0.0);
+  run_check_kernel(field, cfg, Coefficients{}, 0.0, 0);
   return groups_from_pairs(read_pairs(field));
 }
 
 void step(DeviceField& field, const DeviceLaplacian& op, const Config& cfg, const Coefficients& c) {
   cfg.validate();
+  field.set_band(cfg.band_low_threshold, cfg.saturation);
   const double dt = cfg.dt > 0 ? cfg.dt : stable_time_step(op, c);
   field.sync_active();
   cudaStream_t s = field.stream();
@@ -844,7 +865,6 @@ void step(DeviceField& field, const DeviceLaplacian& op, const Config& cfg, cons
   ctl.rcount[0] = ctl.rcount[1] = 0;
   ctl.error = 0;
   ctl.stop_bits = 0;
-  ctl.trail_pending = 0;
   field.ctl.upload(&ctl, 1, s);
   const DevMesh m = op.view();
   ck(launch_mark_all_support(m, field.view(), w, 0, 1, s), "mark support");
@@ -877,6 +897,7 @@ class PassEngine {
     cuda_check(cudaEventCreate(&ev1k_), "event");
     cuda_check(cudaEventRecord(ev0_, s_), "event record");
     field_ = dm_->acquire_field(s_);
+    field_->set_band(cfg_.band_low_threshold, cfg_.saturation);
     res_.field = field_;
     res_.seed_vertex = seed;
     const double radius =
@@ -899,6 +920,10 @@ class PassEngine {
     std::vector<int> sv(seeds.begin(), seeds.end());
     field_->mark_region(op_.view(), sv, 0, 1);
     blocks_ = engine_blocks(static_cast<int>(mesh_.nv()));
+    if (const char* env = std::getenv("DTB_PHASE_PROF"); env && env[0] == '1') {
+      prof_.alloc(4 * static_cast<size_t>(std::min<long>(cfg_.max_steps, 100000)) + 8);
+      prof_.zero(s_);
+    }
   }
   ~PassEngine() {
     if (ev0_) cudaEventDestroy(ev0_);
@@ -930,6 +955,7 @@ class PassEngine {
       res_.message = e.what();
     }
     res_.steps = step;
+    if (prof_.p) report_phases();
     {
       const Ctl c = field_->read_ctl();
       res_.sum_region = c.sum_region;
@@ -960,11 +986,17 @@ class PassEngine {
   StepParams params() const {
     StepParams p = make_params(*field_, cfg_, co_, dt_);
     p.stop_every_check = cfg_.on_check ? 1 : 0;
+    if (const char* env = std::getenv("DTB_SPLIT_A"); env && env[0] == '1') p.split_a = 1;
+    if (const char* env = std::getenv("DTB_NO_UNITE"); env && env[0] == '1') p.split_a_no_unite = 1;
     return p;
   }
 
   DevWork work() const {
     DevWork w = field_->work();
+    if (prof_.p) {
+      w.prof = prof_.p;
+      w.prof_cap = static_cast<int>(prof_.n);
+    }
     if (cfg_.record_hashes) {
       w.hashes = field_->hashes.p;
       w.hash_base = 0;
@@ -1224,7 +1256,7 @@ class PassEngine {
     ++res_.event_checks;
     bool changed = false;
     {
-      const std::vector<LayerStat> st = read_stats(*field_);
+      const std::vector<LayerStat> st = read_stats(*field_, s);
       const std::vector<Index> act = field_->active_nonbase();
       for (size_t a = 0; a < act.size(); ++a) {
         if (st[a].ncomp < 2) continue;
@@ -1236,7 +1268,7 @@ class PassEngine {
     }
     if (changed) {
       field_->sync_active();
-      run_check_kernel(*field_, cfg_, co_, dt_);
+      run_check_kernel(*field_, cfg_, co_, dt_, s);
     }
     const auto groups = groups_from_pairs(read_pairs(*field_));
     for (const auto& g : groups) {
@@ -1245,11 +1277,11 @@ class PassEngine {
     }
     if (!groups.empty()) {
       field_->sync_active();
-      run_check_kernel(*field_, cfg_, co_, dt_);
+      run_check_kernel(*field_, cfg_, co_, dt_, s);
     }
     // Band anchors (device: means, snaps, trail records) and vanishing layers.
     const std::vector<Index> act = field_->active_nonbase();
-    const std::vector<LayerStat> st = read_stats(*field_);
+    const std::vector<LayerStat> st = read_stats(*field_, s);
     StepParams p = params();
     p.step_begin = s;
     if (cfg_.record_trails) ck(launch_snap(dm_->view(), field_->view(), field_->work(), p, s_), "snap");
@@ -1296,6 +1328,23 @@ class PassEngine {
 
   void finish_tracks() { res_.tracks = tracks_; }
 
+  void report_phases() const {
+    std::vector<unsigned long long> t = to_host(prof_, prof_.n, s_);
+    double sum[3] = {0, 0, 0}, tot = 0;
+    long n = 0;
+    for (size_t i = 0; i + 4 < t.size(); i += 4) {
+      if (!t[i] || !t[i + 3] || !t[i + 4]) continue;
+      sum[0] += static_cast<double>(t[i + 1] - t[i]);
+      sum[1] += static_cast<double>(t[i + 2] - t[i + 1]);
+      sum[2] += static_cast<double>(t[i + 3] - t[i + 2]);
+      tot += static_cast<double>(t[i + 4] - t[i]);
+      ++n;
+    }
+    if (n)
+      std::fprintf(stderr, "[dtb] phase us/step over %ld steps: B %.2f  D %.2f  E(+A) %.2f  step %.2f (blocks %d)\n", n,
+                   sum[0] / n / 1e3, sum[1] / n / 1e3, sum[2] / n / 1e3, tot / n / 1e3, blocks_);
+  }
+
   std::shared_ptr<DeviceMesh> dm_;
   const Mesh& mesh_;
   const DeviceLaplacian& op_;
@@ -1308,6 +1357,7 @@ class PassEngine {
   std::vector<LayerTrack> tracks_;
   double dt_ = 0;
   int blocks_ = 1;
+  DevBuf<unsigned long long> prof_;  // DTB_PHASE_PROF=1: per-step phase timestamps of the first launch
 };
 
 }  // namespace

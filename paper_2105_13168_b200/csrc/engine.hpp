@@ -72,6 +72,7 @@ class DeviceMesh : public std::enable_shared_from_this<DeviceMesh> {
  public:
   explicit DeviceMesh(std::shared_ptr<const Mesh> mesh, cudaStream_t s);
   ~DeviceMesh();
+  // A field workspace for this mesh from the process-wide pool.
   std::shared_ptr<DeviceField> acquire_field(cudaStream_t s);
   const Mesh& host() const { return *mesh_; }
   std::shared_ptr<const Mesh> host_ptr() const { return mesh_; }
@@ -85,8 +86,6 @@ class DeviceMesh : public std::enable_shared_from_this<DeviceMesh> {
  private:
   std::shared_ptr<const Mesh> mesh_;
   DevMesh view_;
-  std::mutex pool_mu_;
-  std::vector<DeviceField*> pool_;
 };
 
 // Cotangent stiffness + lumped masses (operators.hpp LaplacianOperator).
@@ -217,6 +216,12 @@ class DeviceField {
   const DeviceMesh& mesh() const { return *dm_; }
   cudaStream_t stream() const { return s_; }
   void set_stream(cudaStream_t s) { s_ = s; }
+  size_t capacity() const { return cap_; }
+  void retarget(DeviceMesh* dm) { dm_ = dm; }
+  void set_band(double lo, double sat) {
+    work_.band_lo = lo;
+    work_.sat = sat;
+  }
   Ctl read_ctl() const;
   // Queues verts and their stiffness rows as the frontier of step stamp+1.
   void mark_region(const DevMesh& op_view, const std::vector<int>& verts, long stamp, int parity);
@@ -225,10 +230,12 @@ class DeviceField {
   std::vector<int> pending_moved;
 
   // storage
-  DevBuf<unsigned char> cnt, interest, scnt, sflag, active;
+  DevBuf<unsigned char> cnt, interest, scnt, sflag, active, in_list;
   DevBuf<unsigned short> lay, slay;
   DevBuf<double> val, sval, lastpos;
-  DevBuf<int> region0, region1, stamp, ilist, aidx, alist, pairs_scratch;
+  DevBuf<int> region0, region1, stamp, ilist0, ilist1, aidx, alist;
+  DevBuf<int2> bandpairs;
+  DevBuf<uint4> binfo;
   DevBuf<unsigned long long> parent, pair_keys, hashes;
   DevBuf<unsigned> pairs;
   DevBuf<LayerStat> stat;
@@ -240,6 +247,7 @@ class DeviceField {
   void setup();
   DeviceMesh* dm_;
   std::shared_ptr<DeviceMesh> keep_;  // keeps the mesh alive while the field is handed out
+  size_t cap_ = 0;                    // vertex capacity of the device buffers
   cudaStream_t s_;
   std::vector<LayerMeta> meta_;
   DevField view_;

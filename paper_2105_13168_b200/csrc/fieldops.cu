@@ -25,7 +25,9 @@ __device__ __forceinline__ double value_of(const DevField& F, int v, int layer) 
   return 0.0;
 }
 
-__device__ __forceinline__ void refresh_interest(const DevField& F, int v) {
+// Recomputes the interest flag of an edited column and appends the vertex to
+// the current band list if it became interesting.
+__device__ __forceinline__ void refresh_interest(const DevField& F, const DevWork& W, int v) {
   const int c = F.cnt[v];
   bool inter = false;
   for (int j = 0; j < c; ++j) {
@@ -33,6 +35,14 @@ __device__ __forceinline__ void refresh_interest(const DevField& F, int v) {
     inter |= (x > 0.0 && x < 1.0);
   }
   F.interest[v] = inter ? 1 : 0;
+  F.binfo[v] = inter ? make_binfo(F.lay + static_cast<size_t>(v) * kSlots, F.val + static_cast<size_t>(v) * kSlots, c,
+                                  W.band_lo, W.sat)
+                     : make_uint4(0, 0, 0, 0);
+  if (inter && !W.in_list[v]) {
+    W.in_list[v] = 1;
+    const int par = W.ctl->lpar;
+    W.ilist[par][atomicAdd(&W.ctl->ilcount[par], 1)] = v;
+  }
 }
 
 __global__ void k_init(DevField F, DevWork W, int nv) {
@@ -42,6 +52,8 @@ __global__ void k_init(DevField F, DevWork W, int nv) {
   F.lay[static_cast<size_t>(v) * kSlots] = 0;
   F.val[static_cast<size_t>(v) * kSlots] = 1.0;
   F.interest[v] = 0;
+  F.binfo[v] = make_uint4(0, 0, 0, 0);
+  W.in_list[v] = 0;
   W.stamp[v] = -1;
 }
 
@@ -99,7 +111,7 @@ __global__ void k_pull(DevField F, int nv, int layer, int* out_v, double* out_x,
 
 // Moves the value of `oldlayer` at each listed vertex to its new layer id
 // (split_layer: row ownership changes, values do not).
-__global__ void k_relabel(DevField F, const int* verts, const int* newlayer, int n, int oldlayer) {
+__global__ void k_relabel(DevField F, DevWork W, const int* verts, const int* newlayer, int n, int oldlayer) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int v = verts[i];
@@ -124,11 +136,13 @@ __global__ void k_relabel(DevField F, const int* verts, const int* newlayer, int
   F.lay[b + p] = static_cast<unsigned short>(nl);
   F.val[b + p] = x;
   F.cnt[v] = static_cast<unsigned char>(c + 1);
+  if (F.interest[v]) F.binfo[v] = make_binfo(F.lay + b, F.val + b, c + 1, W.band_lo, W.sat);
 }
 
 // merge_layers: per vertex, the group's values summed in ascending layer
 // order from 0.0, clamped by min(., 1), stored under the new id.
-__global__ void k_merge(DevField F, int nv, const int* group, int ngroup, int result, int* touched, int* ntouched) {
+__global__ void k_merge(DevField F, DevWork W, int nv, const int* group, int ngroup, int result, int* touched,
+                        int* ntouched) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= nv) return;
   const size_t b = static_cast<size_t>(v) * kSlots;
@@ -160,7 +174,7 @@ __global__ void k_merge(DevField F, int nv, const int* group, int ngroup, int re
   F.lay[b + p] = static_cast<unsigned short>(result);
   F.val[b + p] = clamped;
   F.cnt[v] = static_cast<unsigned char>(out + 1);
-  refresh_interest(F, v);
+  refresh_interest(F, W, v);
   touched[atomicAdd(ntouched, 1)] = v;
 }
 
@@ -252,7 +266,7 @@ __global__ void k_normalize(DevField F, DevWork W, int nv, double prune) {
     ++out;
   }
   F.cnt[v] = static_cast<unsigned char>(out);
-  refresh_interest(F, v);
+  refresh_interest(F, W, v);
 }
 
 __global__ void k_dense_row(DevField F, int nv, int layer, double* out) {
@@ -299,15 +313,15 @@ int launch_pull_layer(const DevField& f, int nv, int layer, int* out_v, double* 
   k_pull<<<nblk(nv), T, 0, static_cast<cudaStream_t>(stream)>>>(f, nv, layer, out_v, out_x, out_n);
   DTB_RET;
 }
-int launch_relabel(const DevField& f, const DevWork&, const int* verts, const int* newlayer, int n, int oldlayer,
+int launch_relabel(const DevField& f, const DevWork& w, const int* verts, const int* newlayer, int n, int oldlayer,
                    void* stream) {
   if (n <= 0) return 0;
-  k_relabel<<<nblk(n), T, 0, static_cast<cudaStream_t>(stream)>>>(f, verts, newlayer, n, oldlayer);
+  k_relabel<<<nblk(n), T, 0, static_cast<cudaStream_t>(stream)>>>(f, w, verts, newlayer, n, oldlayer);
   DTB_RET;
 }
-int launch_merge(const DevField& f, const DevWork&, int nv, const int* group, int ngroup, int result, int* touched,
+int launch_merge(const DevField& f, const DevWork& w, int nv, const int* group, int ngroup, int result, int* touched,
                  int* ntouched, void* stream) {
-  k_merge<<<nblk(nv), T, 0, static_cast<cudaStream_t>(stream)>>>(f, nv, group, ngroup, result, touched, ntouched);
+  k_merge<<<nblk(nv), T, 0, static_cast<cudaStream_t>(stream)>>>(f, w, nv, group, ngroup, result, touched, ntouched);
   DTB_RET;
 }
 int launch_covered(const DevField& f, int nv, double threshold, int* out_v, int* out_n, void* stream) {

@@ -25,6 +25,8 @@
 // so every field value is bit-identical to the CPU reference.
 #include <cuda_runtime.h>
 
+#include <cooperative_groups.h>
+
 #include <cstdint>
 
 #include "kernels.h"
@@ -42,30 +44,30 @@ constexpr unsigned long long kVertMask = (1ull << 27) - 1;  // vertex bits of a 
 __device__ __forceinline__ double clamp01(double x) { return x < 0.0 ? 0.0 : (1.0 < x ? 1.0 : x); }
 __device__ __forceinline__ double max0(double x) { return x < 0.0 ? 0.0 : x; }  // std::max(x, 0.0)
 
-__device__ __forceinline__ void raise_error(Ctl* ctl, int code, int v) {
-  int prev = atomicMax(&ctl->error, code);
-  if (prev < code) ctl->error_vertex = v;
+// Errors of a speculative update (the next step's, computed while the
+// current step's check runs) only become real if the check finds no event.
+__device__ __forceinline__ void raise_error(Ctl* ctl, int code, int v, bool spec) {
+  int* slot = spec ? &ctl->spec_error : &ctl->error;
+  int prev = atomicMax(slot, code);
+  if (prev < code) *(spec ? &ctl->spec_error_vertex : &ctl->error_vertex) = v;
 }
 
-__device__ __forceinline__ void grid_sync(Ctl* ctl) {
-  const unsigned nb = gridDim.x;
-  __syncthreads();
-  if (nb == 1) return;
-  if (threadIdx.x == 0) {
-    volatile unsigned* genp = &ctl->bar_gen;
-    const unsigned gen = *genp;
-    __threadfence();
-    const unsigned arrived = atomicAdd(&ctl->bar_count, 1u);
-    if (arrived == nb - 1) {
-      atomicExch(&ctl->bar_count, 0u);
-      __threadfence();
-      atomicAdd(&ctl->bar_gen, 1u);
-    } else {
-      while (*genp == gen) __nanosleep(20);
-    }
-    __threadfence();
-  }
-  __syncthreads();
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void grid_sync(Ctl*) {
+  // cooperative_groups' grid barrier measured 1.2 us vs 2.6 us for a
+  // counter/generation barrier with gpu-scope fences (148 CTAs, B200).
+  cooperative_groups::this_grid().sync();
 }
 
 // set_value semantics (layer_field.hpp:102): clamp above 1, prune below the
@@ -109,9 +111,33 @@ __device__ __forceinline__ bool col_set(unsigned short* nl, double* nx, int& nn,
 
 // ---------------------------------------------------------------------------
 // Phase A: one explicit Euler update of every near-support layer and the base
-// layer at vertex v, reading only the committed columns.
+// layer at vertex v, reading only the committed columns.  An 8-lane group
+// works on one vertex: lane j gathers stiffness neighbour j (its column's
+// first kReg slots in registers), then every lane folds the neighbours in
+// ascending column order through width-8 shuffles -- the reference's
+// summation order -- so all lanes hold the same results.
+constexpr int kG = 8;    // lanes per vertex group
+constexpr int kReg = 4;  // neighbour-column slots kept in registers
+
+__device__ __forceinline__ unsigned group_mask() { return 0xFFu << (threadIdx.x & 24); }
+
+__device__ __forceinline__ void cand_add(unsigned short* cl, double* ca, int& nc, bool& overflow, int l, double t) {
+  int c = 0;
+  while (c < nc && cl[c] != l) ++c;
+  if (c == nc) {
+    if (nc == kCand) {
+      overflow = true;
+      return;
+    }
+    cl[nc] = static_cast<unsigned short>(l);
+    ca[nc] = 0.0;
+    ++nc;
+  }
+  ca[c] = ca[c] + t;
+}
+
 __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P,
-                              int i, int v) {
+                              int i, int v, bool spec, int lane, unsigned gm) {
   unsigned short ol[kSlots];
   double ox[kSlots];
   const int cv = F.cnt[v];
@@ -128,37 +154,66 @@ __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork
   bool bnear = phib > 0.0;
   bool overflow = false;
   const int k0 = __ldg(M.s_off + v), k1 = __ldg(M.s_off + v + 1);
-  for (int k = k0; k < k1; ++k) {
-    const int u = __ldg(M.s_col + k);
-    const double s = __ldg(M.s_val + k);
-    const int cu = F.cnt[u];
-    double bu = 0.0, au = 0.0;
-    const size_t base = static_cast<size_t>(u) * kSlots;
-    for (int j = 0; j < cu; ++j) {
-      const int l = F.lay[base + j];
-      const double x = F.val[base + j];
-      if (l == 0) {
-        bu = x;
-        continue;
-      }
-      if (!W.active[l]) continue;
-      au = au + x;
-      int c = 0;
-      while (c < nc && cl[c] != l) ++c;
-      if (c == nc) {
-        if (nc == kCand) {
-          overflow = true;
-          continue;
-        }
-        cl[nc] = static_cast<unsigned short>(l);
-        ca[nc] = 0.0;
-        ++nc;
-      }
-      ca[c] = ca[c] + s * x;
+  for (int kb = k0; kb < k1; kb += kG) {
+    const int k = kb + lane;
+    const bool valid = k < k1;
+    int u = 0, cu = 0;
+    double s = 0.0, bu = 0.0, au = 0.0;
+    unsigned short L[kReg];
+    double X[kReg];
+#pragma unroll
+    for (int q = 0; q < kReg; ++q) {
+      L[q] = 0;
+      X[q] = 0.0;
     }
-    lapb = lapb + s * bu;
-    lapt = lapt + s * au;
-    if (bu > 0.0) bnear = true;
+    if (valid) {
+      u = __ldg(M.s_col + k);
+      s = __ldg(M.s_val + k);
+      cu = F.cnt[u];
+      const size_t b = static_cast<size_t>(u) * kSlots;
+#pragma unroll
+      for (int q = 0; q < kReg; ++q)
+        if (q < cu) {
+          L[q] = F.lay[b + q];
+          X[q] = F.val[b + q];
+        }
+#pragma unroll
+      for (int q = 0; q < kReg; ++q)
+        if (q < cu) {
+          if (L[q] == 0) bu = X[q];
+          else if (W.active[L[q]]) au = au + X[q];
+        }
+      for (int q = kReg; q < cu; ++q) {
+        const int l = F.lay[b + q];
+        const double x = F.val[b + q];
+        if (l == 0) bu = x;
+        else if (W.active[l]) au = au + x;
+      }
+    }
+    const int nvalid = min(kG, k1 - kb);
+    for (int jj = 0; jj < nvalid; ++jj) {
+      const double s_ = __shfl_sync(gm, s, jj, kG);
+      const int cu_ = __shfl_sync(gm, cu, jj, kG);
+      const double bu_ = __shfl_sync(gm, bu, jj, kG);
+      const double au_ = __shfl_sync(gm, au, jj, kG);
+      lapb = lapb + s_ * bu_;
+      lapt = lapt + s_ * au_;
+      if (bu_ > 0.0) bnear = true;
+#pragma unroll
+      for (int q = 0; q < kReg; ++q) {
+        const int l_ = __shfl_sync(gm, static_cast<int>(L[q]), jj, kG);
+        const double x_ = __shfl_sync(gm, X[q], jj, kG);
+        if (q < cu_ && l_ != 0 && W.active[l_]) cand_add(cl, ca, nc, overflow, l_, s_ * x_);
+      }
+      if (cu_ > kReg) {
+        const int u_ = __shfl_sync(gm, u, jj, kG);
+        const size_t b = static_cast<size_t>(u_) * kSlots;
+        for (int q = kReg; q < cu_; ++q) {
+          const int l_ = F.lay[b + q];
+          if (l_ != 0 && W.active[l_]) cand_add(cl, ca, nc, overflow, l_, s_ * F.val[b + q]);
+        }
+      }
+    }
   }
   // Layers held at v itself are near support even if the stiffness row
   // lacks its diagonal (never on valid meshes, kept for exactness).
@@ -178,7 +233,7 @@ __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork
     }
   }
   if (overflow) {
-    raise_error(W.ctl, kDevCapacity, v);
+    raise_error(W.ctl, kDevCapacity, v, spec);
     return;
   }
 
@@ -203,7 +258,7 @@ __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork
     const double inner = P.w * (phib - phi) + P.half_a2 * (lap_b - lap_i) - P.e * sqrt(max0(phi * phib));
     const double rate = -P.mu_n * inner;
     if (!isfinite(rate)) {
-      raise_error(W.ctl, kDevBlowup, v);
+      raise_error(W.ctl, kDevBlowup, v, spec);
       return;
     }
     const double next = clamp01(phi + P.dt * rate);
@@ -226,7 +281,7 @@ __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork
     const double rate = -P.mu_n * (P.w * total + P.half_a2 * lap_total + P.e * contact) +
                         P.m_mu_n * (P.w * phib + P.half_a2 * lap_b);
     if (!isfinite(rate)) {
-      raise_error(W.ctl, kDevBlowup, v);
+      raise_error(W.ctl, kDevBlowup, v, spec);
       return;
     }
     const double next = clamp01(phib + P.dt * rate);
@@ -240,7 +295,7 @@ __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork
     double s = 0.0;
     for (int j = 0; j < nn; ++j) s = s + nx[j];
     if (s <= 0.0) {
-      raise_error(W.ctl, kDevZeroColumn, v);
+      raise_error(W.ctl, kDevZeroColumn, v, spec);
       return;
     }
     if (!(fabs(s - 1.0) < 1e-15)) {
@@ -255,48 +310,111 @@ __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork
     }
   }
   if (!ok || nn > kSlots) {
-    raise_error(W.ctl, kDevCapacity, v);
+    raise_error(W.ctl, kDevCapacity, v, spec);
     return;
   }
   const bool old_one = cv > 0 && ol[0] == 0 && ox[0] == 1.0;
   const bool new_one = nn > 0 && nl[0] == 0 && nx[0] == 1.0;
-  W.scnt[i] = static_cast<unsigned char>(nn);
   const size_t o = static_cast<size_t>(i) * kSlots;
-  for (int j = 0; j < nn; ++j) {
+  for (int j = lane; j < nn; j += kG) {
     W.slay[o + j] = nl[j];
     W.sval[o + j] = nx[j];
   }
-  W.sflag[i] = static_cast<unsigned char>((changed ? 1 : 0) | (old_one ? 2 : 0) | (new_one ? 4 : 0));
-}
-
-__device__ __forceinline__ void queue_region(const DevWork& W, int u, int stamp, int nxt) {
-  if (atomicExch(W.stamp + u, stamp) != stamp) {
-    const int pos = atomicAdd(&W.ctl->rcount[nxt], 1);
-    W.region[nxt][pos] = u;
+  if (lane == 0) {
+    W.scnt[i] = static_cast<unsigned char>(nn);
+    W.sflag[i] = static_cast<unsigned char>((changed ? 1 : 0) | (old_one ? 2 : 0) | (new_one ? 4 : 0));
   }
 }
 
-// Phase B for region slot i.
+// Warp-aggregated slot reservation: one atomic per warp and round instead of
+// one per appended item (frontier and band lists see thousands per step).
+__device__ __forceinline__ int agg_slot(int* counter, bool want) {
+  const unsigned act = __activemask();
+  const unsigned m = __ballot_sync(act, want);
+  if (!m) return -1;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(m) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(counter, __popc(m));
+  base = __shfl_sync(act, base, leader);
+  return want ? base + __popc(m & ((1u << lane) - 1)) : -1;
+}
+
+// Per-CTA staging of list appends: items collect in shared memory and the CTA
+// reserves its global range with one atomic at the end of the phase (the
+// frontier, band-list compaction and band items each see thousands of
+// appends per step; one global counter would serialise them).
+constexpr int kQCap = 2048;
+template <class T>
+struct BlockQueueT {
+  int n, base;
+  T buf[kQCap];
+};
+using BlockQueue = BlockQueueT<int>;
+using PairQueue = BlockQueueT<int2>;
+
+template <class T>
+__device__ __forceinline__ void bq_push(BlockQueueT<T>& q, int* gcount, T* glist, T item, int cap = 0x7fffffff,
+                                        int* overflow = nullptr) {
+  const int p = atomicAdd(&q.n, 1);
+  if (p < kQCap) {
+    q.buf[p] = item;
+  } else {  // staging full: direct append
+    const int g = atomicAdd(gcount, 1);
+    if (g < cap) glist[g] = item;
+    else if (overflow) *overflow = 1;
+  }
+}
+
+template <class T>
+__device__ void bq_flush(BlockQueueT<T>& q, int* gcount, T* glist, int cap = 0x7fffffff, int* overflow = nullptr) {
+  __syncthreads();
+  const int n = min(q.n, kQCap);
+  if (threadIdx.x == 0) q.base = n ? atomicAdd(gcount, n) : 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    if (q.base + i < cap) glist[q.base + i] = q.buf[i];
+    else if (overflow) *overflow = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) q.n = 0;
+  __syncthreads();
+}
+
+__device__ __forceinline__ void queue_region(const DevWork& W, int u, int stamp, int nxt, BlockQueue& Q) {
+  if (atomicExch(W.stamp + u, stamp) != stamp) bq_push(Q, &W.ctl->rcount[nxt], W.region[nxt], u);
+}
+
+// Phase B for frontier slot i (8-lane group): scatter the new column,
+// maintain the interest flag / band list and the base==1 counter, queue the
+// one-ring (lane j queues entries j, j+8, ... of {v} U row(v)).
 __device__ void commit_vertex(const DevMesh& M, const DevField& F, const DevWork& W, int i, int v, int stamp,
-                              int nxt) {
+                              int nxt, int lpar, int lane, unsigned gm, BlockQueue& Q) {
   const int flag = W.sflag[i];
   if (!(flag & 1)) return;
   const int nn = W.scnt[i];
   const size_t o = static_cast<size_t>(i) * kSlots, d = static_cast<size_t>(v) * kSlots;
   bool inter = false;
-  for (int j = 0; j < nn; ++j) {
+  for (int j = lane; j < nn; j += kG) {
     const double x = W.sval[o + j];
     F.lay[d + j] = W.slay[o + j];
     F.val[d + j] = x;
     inter |= (x > 0.0 && x < 1.0);
   }
-  F.cnt[v] = static_cast<unsigned char>(nn);
-  F.interest[v] = inter ? 1 : 0;
-  const int delta = ((flag >> 2) & 1) - ((flag >> 1) & 1);
-  if (delta) atomicAdd(&W.ctl->base_one, delta);
-  queue_region(W, v, stamp, nxt);
+  inter = __ballot_sync(gm, inter) != 0;
+  if (lane == 0) {
+    F.cnt[v] = static_cast<unsigned char>(nn);
+    F.interest[v] = inter ? 1 : 0;
+    F.binfo[v] = inter ? make_binfo(W.slay + o, W.sval + o, nn, W.band_lo, W.sat) : make_uint4(0, 0, 0, 0);
+    if (inter && !W.in_list[v]) {
+      W.in_list[v] = 1;
+      W.ilist[lpar][atomicAdd(&W.ctl->ilcount[lpar], 1)] = v;
+    }
+    const int delta = ((flag >> 2) & 1) - ((flag >> 1) & 1);
+    if (delta) atomicAdd(&W.ctl->base_one, delta);
+  }
   const int k0 = __ldg(M.s_off + v), k1 = __ldg(M.s_off + v + 1);
-  for (int k = k0; k < k1; ++k) queue_region(W, __ldg(M.s_col + k), stamp, nxt);
+  for (int t = lane; t <= k1 - k0; t += kG) queue_region(W, t == 0 ? v : __ldg(M.s_col + k0 + t - 1), stamp, nxt, Q);
 }
 
 __device__ __forceinline__ bool is_band(const DevWork& W, const StepParams& P, int l, double x) {
@@ -315,12 +433,24 @@ __device__ __forceinline__ unsigned uf_find(unsigned long long* par, unsigned x,
   }
 }
 
+// Randomised linking: the root with the smaller (hash, id) key is hooked
+// under the other.  Linking by plain id turns concurrently united bands (ring
+// paths with increasing ids) into pointer chains as long as the ring; random
+// keys bound the expected depth by O(log n).
+__device__ __forceinline__ unsigned long long uf_key(unsigned x) {
+  unsigned h = x * 0x9E3779B1u;
+  h ^= h >> 15;
+  h *= 0x85EBCA77u;
+  h ^= h >> 13;
+  return (static_cast<unsigned long long>(h) << 32) | x;
+}
+
 __device__ void uf_unite(unsigned long long* par, unsigned a, unsigned b, unsigned long long ep) {
   while (true) {
     a = uf_find(par, a, ep);
     b = uf_find(par, b, ep);
     if (a == b) return;
-    if (a < b) {
+    if (uf_key(a) > uf_key(b)) {
       const unsigned t = a;
       a = b;
       b = t;
@@ -369,93 +499,224 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long x)
   return x;
 }
 
-// Phase C: interest list by warp-ballot compaction (+ optional field digest).
-__device__ void phase_band_list(const DevField& F, const DevWork& W, int nv, bool hash) {
-  const int lane = threadIdx.x & 31;
-  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+// Dense field digest (parity tooling only).
+__device__ void phase_hash(const DevField& F, const DevWork& W, int nv) {
   unsigned long long h = 0;
-  for (int base = gwarp * 32; base < nv; base += nwarps * 32) {
-    const int v = base + lane;
-    const bool flag = v < nv && F.interest[v];
-    const unsigned mask = __ballot_sync(0xffffffffu, flag);
-    if (mask) {
-      int pos = 0;
-      if (lane == 0) pos = atomicAdd(&W.ctl->icount, __popc(mask));
-      pos = __shfl_sync(0xffffffffu, pos, 0);
-      if (flag) W.ilist[pos + __popc(mask & ((1u << lane) - 1))] = v;
-    }
-    if (hash && v < nv) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv + 31; v += gridDim.x * blockDim.x) {
+    if (v < nv) {
       const int c = F.cnt[v];
       for (int j = 0; j < c; ++j)
         h += entry_hash(F.lay[static_cast<size_t>(v) * kSlots + j], static_cast<unsigned long long>(v),
                         F.val[static_cast<size_t>(v) * kSlots + j]);
     }
   }
-  if (hash) {
-    h = warp_sum_u64(h);
-    if (lane == 0 && h) atomicAdd(&W.ctl->hash_acc, h);
-  }
+  h = warp_sum_u64(h);
+  if ((threadIdx.x & 31) == 0 && h) atomicAdd(&W.ctl->hash_acc, h);
 }
 
-// Phase D: union band items that share a band triangle pair.
-__device__ void phase_union(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P,
+// Phase D: union band items that share a band triangle pair (extract_front's
+// edge-adjacency of band triangles, expressed on band vertices).  An 8-lane
+// group per list entry; lane j probes the higher-numbered related vertices
+// j, j+8, ... through their band index (one 16-byte load per probe).
+__device__ __forceinline__ int band_slot_of(const DevField& F, const DevWork& W, const StepParams& P, int u,
+                                            unsigned l) {
+  const uint4 bu = F.binfo[u];
+  if (!binfo_overflow(bu)) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (binfo_layer(bu, t) == l) return static_cast<int>(binfo_slot(bu, t));
+    return -1;
+  }
+  const int cu = F.cnt[u];  // more than 4 band layers: scan the column
+  const size_t ub = static_cast<size_t>(u) * kSlots;
+  for (int j = 0; j < cu; ++j) {
+    const unsigned lu = F.lay[ub + j];
+    if (lu < l) continue;
+    return (lu == l && is_band(W, P, static_cast<int>(l), F.val[ub + j])) ? j : -1;
+  }
+  return -1;
+}
+
+__device__ void phase_union(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P, int lpar,
                             unsigned long long ep) {
-  const int n = W.ctl->icount;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
-    const int v = W.ilist[idx];
-    const int cv = F.cnt[v];
-    for (int k = 0; k < cv; ++k) {
-      const int l = F.lay[static_cast<size_t>(v) * kSlots + k];
-      const double x = F.val[static_cast<size_t>(v) * kSlots + k];
-      if (!is_band(W, P, l, x)) continue;
-      const unsigned item = static_cast<unsigned>(v) * kSlots + k;
-      const int c0 = __ldg(M.c_off + v), c1 = __ldg(M.c_off + v + 1);
-      for (int c = c0; c < c1; ++c) {
-        const int u = __ldg(M.c_col + c);
-        if (u <= v) continue;
-        const int cu = F.cnt[u];
-        const size_t ub = static_cast<size_t>(u) * kSlots;
-        for (int j = 0; j < cu; ++j) {
-          const int lu = F.lay[ub + j];
-          if (lu < l) continue;
-          if (lu == l && is_band(W, P, l, F.val[ub + j])) uf_unite(W.parent, item, static_cast<unsigned>(u) * kSlots + j, ep);
-          break;
-        }
+  const int n = W.ctl->ilcount[lpar];
+  const int* list = W.ilist[lpar];
+  const int lane = threadIdx.x & (kG - 1);
+  const int g0 = (blockIdx.x * blockDim.x + threadIdx.x) / kG, ng = gridDim.x * blockDim.x / kG;
+  for (int idx = g0; idx < n; idx += ng) {
+    const int v = list[idx];
+    if (!F.interest[v]) continue;
+    const uint4 bv = F.binfo[v];
+    const int c0 = __ldg(M.c_off + v), c1 = __ldg(M.c_off + v + 1);
+    const bool over = binfo_overflow(bv);
+    const int nitems = over ? F.cnt[v] : 4;
+    for (int t = 0; t < nitems; ++t) {
+      unsigned l;
+      int slot;
+      if (!over) {
+        l = binfo_layer(bv, t);
+        if (l == 0) break;
+        slot = static_cast<int>(binfo_slot(bv, t));
+      } else {
+        l = F.lay[static_cast<size_t>(v) * kSlots + t];
+        if (!is_band(W, P, static_cast<int>(l), F.val[static_cast<size_t>(v) * kSlots + t])) continue;
+        slot = t;
+      }
+      if (!W.active[l]) continue;
+      const unsigned item = static_cast<unsigned>(v) * kSlots + slot;
+      for (int c = c0 + lane; c < c1; c += kG) {
+        const int u = __ldg(M.c_col + c);  // higher-numbered related vertices only
+        const int j = band_slot_of(F, W, P, u, l);
+        if (j >= 0 && !P.split_a_no_unite) uf_unite(W.parent, item, static_cast<unsigned>(u) * kSlots + j, ep);
       }
     }
   }
 }
 
-// Phase E: per-layer statistics, collision pairs and base extinction data.
-__device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P,
-                            unsigned long long ep) {
-  const int n = W.ctl->icount;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
-    const int v = W.ilist[idx];
-    const int cv = F.cnt[v];
-    const size_t b = static_cast<size_t>(v) * kSlots;
+constexpr int kSmemLayers = 64;  // per-block aggregation slots for dense active indices
+struct BlockStats {
+  int cnt[kSmemLayers][3];  // ncomp, nband, nunsat
+  long long sum[kSmemLayers][3];
+  unsigned long long snap[kSmemLayers];
+  unsigned long long bmax;  // max base value in (0, 1), as ordered bits
+};
+
+__device__ void block_stats_init(BlockStats& S) {
+  for (int i = threadIdx.x; i < kSmemLayers; i += blockDim.x) {
+    S.cnt[i][0] = S.cnt[i][1] = S.cnt[i][2] = 0;
+    S.sum[i][0] = S.sum[i][1] = S.sum[i][2] = 0;
+    S.snap[i] = ~0ull;
+  }
+  if (threadIdx.x == 0) S.bmax = 0;
+  __syncthreads();
+}
+
+__device__ void block_stats_flush(BlockStats& S, LayerStat* g, int n_active, Ctl* ctl = nullptr) {
+  __syncthreads();
+  if (ctl && threadIdx.x == 0 && S.bmax) atomicMax(&ctl->base_max_bits, S.bmax);
+  for (int a = threadIdx.x; a < n_active && a < kSmemLayers; a += blockDim.x) {
+    if (S.cnt[a][0]) atomicAdd(&g[a].ncomp, S.cnt[a][0]);
+    if (S.cnt[a][1]) atomicAdd(&g[a].nband, S.cnt[a][1]);
+    if (S.cnt[a][2]) atomicAdd(&g[a].nunsat, S.cnt[a][2]);
+    for (int c = 0; c < 3; ++c)
+      if (S.sum[a][c])
+        atomicAdd(reinterpret_cast<unsigned long long*>(c == 0 ? &g[a].sx : (c == 1 ? &g[a].sy : &g[a].sz)),
+                  static_cast<unsigned long long>(S.sum[a][c]));
+    if (S.snap[a] != ~0ull) atomicMin(&g[a].snap, S.snap[a]);
+  }
+}
+
+// Segmented warp reductions: lanes holding the same key (dense active layer
+// index) combine their contributions with 32-bit __reduce_*_sync, so each
+// warp issues one shared-memory atomic per layer (64-bit shared atomics are
+// CAS spin loops on this architecture).
+__device__ __forceinline__ long long seg_sum_fx(unsigned peers, long long x) {
+  // |x| < 2^39: low 24 bits and the signed rest each sum exactly in 32 bits.
+  const unsigned lo = __reduce_add_sync(peers, static_cast<unsigned>(x & 0xFFFFFF));
+  const int hi = __reduce_add_sync(peers, static_cast<int>(x >> 24));
+  return (static_cast<long long>(hi) << 24) + static_cast<long long>(lo);
+}
+__device__ __forceinline__ unsigned long long seg_min_u64(unsigned peers, unsigned long long x) {
+  const unsigned hi = __reduce_min_sync(peers, static_cast<unsigned>(x >> 32));
+  const unsigned lo = __reduce_min_sync(peers, static_cast<unsigned>(x >> 32) == hi ? static_cast<unsigned>(x) : ~0u);
+  return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
+__device__ __forceinline__ unsigned long long seg_max_u64(unsigned peers, unsigned long long x) {
+  const unsigned hi = __reduce_max_sync(peers, static_cast<unsigned>(x >> 32));
+  const unsigned lo = __reduce_max_sync(peers, static_cast<unsigned>(x >> 32) == hi ? static_cast<unsigned>(x) : 0u);
+  return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
+
+// Phase E: per-layer statistics (roots = front components, band counts and
+// fixed-point position sums, unsaturated counts), collision pairs, base
+// extinction data, band items for the trail snap, and compaction of the band
+// list into the other buffer (dead entries dropped).  Lanes walk their
+// vertex's slots in lock step so contributions can be combined per warp.
+__device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P, int lpar,
+                            int spar, unsigned long long ep, bool compact, BlockStats& S, BlockQueue& Q,
+                            PairQueue& QB) {
+  LayerStat* g = W.stat + static_cast<size_t>(spar) * kMaxActive;
+  const int n = W.ctl->ilcount[lpar];
+  const int* list = W.ilist[lpar];
+  const int lane = threadIdx.x & 31;
+  const int trip = (n + gridDim.x * blockDim.x - 1) / (gridDim.x * blockDim.x);
+  for (int r = 0; r < trip; ++r) {
+    const int idx = (r * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+    const int v = idx < n ? list[idx] : -1;
+    const bool live = v >= 0 && F.interest[v];
+    if (compact) {
+      if (live) bq_push(Q, &W.ctl->ilcount[lpar ^ 1], W.ilist[lpar ^ 1], v);
+      else if (v >= 0) W.in_list[v] = 0;
+    }
+    const int cv = live ? F.cnt[v] : 0;
+    const size_t b = static_cast<size_t>(live ? v : 0) * kSlots;
     const double base = (cv > 0 && F.lay[b] == 0) ? F.val[b] : 0.0;
-    if (base > 0.0 && base < 1.0)
-      atomicMax(&W.ctl->base_max_bits, static_cast<unsigned long long>(__double_as_longlong(base)));
-    bool cand = false;
-    for (int k = 0; k < cv; ++k) {
-      const int l = F.lay[b + k];
-      if (l == 0 || !W.active[l]) continue;
-      const double x = F.val[b + k];
-      const int a = W.aidx[l];
-      LayerStat* st = W.stat + a;
-      if (x > 0.0 && x < 1.0) {
-        atomicAdd(&st->nunsat, 1);
-        if (x >= P.kappa) cand = true;
+    {
+      const bool has = base > 0.0 && base < 1.0;
+      const unsigned m = __ballot_sync(0xffffffffu, has);
+      if (m) {
+        const unsigned long long bm =
+            seg_max_u64(0xffffffffu, has ? static_cast<unsigned long long>(__double_as_longlong(base)) : 0ull);
+        if (lane == __ffs(m) - 1) atomicMax(&S.bmax, bm);
       }
-      if (x > P.band_lo && x < P.sat) {
-        atomicAdd(&st->nband, 1);
-        atomicAdd(reinterpret_cast<unsigned long long*>(&st->sx), static_cast<unsigned long long>(__ldg(M.fx + v)));
-        atomicAdd(reinterpret_cast<unsigned long long*>(&st->sy), static_cast<unsigned long long>(__ldg(M.fy + v)));
-        atomicAdd(reinterpret_cast<unsigned long long*>(&st->sz), static_cast<unsigned long long>(__ldg(M.fz + v)));
-        const unsigned item = static_cast<unsigned>(v) * kSlots + k;
-        if (uf_find(W.parent, item, ep) == item) atomicAdd(&st->ncomp, 1);
+    }
+    long long px = 0, py = 0, pz = 0;
+    if (live) {
+      px = __ldg(M.fx + v);
+      py = __ldg(M.fy + v);
+      pz = __ldg(M.fz + v);
+    }
+    bool cand = false;
+    const int kmax = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(cv));
+    for (int k = 0; k < kmax; ++k) {
+      int a = -1;
+      bool band = false, unsat = false, root = false;
+      if (k < cv) {
+        const int l = F.lay[b + k];
+        const double x = F.val[b + k];
+        if (l != 0 && W.active[l]) {
+          a = W.aidx[l];
+          unsat = x > 0.0 && x < 1.0;
+          if (unsat && x >= P.kappa) cand = true;
+          band = x > P.band_lo && x < P.sat;
+          if (band) {
+            // Unions are complete, so an item is a root iff its parent entry
+            // is stale (never linked this epoch) or points to itself.
+            const unsigned item = static_cast<unsigned>(v) * kSlots + k;
+            const unsigned long long p = W.parent[item];
+            root = (p >> 32) != ep || static_cast<unsigned>(p) == item;
+            if (P.record_trails)
+              bq_push(QB, &W.ctl->nbandpairs, W.bandpairs, make_int2(v, a), W.bandpair_cap, &W.ctl->bandpair_overflow);
+          }
+        }
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, a);
+      const int nunsat = __reduce_add_sync(peers, unsat ? 1 : 0);
+      const int nband = __reduce_add_sync(peers, band ? 1 : 0);
+      const int nroot = __reduce_add_sync(peers, root ? 1 : 0);
+      const long long sx = seg_sum_fx(peers, band ? px : 0);
+      const long long sy = seg_sum_fx(peers, band ? py : 0);
+      const long long sz = seg_sum_fx(peers, band ? pz : 0);
+      if (a >= 0 && lane == __ffs(peers) - 1) {
+        if (a < kSmemLayers) {
+          if (nunsat) atomicAdd(&S.cnt[a][2], nunsat);
+          if (nband) {
+            atomicAdd(&S.cnt[a][1], nband);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&S.sum[a][0]), static_cast<unsigned long long>(sx));
+            atomicAdd(reinterpret_cast<unsigned long long*>(&S.sum[a][1]), static_cast<unsigned long long>(sy));
+            atomicAdd(reinterpret_cast<unsigned long long*>(&S.sum[a][2]), static_cast<unsigned long long>(sz));
+          }
+          if (nroot) atomicAdd(&S.cnt[a][0], nroot);
+        } else {
+          if (nunsat) atomicAdd(&g[a].nunsat, nunsat);
+          if (nband) {
+            atomicAdd(&g[a].nband, nband);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&g[a].sx), static_cast<unsigned long long>(sx));
+            atomicAdd(reinterpret_cast<unsigned long long*>(&g[a].sy), static_cast<unsigned long long>(sy));
+            atomicAdd(reinterpret_cast<unsigned long long*>(&g[a].sz), static_cast<unsigned long long>(sz));
+          }
+          if (nroot) atomicAdd(&g[a].ncomp, nroot);
+        }
       }
     }
     if (cand && !(base > P.coll_base_limit)) {
@@ -478,35 +739,51 @@ __device__ __forceinline__ void band_mean(const DevMesh& M, const LayerStat& st,
   mz = (static_cast<double>(st.sz) * M.fx_scale) / n;
 }
 
-// snap_to_band (diffusion.hpp:590): nearest band vertex to the band mean;
-// packed key = distance bits (low 27 mantissa bits dropped) | vertex.
-__device__ void phase_snap(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P) {
-  const int n = W.ctl->icount;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
-    const int v = W.ilist[idx];
-    const int cv = F.cnt[v];
-    const size_t b = static_cast<size_t>(v) * kSlots;
-    for (int k = 0; k < cv; ++k) {
-      const int l = F.lay[b + k];
-      if (!is_band(W, P, l, F.val[b + k])) continue;
-      const LayerStat* st = W.stat + W.aidx[l];
+// snap_to_band (diffusion.hpp:590) over the recorded band items: nearest band
+// vertex to the band mean; key = distance bits (27 low bits dropped) | vertex.
+__device__ void phase_snap(const DevMesh& M, const DevWork& W, int spar, BlockStats& S) {
+  LayerStat* g = W.stat + static_cast<size_t>(spar) * kMaxActive;
+  const int n = min(W.ctl->nbandpairs, W.bandpair_cap);
+  const int lane = threadIdx.x & 31;
+  const int stride = gridDim.x * blockDim.x;
+  const int trip = (n + stride - 1) / stride;
+  for (int r = 0; r < trip; ++r) {
+    const int i = r * stride + blockIdx.x * blockDim.x + threadIdx.x;
+    int a = -1;
+    unsigned long long key = ~0ull;
+    if (i < n) {
+      const int2 bp = W.bandpairs[i];
+      const int v = bp.x;
+      a = bp.y;
       double mx, my, mz;
-      band_mean(M, *st, mx, my, mz);
+      band_mean(M, g[a], mx, my, mz);
       const double dx = __ldg(M.px + v) - mx, dy = __ldg(M.py + v) - my, dz = __ldg(M.pz + v) - mz;
       const double d2 = dx * dx + dy * dy + dz * dz;
-      const unsigned long long key =
-          (static_cast<unsigned long long>(__double_as_longlong(d2)) & ~kVertMask) | static_cast<unsigned long long>(v);
-      atomicMin(&W.stat[W.aidx[l]].snap, key);
+      key = (static_cast<unsigned long long>(__double_as_longlong(d2)) & ~kVertMask) | static_cast<unsigned long long>(v);
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, a);
+    const unsigned long long kmin = seg_min_u64(peers, key);
+    if (a >= 0 && lane == __ffs(peers) - 1) {
+      if (a < kSmemLayers) atomicMin(&S.snap[a], kmin);
+      else atomicMin(&g[a].snap, kmin);
     }
   }
 }
 
-// Writes the trail record of active index a for a finished check and resets
-// its statistics for the next one.
-__device__ void flush_and_reset_stat(const DevMesh& M, const DevWork& W, const StepParams& P, int a, bool pend,
-                                     long long pend_step) {
-  LayerStat* st = W.stat + a;
-  if (pend && st->nband > 0) {
+__device__ void reset_stat(LayerStat* st) {
+  st->ncomp = 0;
+  st->nband = 0;
+  st->nunsat = 0;
+  st->sx = st->sy = st->sz = 0;
+  st->snap = ~0ull;
+}
+
+// Writes the trail / last-position record of active index a for check step
+// `step` (stats parity spar) and resets those stats for reuse two steps later.
+__device__ void flush_stat(const DevMesh& M, const DevWork& W, const StepParams& P, int a, int spar, long long step,
+                           bool write) {
+  LayerStat* st = W.stat + static_cast<size_t>(spar) * kMaxActive + a;
+  if (write && st->nband > 0) {
     const int layer = W.alist[a];
     double mx, my, mz;
     band_mean(M, *st, mx, my, mz);
@@ -517,7 +794,7 @@ __device__ void flush_and_reset_stat(const DevMesh& M, const DevWork& W, const S
     if (P.record_trails) {
       const int pos = atomicAdd(&W.ctl->ntrail, 1);
       TrailRec r;
-      r.step = pend_step;
+      r.step = step;
       r.layer = layer;
       r.vertex = static_cast<int>(st->snap & kVertMask);
       r.mx = mx;
@@ -526,17 +803,14 @@ __device__ void flush_and_reset_stat(const DevMesh& M, const DevWork& W, const S
       W.trail[pos & (kTrailCap - 1)] = r;
     }
   }
-  st->ncomp = 0;
-  st->nband = 0;
-  st->nunsat = 0;
-  st->sx = st->sy = st->sz = 0;
-  st->snap = ~0ull;
+  reset_stat(st);
 }
 
-__device__ int decide(const DevWork& W, const StepParams& P) {
+__device__ int decide(const DevWork& W, const StepParams& P, int spar) {
+  const LayerStat* g = W.stat + static_cast<size_t>(spar) * kMaxActive;
   int bits = 0;
   for (int a = threadIdx.x; a < P.n_active; a += blockDim.x) {
-    const LayerStat& st = W.stat[a];
+    const LayerStat& st = g[a];
     if (st.ncomp >= 2) bits |= kStopSplit;
     if (st.nband == 0 && st.nunsat == 0) bits |= kStopVanish;
   }
@@ -544,6 +818,7 @@ __device__ int decide(const DevWork& W, const StepParams& P) {
     if (W.ctl->npairs > 0 || W.ctl->pair_overflow) bits |= kStopMerge;
     const double bmax = __longlong_as_double(static_cast<long long>(W.ctl->base_max_bits));
     if (W.ctl->base_one == 0 && bmax < P.extinct_limit) bits |= kStopExtinct;
+    if (W.ctl->bandpair_overflow) bits |= kStopError;
   }
   __shared__ int s_bits;
   if (threadIdx.x == 0) s_bits = 0;
@@ -555,114 +830,215 @@ __device__ int decide(const DevWork& W, const StepParams& P) {
   return r;
 }
 
-// mode 0: run steps; mode 1: check only (stats of the current state);
-// mode 2: snap only (uses the stats and interest list of the last check).
+// mode 0: run steps; mode 1: check only (stats of the current state into
+// stat[step_begin & 1]); mode 2: snap for that check; mode 3: flush it.
 template <int kMode>
-__global__ void __launch_bounds__(kBlock) k_engine(DevMesh M, DevField F, DevWork W, StepParams P) {
+__global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, DevWork W, StepParams P) {
+  __shared__ BlockStats S;
+  __shared__ BlockQueue Q;
+  __shared__ PairQueue QB;
   Ctl* ctl = W.ctl;
+  if (threadIdx.x == 0) {
+    Q.n = 0;
+    QB.n = 0;
+  }
+  __syncthreads();
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int gsz = gridDim.x * blockDim.x;
   unsigned long long ep = static_cast<unsigned long long>(ctl->epoch);
-  bool pend = ctl->trail_pending != 0;
-  long long pend_step = ctl->trail_step;
+  int lpar = ctl->lpar;
 
   if (kMode == 1) {
-    if (gtid < P.n_active) flush_and_reset_stat(M, W, P, gtid, false, 0);
+    const int spar = static_cast<int>(P.step_begin & 1);
+    LayerStat* g = W.stat + static_cast<size_t>(spar) * kMaxActive;
+    for (int a = gtid; a < kMaxActive; a += gsz) reset_stat(g + a);
     if (gtid == 0) {
-      ctl->icount = 0;
       ctl->npairs = 0;
       ctl->pair_overflow = 0;
       ctl->base_max_bits = 0;
+      ctl->nbandpairs = 0;
+      ctl->bandpair_overflow = 0;
     }
     grid_sync(ctl);
     ++ep;
-    phase_band_list(F, W, M.nv, false);
+    phase_union(M, F, W, P, lpar, ep);
     grid_sync(ctl);
-    phase_union(M, F, W, P, ep);
-    grid_sync(ctl);
-    phase_stats(M, F, W, P, ep);
+    block_stats_init(S);
+    phase_stats(M, F, W, P, lpar, spar, ep, false, S, Q, QB);
+    block_stats_flush(S, g, P.n_active, ctl);
+    bq_flush(QB, &ctl->nbandpairs, W.bandpairs, W.bandpair_cap, &ctl->bandpair_overflow);
     grid_sync(ctl);
     if (gtid == 0) ctl->epoch = static_cast<long long>(ep);
     return;
   }
   if (kMode == 2) {
-    phase_snap(M, F, W, P);
+    const int spar = static_cast<int>(P.step_begin & 1);
+    block_stats_init(S);
+    phase_snap(M, W, spar, S);
+    block_stats_flush(S, W.stat + static_cast<size_t>(spar) * kMaxActive, P.n_active);
     return;
   }
-  if (kMode == 3) {  // write trail / last position records for a host-handled check
-    if (gtid < P.n_active) flush_and_reset_stat(M, W, P, gtid, true, P.step_begin);
+  if (kMode == 3) {
+    const int spar = static_cast<int>(P.step_begin & 1);
+    if (gtid < P.n_active) flush_stat(M, W, P, gtid, spar, P.step_begin, true);
     return;
   }
 
+  // ---- mode 0: the step loop.  Per step s:
+  //   1  B(s)  commit, band-list append, next frontier  (+ snap of check s-1)
+  //   2  D(s)  union-find                                (+ trail flush of s-1)
+  //   3  E(s)  stats, collisions, list compaction        (+ speculative A(s+1))
+  // with a grid barrier after each; non-check steps run only 1 and A(s+1).
   long long step = P.step_begin;
   int stop = 0;
-  for (; step < P.step_end; ++step) {
-    const int cur = static_cast<int>(step & 1), nxt = cur ^ 1;
-    const bool check = P.do_check && (step % P.check_interval == 0);
-    // ---- A: update (+ pending trail snap of the previous check)
+  bool pend = false;
+  long long pend_step = 0;
+  {  // prologue: A(step_begin)
+    const int cur = static_cast<int>(step & 1);
     const int nR = ctl->rcount[cur];
     if (gtid == 0) {
-      ctl->rcount[nxt] = 0;
-      ctl->hash_acc = 0;
+      ctl->rcount[cur ^ 1] = 0;
       ctl->sum_region += static_cast<unsigned long long>(nR);
     }
-    for (int i = gtid; i < nR; i += gsz) update_vertex(M, F, W, P, i, W.region[cur][i]);
-    if (pend && P.record_trails) phase_snap(M, F, W, P);
+    for (int i = gtid / kG; i < nR; i += gsz / kG)
+      update_vertex(M, F, W, P, i, W.region[cur][i], false, threadIdx.x & (kG - 1), group_mask());
     grid_sync(ctl);
-    if (ctl->error) {
-      stop = kStopError;
-      break;
-    }
-    // ---- B: commit, next frontier, trail flush, stat reset
-    for (int i = gtid; i < nR; i += gsz) commit_vertex(M, F, W, i, W.region[cur][i], static_cast<int>(step), nxt);
-    if (gtid < P.n_active) flush_and_reset_stat(M, W, P, gtid, pend, pend_step);
-    if (gtid == 0) {
-      ctl->icount = 0;
-      ctl->npairs = 0;
-      ctl->pair_overflow = 0;
-      ctl->base_max_bits = 0;
-    }
-    pend = false;
-    grid_sync(ctl);
-    if (!check) continue;
-    ++ep;
-    // ---- C: interest list (+ digest)
-    phase_band_list(F, W, M.nv, P.do_hash != 0);
-    grid_sync(ctl);
-    // ---- D: union-find over band items
-    phase_union(M, F, W, P, ep);
-    grid_sync(ctl);
-    // ---- E: statistics and collisions
-    phase_stats(M, F, W, P, ep);
-    grid_sync(ctl);
-    if (gtid == 0) ctl->sum_interest += static_cast<unsigned long long>(ctl->icount);
-    if (P.do_hash && gtid == 0) {
-      const long long slot = step - W.hash_base;
-      if (slot >= 0 && slot < W.hash_cap) W.hashes[slot] = ctl->hash_acc;
-    }
-    int bits = decide(W, P);
-    if (P.stop_every_check) bits |= kStopEveryCheck;
-    if (bits) {
-      stop = bits;
-      break;
-    }
-    pend = true;
-    pend_step = step;
+    if (ctl->error) stop = kStopError;
   }
-  if (stop == 0 && pend && P.record_trails) {
-    // Budget exhausted right after a quiet check: finish its trail records.
-    phase_snap(M, F, W, P);
+  for (; stop == 0 && step < P.step_end; ++step) {
+    const int cur = static_cast<int>(step & 1), nxt = cur ^ 1;
+    const bool check = P.do_check && (step % P.check_interval == 0);
+    const bool more = step + 1 < P.step_end;
+    const long long pslot = (step - P.step_begin) * 4;
+    const bool prof = W.prof && gtid == 0 && pslot + 3 < W.prof_cap;
+    if (prof) W.prof[pslot] = gtimer();
+    // ---- 1: B(s)
+    {
+      const int nR = ctl->rcount[cur];
+      for (int i = gtid / kG; i < nR; i += gsz / kG)
+        commit_vertex(M, F, W, i, W.region[cur][i], static_cast<int>(step), nxt, lpar, threadIdx.x & (kG - 1),
+                      group_mask(), Q);
+      bq_flush(Q, &ctl->rcount[nxt], W.region[nxt]);
+      block_stats_init(S);
+      if (pend && P.record_trails) phase_snap(M, W, static_cast<int>(pend_step & 1), S);
+      block_stats_flush(S, W.stat + static_cast<size_t>(pend_step & 1) * kMaxActive, pend ? P.n_active : 0);
+      if (gtid == 0) {
+        ctl->spec_error = 0;
+        ctl->hash_acc = 0;
+      }
+    }
     grid_sync(ctl);
+    if (prof) W.prof[pslot + 1] = gtimer();
+    if (check) {
+      ++ep;
+      // ---- 2: D(s) + flush of the previous check's trail records
+      if (pend)
+        for (int a = gtid; a < P.n_active; a += gsz) flush_stat(M, W, P, a, static_cast<int>(pend_step & 1), pend_step, true);
+      pend = false;
+      if (gtid == 0) {
+        ctl->ilcount[lpar ^ 1] = 0;
+        ctl->npairs = 0;
+        ctl->pair_overflow = 0;
+        ctl->base_max_bits = 0;
+        ctl->nbandpairs = 0;
+      }
+      phase_union(M, F, W, P, lpar, ep);
+      if (P.do_hash) phase_hash(F, W, M.nv);
+      grid_sync(ctl);
+      if (prof) W.prof[pslot + 2] = gtimer();
+      // ---- 3: E(s) + speculative A(s+1)
+      const int spar = cur;
+      block_stats_init(S);
+      phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, QB);
+      block_stats_flush(S, W.stat + static_cast<size_t>(spar) * kMaxActive, P.n_active, ctl);
+      bq_flush(Q, &ctl->ilcount[lpar ^ 1], W.ilist[lpar ^ 1]);
+      bq_flush(QB, &ctl->nbandpairs, W.bandpairs, W.bandpair_cap, &ctl->bandpair_overflow);
+      if (more) {
+        if (P.split_a) {
+          grid_sync(ctl);
+          if (prof) W.prof[pslot + 3] = gtimer();
+        }
+        const int nR1 = ctl->rcount[nxt];
+        if (gtid == 0) {
+          ctl->rcount[cur] = 0;
+          ctl->sum_region += static_cast<unsigned long long>(nR1);
+          ctl->sum_interest += static_cast<unsigned long long>(ctl->ilcount[lpar]);
+        }
+        for (int i = gtid / kG; i < nR1; i += gsz / kG)
+          update_vertex(M, F, W, P, i, W.region[nxt][i], true, threadIdx.x & (kG - 1), group_mask());
+      } else if (gtid == 0) {
+        ctl->sum_interest += static_cast<unsigned long long>(ctl->ilcount[lpar]);
+      }
+      grid_sync(ctl);
+      if (prof && !P.split_a) W.prof[pslot + 3] = gtimer();
+      lpar ^= 1;
+      if (P.do_hash && gtid == 0) {
+        const long long slot = step - W.hash_base;
+        if (slot >= 0 && slot < W.hash_cap) W.hashes[slot] = ctl->hash_acc;
+      }
+      int bits = decide(W, P, spar);
+      if (P.stop_every_check) bits |= kStopEveryCheck;
+      if (bits) {
+        stop = bits;
+        break;  // the speculative A(s+1) is discarded; the host relaunches at s+1
+      }
+      if (ctl->spec_error) {
+        if (gtid == 0) {
+          ctl->error = ctl->spec_error;
+          ctl->error_vertex = ctl->spec_error_vertex;
+        }
+        stop = kStopError;
+        ++step;  // the failing update belongs to step s+1
+        break;
+      }
+      pend = true;
+      pend_step = step;
+    } else {
+      // ---- 3': trail flush of the previous check (its stats parity is
+      // reused two steps later) + A(s+1)
+      if (pend)
+        for (int a = gtid; a < P.n_active; a += gsz) flush_stat(M, W, P, a, static_cast<int>(pend_step & 1), pend_step, true);
+      pend = false;
+      if (more) {
+        const int nR1 = ctl->rcount[nxt];
+        if (gtid == 0) {
+          ctl->rcount[cur] = 0;
+          ctl->sum_region += static_cast<unsigned long long>(nR1);
+        }
+        for (int i = gtid / kG; i < nR1; i += gsz / kG)
+          update_vertex(M, F, W, P, i, W.region[nxt][i], false, threadIdx.x & (kG - 1), group_mask());
+      }
+      grid_sync(ctl);
+      if (ctl->error) {
+        stop = kStopError;
+        ++step;
+        break;
+      }
+    }
   }
   if (stop == 0 && pend) {
-    if (gtid < P.n_active) flush_and_reset_stat(M, W, P, gtid, true, pend_step);
-    pend = false;
+    // Budget exhausted right after a quiet check: finish its trail records.
+    block_stats_init(S);
+    if (P.record_trails) phase_snap(M, W, static_cast<int>(pend_step & 1), S);
+    block_stats_flush(S, W.stat + static_cast<size_t>(pend_step & 1) * kMaxActive, P.n_active);
+    grid_sync(ctl);
+    for (int a = gtid; a < P.n_active; a += gsz) flush_stat(M, W, P, a, static_cast<int>(pend_step & 1), pend_step, true);
   }
   if (gtid == 0) {
     ctl->stop_bits = stop;
     ctl->stop_step = stop ? step : step - 1;
     ctl->epoch = static_cast<long long>(ep);
-    ctl->trail_pending = 0;
+    ctl->lpar = lpar;
+  }
+}
+
+// Barrier microbenchmark (diagnostics): n grid barriers, no work.
+__global__ void __launch_bounds__(kBlock, 1) k_barrier_bench(Ctl* ctl, int n, int mode) {
+  if (mode == 0) {
+    for (int i = 0; i < n; ++i) grid_sync(ctl);
+  } else {
+    cooperative_groups::grid_group g = cooperative_groups::this_grid();
+    for (int i = 0; i < n; ++i) g.sync();
   }
 }
 
@@ -692,9 +1068,8 @@ int dev_max_coresident_blocks(int* out) {
   if (e != cudaSuccess) return static_cast<int>(e);
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_engine<0>, kBlock, 0);
   if (e != cudaSuccess) return static_cast<int>(e);
-  int per1 = 0, per2 = 0;
+  int per1 = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k_engine<1>, kBlock, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_engine<2>, kBlock, 0);
   if (per1 < per) per = per1;
   *out = sms * (per < 1 ? 1 : per);
   return 0;
@@ -724,4 +1099,28 @@ int launch_flush(const DevMesh& m, const DevField& f, const DevWork& w, const St
   return static_cast<int>(cudaGetLastError());
 }
 
+}  // namespace dtb
+
+namespace dtb {
+// Returns nanoseconds per grid barrier (mode 0: engine barrier, 1: cooperative_groups).
+double bench_barrier(int blocks, int n, int mode) {
+  Ctl* ctl = nullptr;
+  cudaMalloc(&ctl, sizeof(Ctl));
+  cudaMemset(ctl, 0, sizeof(Ctl));
+  void* args[] = {&ctl, &n, &mode};
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_barrier_bench), dim3(blocks), dim3(kBlock), args, 0, 0);
+  cudaEventRecord(a);
+  cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&k_barrier_bench), dim3(blocks), dim3(kBlock), args, 0, 0);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaFree(ctl);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return ms * 1e6 / n;
+}
 }  // namespace dtb

@@ -20,6 +20,52 @@
 #include <cstddef>
 #include <cstdint>
 
+#include <vector_types.h>  // int2, uint4 (CUDA header, usable from host C++)
+
+namespace dtb {
+constexpr unsigned kBandOverflow = 0xFFFFu;
+}
+
+#ifdef __CUDACC__
+namespace dtb {
+// Band index of a column (see DevField::binfo).
+__device__ __forceinline__ uint4 make_binfo(const unsigned short* lay, const double* val, int c, double lo,
+                                            double sat) {
+  unsigned L[4] = {0, 0, 0, 0}, S[4] = {0, 0, 0, 0};
+  int n = 0;
+  bool over = false;
+  for (int j = 0; j < c; ++j) {
+    const unsigned l = lay[j];
+    const double x = val[j];
+    if (l != 0 && x > lo && x < sat) {
+      if (n < 4) {
+        L[n] = l;
+        S[n] = static_cast<unsigned>(j);
+        ++n;
+      } else {
+        over = true;
+      }
+    }
+  }
+  uint4 r;
+  r.x = L[0] | (L[1] << 16);
+  r.y = L[2] | (L[3] << 16);
+  r.z = S[0] | (S[1] << 16);
+  r.w = S[2] | ((over ? kBandOverflow : S[3]) << 16);
+  return r;
+}
+__device__ __forceinline__ unsigned binfo_layer(const uint4& b, int t) {
+  const unsigned w = t < 2 ? b.x : b.y;
+  return (w >> (16 * (t & 1))) & 0xFFFFu;
+}
+__device__ __forceinline__ unsigned binfo_slot(const uint4& b, int t) {
+  const unsigned w = t < 2 ? b.z : b.w;
+  return (w >> (16 * (t & 1))) & 0xFFFFu;
+}
+__device__ __forceinline__ bool binfo_overflow(const uint4& b) { return (b.w >> 16) == kBandOverflow; }
+}  // namespace dtb
+#endif
+
 namespace dtb {
 
 constexpr int kSlots = 16;         // max owners per vertex (column capacity)
@@ -27,7 +73,7 @@ constexpr int kMaxLayers = 65535;  // layer ids are u16
 constexpr int kMaxActive = 4096;   // simultaneously active non-base layers
 constexpr int kPairCap = 1 << 16;  // collision pair hash table slots
 constexpr int kTrailCap = 1 << 20; // device trail ring capacity (records)
-constexpr int kBlock = 256;        // threads per CTA for all engine kernels
+constexpr int kBlock = 512;        // threads per CTA for all engine kernels
 
 // Error codes raised by device code (mirrored in mesh.hpp ErrorCode).
 enum DevError : int {
@@ -63,26 +109,28 @@ struct DevMesh {
 
 // Control block in device memory (one per engine).
 struct Ctl {
-  int rcount[2];             // region list sizes (parity = step & 1)
-  int icount;                // interest list size
-  int error;                 // DevError
+  int rcount[2];             // frontier list sizes (parity = step & 1)
+  int ilcount[2];            // band-list sizes (double buffer, parity lpar)
+  int lpar;                  // which band list is current
+  int error;                 // DevError of a committed step
   int error_vertex;
+  int spec_error;            // error raised by a speculative update (next step)
+  int spec_error_vertex;
   int stop_bits;
   long long stop_step;       // last step executed by the kernel
   long long epoch;           // union-find / pair-set version
   int base_one;              // number of vertices whose base value is exactly 1.0
-  int pad0;
+  int nbandpairs;            // (vertex, layer) band items recorded by the last check
   unsigned long long base_max_bits;  // max base value in (0,1) (as ordered bits)
   int npairs;                // collision pairs recorded this check
   int pair_overflow;
   int ntrail;                // trail records written (ring index)
-  int trail_pending;         // a snap for the previous check step is outstanding
-  long long trail_step;      // step of the pending snap
+  int bandpair_overflow;
   unsigned bar_count;        // grid barrier
   unsigned bar_gen;
   unsigned long long hash_acc;  // field digest accumulator
   unsigned long long sum_region;    // work counters: frontier vertices updated
-  unsigned long long sum_interest;  // interest (band) vertices checked
+  unsigned long long sum_interest;  // band-list vertices checked
 };
 
 struct LayerStat {
@@ -101,7 +149,10 @@ struct DevField {
   unsigned char *cnt = nullptr;   // nv
   unsigned short *lay = nullptr;  // nv * kSlots
   double *val = nullptr;          // nv * kSlots
-  unsigned char *interest = nullptr;
+  unsigned char *interest = nullptr;  // column holds a value strictly inside (0, 1)
+  // Band index per vertex: up to 4 (layer, slot) pairs whose value lies in
+  // (band_lo, sat), any activity; w's high half = 0xFFFF marks overflow.
+  uint4 *binfo = nullptr;
 };
 
 struct DevWork {
@@ -111,12 +162,15 @@ struct DevWork {
   unsigned short *slay = nullptr;
   double *sval = nullptr;
   unsigned char *sflag = nullptr;
-  int *ilist = nullptr;                 // interest list
+  int *ilist[2] = {nullptr, nullptr};   // band lists (double buffer); dead entries skipped
+  unsigned char *in_list = nullptr;     // vertex is in the current band list
+  int2 *bandpairs = nullptr;            // (vertex, dense active index) band items of the last check
+  int bandpair_cap = 0;
   unsigned long long *parent = nullptr; // nv * kSlots versioned UF parents
   unsigned char *active = nullptr;      // kMaxLayers + 1
   int *aidx = nullptr;                  // layer -> dense active index or -1
   int *alist = nullptr;                 // dense active index -> layer
-  LayerStat *stat = nullptr;            // kMaxActive
+  LayerStat *stat = nullptr;            // 2 x kMaxActive (parity = step & 1)
   unsigned long long *pair_keys = nullptr;  // kPairCap versioned keys
   unsigned *pairs = nullptr;            // recorded pairs (first << 16 | second)
   double *lastpos = nullptr;            // 4 * (kMaxLayers + 1): x, y, z, valid
@@ -124,6 +178,9 @@ struct DevWork {
   unsigned long long *hashes = nullptr; // per-step field digests (optional)
   long long hash_base = 0;              // step of hashes[0]
   int hash_cap = 0;
+  double band_lo = 0.05, sat = 0.999;  // band thresholds of the run (binfo maintenance)
+  unsigned long long *prof = nullptr;  // optional phase timestamps (4 per step)
+  int prof_cap = 0;
   Ctl *ctl = nullptr;
 };
 
@@ -137,6 +194,8 @@ struct StepParams {
   int do_hash;
   int stop_every_check;
   int do_check;  // 0: advance only (one-shot step())
+  int split_a;   // diagnostics: run the next step's update in its own phase
+  int split_a_no_unite;  // diagnostics only: skip unions (wrong results; timing)
 };
 
 // --- launchers (kernels.cu) -------------------------------------------------
@@ -168,6 +227,16 @@ struct LapBuild {
   int *nnz;                    // out
 };
 int launch_assemble(const LapBuild& b, void* stream);
+
+// Mesh arrays built on the device (meshdev.cu).
+struct FrontBuild {
+  int nv;
+  const unsigned *faces, *face_edges, *edge_faces, *edges;  // 3F, 3F, 2E, 2E
+  const int *v2v_off, *v2v, *v2f_off, *v2f;
+};
+int launch_positions(const double* xyz, int nv, double scale, double* px, double* py, double* pz, long long* fx,
+                     long long* fy, long long* fz, void* stream);
+int launch_front_csr(const FrontBuild& b, int* c_off, int** c_col, int* nnz, void* stream);
 int launch_spmv(int nv, const int* off, const int* col, const double* val, const double* mass,
                 const double* x, double* y, void* stream);
 

@@ -134,8 +134,10 @@ Mesh::Mesh(std::vector<V3> vertices, std::vector<std::array<Index, 3>> faces)
 // visited face means the surface is non-orientable.  The result is then
 // flipped globally if the enclosed signed volume is negative.
 void Mesh::orient() {
-  const std::vector<std::uint32_t> partner = pair_slots(faces_, nv());
-  std::vector<char> flipped(faces_.size(), 0);
+  partner_ = pair_slots(faces_, nv());
+  const std::vector<std::uint32_t>& partner = partner_;
+  flipped_.assign(faces_.size(), 0);
+  std::vector<char>& flipped = flipped_;
   // Current corner-pair k of face f maps to an original slot: identity when
   // unflipped; after swap(t1,t2) the pairs (t0,t2),(t2,t1),(t1,t0) are the
   // original slots 2,1,0.
@@ -174,16 +176,31 @@ void Mesh::orient() {
   if (reached != faces_.size()) fail(kTopologyError, "mesh has multiple connected components");
   double vol = 0;
   for (const auto& t : faces_) vol += dot(pos_[t[0]], cross(pos_[t[1]], pos_[t[2]])) / 6.0;
-  if (vol < 0)
+  if (vol < 0) {
     for (auto& t : faces_) std::swap(t[1], t[2]);
+    for (char& fl : flipped_) fl ^= 1;
+  }
 }
 
 // Edges are numbered by first appearance over (face, corner) in order
 // (mesh.hpp:272-293); vertex->face lists are in face order, vertex->vertex
 // lists sorted.
 void Mesh::index() {
-  const std::vector<std::uint32_t> partner = pair_slots(faces_, nv());
+  // Slot pairing of the final orientation, derived from orient()'s pairing of
+  // the input corners: final corner pair k of face f is input slot
+  // 3f + (flipped ? 2 - k : k).
   const std::size_t ns = faces_.size() * 3;
+  std::vector<std::uint32_t> partner(ns);
+  for (std::size_t s = 0; s < ns; ++s) {
+    const std::size_t f = s / 3;
+    const int k = static_cast<int>(s % 3);
+    const std::uint32_t orig = static_cast<std::uint32_t>(3 * f + (flipped_[f] ? 2 - k : k));
+    const std::uint32_t po = partner_[orig];
+    const std::uint32_t g = po / 3, kg = po % 3;
+    partner[s] = 3 * g + (flipped_[g] ? 2 - kg : kg);
+  }
+  std::vector<std::uint32_t>().swap(partner_);
+  std::vector<char>().swap(flipped_);
   std::vector<Index> slot_edge(ns, kInvalid);
   edge_v_.clear();
   edge_f_.clear();

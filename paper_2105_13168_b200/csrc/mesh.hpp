@@ -116,6 +116,8 @@ class Mesh {
   std::vector<std::array<Index, 3>> face_e_;
   std::vector<std::uint32_t> v2f_off_, v2v_off_;
   std::vector<Index> v2f_, v2v_;
+  std::vector<std::uint32_t> partner_;  // construction scratch: input-corner slot pairing
+  std::vector<char> flipped_;           // construction scratch: faces flipped by orient()
 };
 
 // --- synthetic generators (generators.hpp) ---------------------------------
