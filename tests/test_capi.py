@@ -56,3 +56,14 @@ def test_device_calls_fail_loudly_without_gpu():
     assert e.value.kind == "CudaError"
     with pytest.raises(dt.DiffTopoError):
         dt.LayerField(m, [0])
+
+
+def test_cpp_facade_compiles(tmp_path):
+    """The C++ drop-in header (include/difftopo_b200.hpp) compiles and links
+    against the library exactly as a reference user's program would."""
+    import subprocess
+    exe = tmp_path / "detect_loops"
+    subprocess.run(["g++", "-O2", "-std=c++17", "-Wall", "-Werror", f"-I{ROOT}/include",
+                    f"{ROOT}/examples/detect_loops.cpp", f"-L{ROOT}/paper_2105_13168_b200/lib", "-ldifftopo_b200",
+                    f"-Wl,-rpath,{ROOT}/paper_2105_13168_b200/lib", "-o", str(exe)], check=True)
+    assert exe.exists()

@@ -101,3 +101,16 @@ def test_repeated_passes_reuse_workspace():
     assert [int(h) for h in b.hashes()] == ha
     c = dt.run_initial_pass(mesh, op, 7, cfg)  # different seed: different trajectory
     assert [int(h) for h in c.hashes()] != ha
+
+
+def test_cpp_facade_runs(tmp_path):
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "detect_loops"
+    subprocess.run(["g++", "-O2", "-std=c++17", f"-I{root}/include", f"{root}/examples/detect_loops.cpp",
+                    f"-L{root}/paper_2105_13168_b200/lib", "-ldifftopo_b200",
+                    f"-Wl,-rpath,{root}/paper_2105_13168_b200/lib", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe), "icosphere:3:2.0"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    assert '"status":0' in out.stdout and "vanish" in out.stdout and "cycle_rank 0" in out.stdout
