@@ -921,7 +921,7 @@ class PassEngine {
     field_->mark_region(op_.view(), sv, 0, 1);
     blocks_ = engine_blocks(static_cast<int>(mesh_.nv()));
     if (const char* env = std::getenv("DTB_PHASE_PROF"); env && env[0] == '1') {
-      prof_.alloc(4 * static_cast<size_t>(std::min<long>(cfg_.max_steps, 100000)) + 8);
+      prof_.alloc(4 * static_cast<size_t>(std::min<long>(cfg_.max_steps, 100000)) + 8 + 2 * 64 * 3 * 160 + 64);
       prof_.zero(s_);
     }
   }
@@ -1332,7 +1332,8 @@ class PassEngine {
     std::vector<unsigned long long> t = to_host(prof_, prof_.n, s_);
     double sum[3] = {0, 0, 0}, tot = 0;
     long n = 0;
-    for (size_t i = 0; i + 4 < t.size(); i += 4) {
+    const size_t nstep_slots = 4 * static_cast<size_t>(std::min<long>(cfg_.max_steps, 100000));
+    for (size_t i = 0; i + 4 < nstep_slots; i += 4) {
       if (!t[i] || !t[i + 3] || !t[i + 4]) continue;
       sum[0] += static_cast<double>(t[i + 1] - t[i]);
       sum[1] += static_cast<double>(t[i + 2] - t[i + 1]);
@@ -1343,6 +1344,45 @@ class PassEngine {
     if (n)
       std::fprintf(stderr, "[dtb] phase us/step over %ld steps: B %.2f  D %.2f  E(+A) %.2f  step %.2f (blocks %d)\n", n,
                    sum[0] / n / 1e3, sum[1] / n / 1e3, sum[2] / n / 1e3, tot / n / 1e3, blocks_);
+    {
+      const size_t tb = t.size() - 64 * 3 * static_cast<size_t>(blocks_) - 16;
+      std::fprintf(stderr, "[dtb]   trace (last D item of CTA0/thread0, us from phase start): list+binfo %.2f  active %.2f  probe %.2f  unite %.2f\n",
+                   (t[tb + 1] - t[tb]) / 1e3, (t[tb + 2] - t[tb]) / 1e3, (t[tb + 3] - t[tb]) / 1e3, (t[tb + 4] - t[tb]) / 1e3);
+    }
+    // Per-CTA completion spread within each phase (steps 8..63 of the first launch).
+    const size_t base = t.size() - 64 * 3 * static_cast<size_t>(blocks_);
+    for (int ph = 0; ph < 3; ++ph) {
+      std::vector<double> lat;
+      const long off = std::min<long>(cfg_.max_steps, 100000) - 64;  // trace covers the launch's last 64 steps
+      for (long st = 8; st < 64; ++st) {
+        const unsigned long long t0 = off >= 0 ? t[4 * (off + st) + ph] : 0;  // phase start = previous phase's barrier exit
+        if (!t0) continue;
+        for (int b = 0; b < blocks_; ++b) {
+          const unsigned long long tb = t[base + (st * 3 + ph) * blocks_ + b];
+          if (tb > t0) lat.push_back(static_cast<double>(tb - t0) / 1e3);
+        }
+      }
+      if (lat.empty()) continue;
+      std::vector<double> work, skew;
+      const size_t sbase = t.size() - 2 * 64 * 3 * static_cast<size_t>(blocks_) - 16;
+      for (long st = 8; st < 64; ++st)
+        for (int b = 0; b < blocks_; ++b) {
+          const unsigned long long ts = t[sbase + (st * 3 + ph) * blocks_ + b];
+          const unsigned long long td = t[base + (st * 3 + ph) * blocks_ + b];
+          const unsigned long long t0 = off >= 0 ? t[4 * (off + st) + ph] : 0;
+          if (ts && td > ts) work.push_back(static_cast<double>(td - ts) / 1e3);
+          if (ts && t0 && ts > t0) skew.push_back(static_cast<double>(ts - t0) / 1e3);
+        }
+      std::sort(work.begin(), work.end());
+      std::sort(skew.begin(), skew.end());
+      if (!work.empty() && !skew.empty())
+        std::fprintf(stderr, "[dtb]   phase %d CTA work (us): p50 %.2f p90 %.2f max %.2f | start skew p50 %.2f p90 %.2f max %.2f\n",
+                     ph, work[work.size() / 2], work[work.size() * 9 / 10], work.back(), skew[skew.size() / 2],
+                     skew[skew.size() * 9 / 10], skew.back());
+      std::sort(lat.begin(), lat.end());
+      std::fprintf(stderr, "[dtb]   phase %d CTA done after start (us): min %.2f p50 %.2f p90 %.2f max %.2f\n", ph,
+                   lat.front(), lat[lat.size() / 2], lat[lat.size() * 9 / 10], lat.back());
+    }
   }
 
   std::shared_ptr<DeviceMesh> dm_;

@@ -64,6 +64,28 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+// Diagnostics (DTB_PHASE_PROF): per-CTA completion time of phase `ph` of the
+// first 64 steps of a launch, recorded just before the grid barrier.
+__device__ __forceinline__ unsigned long long gtimer_raw() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void block_done(const DevWork& W, long long rel_step, int ph) {
+  if (!W.prof || rel_step < 0 || rel_step >= 64) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const long long base = W.prof_cap - 64LL * 3 * gridDim.x;
+    W.prof[base + (rel_step * 3 + ph) * gridDim.x + blockIdx.x] = gtimer_raw();
+  }
+}
+// Per-CTA phase start (barrier exit) for steps < 64: second table below the first.
+__device__ __forceinline__ void block_start(const DevWork& W, long long rel_step, int ph) {
+  if (!W.prof || rel_step < 0 || rel_step >= 64 || threadIdx.x != 0) return;
+  const long long base = W.prof_cap - 2 * 64LL * 3 * gridDim.x - 16;
+  W.prof[base + (rel_step * 3 + ph) * gridDim.x + blockIdx.x] = gtimer_raw();
+}
+
 __device__ __forceinline__ void grid_sync(Ctl*) {
   // cooperative_groups' grid barrier measured 1.2 us vs 2.6 us for a
   // counter/generation barrier with gpu-scope fences (148 CTAs, B200).
@@ -326,6 +348,326 @@ __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork
   }
 }
 
+// ---------------------------------------------------------------------------
+// Register-resident fast path of update_vertex for the common case -- at most
+// kF owners at v, at most kF candidate layers, at most 8 owners afterwards.
+// Every array index is a compile-time constant after unrolling, so nothing
+// spills to local memory; the arithmetic (and its order) is exactly the slow
+// path's.  Returns false, with no side effects, when the case does not fit.
+constexpr int kF = 4;
+constexpr int kN = 8;
+constexpr int kNoLayer = 0x10000;  // sorts after every layer id
+
+__device__ __forceinline__ void cand_add_reg(int (&Cl)[kF], double (&Ca)[kF], int& nc, bool& over, int l, double t) {
+  bool found = false;
+#pragma unroll
+  for (int c = 0; c < kF; ++c)
+    if (c < nc && Cl[c] == l) {
+      Ca[c] = Ca[c] + t;
+      found = true;
+    }
+  if (found) return;
+  if (nc == kF) {
+    over = true;
+    return;
+  }
+#pragma unroll
+  for (int c = 0; c < kF; ++c)
+    if (c == nc) {
+      Cl[c] = l;
+      Ca[c] = 0.0;
+      Ca[c] = Ca[c] + t;
+    }
+  ++nc;
+}
+
+// Inserts (l, x) into the sorted register column E[0..n).
+__device__ __forceinline__ void reg_insert(int (&El)[kN], double (&Ex)[kN], int& n, int l, double x) {
+  int pos = 0;
+#pragma unroll
+  for (int j = 0; j < kN; ++j)
+    if (j < n && El[j] < l) ++pos;
+#pragma unroll
+  for (int j = kN - 1; j > 0; --j)
+    if (j > pos && j <= n) {
+      El[j] = El[j - 1];
+      Ex[j] = Ex[j - 1];
+    }
+#pragma unroll
+  for (int j = 0; j < kN; ++j)
+    if (j == pos) {
+      El[j] = l;
+      Ex[j] = x;
+    }
+  ++n;
+}
+
+__device__ bool update_vertex_fast(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P, int i,
+                                   int v, bool spec, int lane, unsigned gm) {
+  const int cv = F.cnt[v];
+  if (cv > kF) return false;
+  const size_t vb = static_cast<size_t>(v) * kSlots;
+  int Ol[kF];
+  double Ox[kF];
+#pragma unroll
+  for (int q = 0; q < kF; ++q) {
+    Ol[q] = q < cv ? static_cast<int>(F.lay[vb + q]) : kNoLayer;
+    Ox[q] = q < cv ? F.val[vb + q] : 0.0;
+  }
+  const double phib = (cv > 0 && Ol[0] == 0) ? Ox[0] : 0.0;
+
+  int Cl[kF];
+  double Ca[kF];
+#pragma unroll
+  for (int c = 0; c < kF; ++c) {
+    Cl[c] = kNoLayer;
+    Ca[c] = 0.0;
+  }
+  int nc = 0;
+  bool over = false;
+  double lapb = 0.0, lapt = 0.0;
+  bool bnear = phib > 0.0;
+  const int k0 = __ldg(M.s_off + v), k1 = __ldg(M.s_off + v + 1);
+  for (int kb = k0; kb < k1; kb += kG) {
+    const int k = kb + lane;
+    const bool valid = k < k1;
+    int u = 0, cu = 0;
+    double s = 0.0, bu = 0.0, au = 0.0;
+    unsigned short L[kReg];
+    double X[kReg];
+#pragma unroll
+    for (int q = 0; q < kReg; ++q) {
+      L[q] = 0;
+      X[q] = 0.0;
+    }
+    if (valid) {
+      u = __ldg(M.s_col + k);
+      s = __ldg(M.s_val + k);
+      cu = F.cnt[u];
+      const size_t b = static_cast<size_t>(u) * kSlots;
+#pragma unroll
+      for (int q = 0; q < kReg; ++q)
+        if (q < cu) {
+          L[q] = F.lay[b + q];
+          X[q] = F.val[b + q];
+        }
+#pragma unroll
+      for (int q = 0; q < kReg; ++q)
+        if (q < cu) {
+          if (L[q] == 0) bu = X[q];
+          else if (W.active[L[q]]) au = au + X[q];
+        }
+      for (int q = kReg; q < cu; ++q) {
+        const int l = F.lay[b + q];
+        const double x = F.val[b + q];
+        if (l == 0) bu = x;
+        else if (W.active[l]) au = au + x;
+      }
+    }
+    const int nvalid = min(kG, k1 - kb);
+    for (int jj = 0; jj < nvalid; ++jj) {
+      const double s_ = __shfl_sync(gm, s, jj, kG);
+      const int cu_ = __shfl_sync(gm, cu, jj, kG);
+      const double bu_ = __shfl_sync(gm, bu, jj, kG);
+      const double au_ = __shfl_sync(gm, au, jj, kG);
+      lapb = lapb + s_ * bu_;
+      lapt = lapt + s_ * au_;
+      if (bu_ > 0.0) bnear = true;
+#pragma unroll
+      for (int q = 0; q < kReg; ++q) {
+        const int l_ = __shfl_sync(gm, static_cast<int>(L[q]), jj, kG);
+        const double x_ = __shfl_sync(gm, X[q], jj, kG);
+        if (q < cu_ && l_ != 0 && W.active[l_]) cand_add_reg(Cl, Ca, nc, over, l_, s_ * x_);
+      }
+      if (cu_ > kReg) {
+        const int u_ = __shfl_sync(gm, u, jj, kG);
+        const size_t b = static_cast<size_t>(u_) * kSlots;
+        for (int q = kReg; q < cu_; ++q) {
+          const int l_ = F.lay[b + q];
+          if (l_ != 0 && W.active[l_]) cand_add_reg(Cl, Ca, nc, over, l_, s_ * F.val[b + q]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kF; ++q)  // own layers (missing diagonal; never on valid meshes)
+    if (q < cv && Ol[q] != 0 && W.active[Ol[q]]) {
+      bool found = false;
+#pragma unroll
+      for (int c = 0; c < kF; ++c) found |= (c < nc && Cl[c] == Ol[q]);
+      if (!found) cand_add_reg(Cl, Ca, nc, over, Ol[q], 0.0);
+    }
+  if (over) return false;
+
+  const double mass = __ldg(M.mass + v);
+  const double lap_b = lapb / mass;
+  bool touched = false;
+  bool Cupd[kF];
+  double Cn[kF];
+#pragma unroll
+  for (int c = 0; c < kF; ++c) {
+    Cupd[c] = false;
+    Cn[c] = 0.0;
+    if (c >= nc) continue;
+    double phi = 0.0;
+#pragma unroll
+    for (int q = 0; q < kF; ++q)
+      if (Ol[q] == Cl[c]) phi = Ox[q];
+    if (phi == 0.0 && phib <= P.prune) continue;
+    const double lap_i = Ca[c] / mass;
+    const double inner = P.w * (phib - phi) + P.half_a2 * (lap_b - lap_i) - P.e * sqrt(max0(phi * phib));
+    const double rate = -P.mu_n * inner;
+    if (!isfinite(rate)) {
+      raise_error(W.ctl, kDevBlowup, v, spec);
+      return true;
+    }
+    const double next = clamp01(phi + P.dt * rate);
+    if (next != phi) {
+      touched = true;
+      Cupd[c] = true;
+      Cn[c] = next;
+    }
+  }
+  bool bupd = false;
+  double bnext = 0.0;
+  if (bnear) {
+    double total = 0.0, contact = 0.0;
+#pragma unroll
+    for (int q = 0; q < kF; ++q)
+      if (q < cv && Ol[q] != 0 && W.active[Ol[q]]) total = total + Ox[q];
+#pragma unroll
+    for (int q = 0; q < kF; ++q)
+      if (q < cv && Ol[q] != 0 && W.active[Ol[q]]) contact = contact + sqrt(max0(phib * Ox[q]));
+    const double lap_total = lapt / mass;
+    const double rate = -P.mu_n * (P.w * total + P.half_a2 * lap_total + P.e * contact) +
+                        P.m_mu_n * (P.w * phib + P.half_a2 * lap_b);
+    if (!isfinite(rate)) {
+      raise_error(W.ctl, kDevBlowup, v, spec);
+      return true;
+    }
+    const double next = clamp01(phib + P.dt * rate);
+    if (next != phib) {
+      touched = true;
+      bupd = true;
+      bnext = next;
+    }
+  }
+  // Apply the updates with set_value semantics into a sorted register column.
+  bool changed = false;
+  int El[kN];
+  double Ex[kN];
+#pragma unroll
+  for (int j = 0; j < kN; ++j) {
+    El[j] = kNoLayer;
+    Ex[j] = 0.0;
+  }
+  int n = 0;
+#pragma unroll
+  for (int q = 0; q < kF; ++q) {
+    if (q >= cv) continue;
+    double val = Ox[q];
+    bool upd = false;
+    if (Ol[q] == 0) {
+      if (bupd) {
+        val = bnext;
+        upd = true;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < kF; ++c)
+        if (Cupd[c] && Cl[c] == Ol[q]) {
+          val = Cn[c];
+          upd = true;
+        }
+    }
+    if (upd) {
+      if (val > 1.0) val = 1.0;
+      if (val < P.prune) val = 0.0;
+      if (val != Ox[q]) changed = true;
+    }
+    if (val != 0.0) {
+#pragma unroll
+      for (int j = 0; j < kN; ++j)
+        if (j == n) {
+          El[j] = Ol[q];
+          Ex[j] = val;
+        }
+      ++n;
+    }
+  }
+  if (bupd && phib == 0.0) {  // base enters the column
+    double val = bnext;
+    if (val > 1.0) val = 1.0;
+    if (val < P.prune) val = 0.0;
+    if (val != 0.0) {
+      reg_insert(El, Ex, n, 0, val);
+      changed = true;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kF; ++c) {
+    if (!Cupd[c]) continue;
+    bool present = false;
+#pragma unroll
+    for (int q = 0; q < kF; ++q) present |= (Ol[q] == Cl[c]);
+    if (present) continue;
+    double val = Cn[c];
+    if (val > 1.0) val = 1.0;
+    if (val < P.prune) val = 0.0;
+    if (val != 0.0) {
+      reg_insert(El, Ex, n, Cl[c], val);
+      changed = true;
+    }
+  }
+  // Column normalisation of touched vertices (layer_field.hpp:143).
+  if (touched) {
+    double ssum = 0.0;
+#pragma unroll
+    for (int j = 0; j < kN; ++j)
+      if (j < n) ssum = ssum + Ex[j];
+    if (ssum <= 0.0) {
+      raise_error(W.ctl, kDevZeroColumn, v, spec);
+      return true;
+    }
+    if (!(fabs(ssum - 1.0) < 1e-15)) {
+      int m = 0;
+#pragma unroll
+      for (int j = 0; j < kN; ++j) {
+        if (j >= n) continue;
+        double q = Ex[j] / ssum;
+        if (q > 1.0) q = 1.0;
+        if (q < P.prune) q = 0.0;
+        if (q != Ex[j]) changed = true;
+        if (q != 0.0) {
+          const int l = El[j];
+#pragma unroll
+          for (int t = 0; t < kN; ++t)
+            if (t == m) {
+              El[t] = l;
+              Ex[t] = q;
+            }
+          ++m;
+        }
+      }
+      n = m;
+    }
+  }
+  const bool old_one = cv > 0 && Ol[0] == 0 && Ox[0] == 1.0;
+  const bool new_one = n > 0 && El[0] == 0 && Ex[0] == 1.0;
+  const size_t o = static_cast<size_t>(i) * kSlots;
+#pragma unroll
+  for (int j = 0; j < kN; ++j)
+    if (j == lane && j < n) {
+      W.slay[o + j] = static_cast<unsigned short>(El[j]);
+      W.sval[o + j] = Ex[j];
+    }
+  if (lane == 0) {
+    W.scnt[i] = static_cast<unsigned char>(n);
+    W.sflag[i] = static_cast<unsigned char>((changed ? 1 : 0) | (old_one ? 2 : 0) | (new_one ? 4 : 0));
+  }
+  return true;
+}
+
 // Warp-aggregated slot reservation: one atomic per warp and round instead of
 // one per appended item (frontier and band lists see thousands per step).
 __device__ __forceinline__ int agg_slot(int* counter, bool want) {
@@ -446,10 +788,18 @@ __device__ __forceinline__ unsigned long long uf_key(unsigned x) {
 }
 
 __device__ void uf_unite(unsigned long long* par, unsigned a, unsigned b, unsigned long long ep) {
+  const unsigned a0 = a, b0 = b;
   while (true) {
     a = uf_find(par, a, ep);
     b = uf_find(par, b, ep);
-    if (a == b) return;
+    if (a == b) {
+      // Shortcut both starting items to the common root: later finds from
+      // them (each item takes part in ~6 unions per step) are one hop.
+      const unsigned long long r = (ep << 32) | a;
+      if (a0 != a) par[a0] = r;
+      if (b0 != a) par[b0] = r;
+      return;
+    }
     if (uf_key(a) > uf_key(b)) {
       const unsigned t = a;
       a = b;
@@ -538,15 +888,18 @@ __device__ __forceinline__ int band_slot_of(const DevField& F, const DevWork& W,
 }
 
 __device__ void phase_union(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P, int lpar,
-                            unsigned long long ep) {
+                            unsigned long long ep, int g0, int ng) {
   const int n = W.ctl->ilcount[lpar];
   const int* list = W.ilist[lpar];
   const int lane = threadIdx.x & (kG - 1);
-  const int g0 = (blockIdx.x * blockDim.x + threadIdx.x) / kG, ng = gridDim.x * blockDim.x / kG;
+  const bool trace = W.prof && blockIdx.x == 0 && threadIdx.x == 0;
+  unsigned long long* tr = trace ? W.prof + (W.prof_cap - 64LL * 3 * gridDim.x - 16) : nullptr;
+  if (trace) tr[0] = gtimer_raw();
   for (int idx = g0; idx < n; idx += ng) {
     const int v = list[idx];
     if (!F.interest[v]) continue;
     const uint4 bv = F.binfo[v];
+    if (trace) tr[1] = gtimer_raw() + (bv.x & 0);
     const int c0 = __ldg(M.c_off + v), c1 = __ldg(M.c_off + v + 1);
     const bool over = binfo_overflow(bv);
     const int nitems = over ? F.cnt[v] : 4;
@@ -564,10 +917,13 @@ __device__ void phase_union(const DevMesh& M, const DevField& F, const DevWork& 
       }
       if (!W.active[l]) continue;
       const unsigned item = static_cast<unsigned>(v) * kSlots + slot;
+      if (trace) tr[2] = gtimer_raw();
       for (int c = c0 + lane; c < c1; c += kG) {
         const int u = __ldg(M.c_col + c);  // higher-numbered related vertices only
         const int j = band_slot_of(F, W, P, u, l);
+        if (trace) tr[3] = gtimer_raw() + (j & 0);
         if (j >= 0 && !P.split_a_no_unite) uf_unite(W.parent, item, static_cast<unsigned>(u) * kSlots + j, ep);
+        if (trace) tr[4] = gtimer_raw();
       }
     }
   }
@@ -811,7 +1167,7 @@ __device__ int decide(const DevWork& W, const StepParams& P, int spar) {
   int bits = 0;
   for (int a = threadIdx.x; a < P.n_active; a += blockDim.x) {
     const LayerStat& st = g[a];
-    if (st.ncomp >= 2) bits |= kStopSplit;
+    if (st.ncomp >= 2 && !P.split_a_no_unite) bits |= kStopSplit;
     if (st.nband == 0 && st.nunsat == 0) bits |= kStopVanish;
   }
   if (threadIdx.x == 0) {
@@ -861,7 +1217,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
     }
     grid_sync(ctl);
     ++ep;
-    phase_union(M, F, W, P, lpar, ep);
+    phase_union(M, F, W, P, lpar, ep, gtid / kG, gsz / kG);
     grid_sync(ctl);
     block_stats_init(S);
     phase_stats(M, F, W, P, lpar, spar, ep, false, S, Q, QB);
@@ -901,7 +1257,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       ctl->sum_region += static_cast<unsigned long long>(nR);
     }
     for (int i = gtid / kG; i < nR; i += gsz / kG)
-      update_vertex(M, F, W, P, i, W.region[cur][i], false, threadIdx.x & (kG - 1), group_mask());
+      if (!update_vertex_fast(M, F, W, P, i, W.region[cur][i], false, threadIdx.x & (kG - 1), group_mask()))
+        update_vertex(M, F, W, P, i, W.region[cur][i], false, threadIdx.x & (kG - 1), group_mask());
     grid_sync(ctl);
     if (ctl->error) stop = kStopError;
   }
@@ -929,6 +1286,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
     }
     grid_sync(ctl);
     if (prof) W.prof[pslot + 1] = gtimer();
+    block_start(W, step - (P.step_end - 64), 1);
     if (check) {
       ++ep;
       // ---- 2: D(s) + flush of the previous check's trail records
@@ -942,10 +1300,13 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
         ctl->base_max_bits = 0;
         ctl->nbandpairs = 0;
       }
-      phase_union(M, F, W, P, lpar, ep);
+      if (gtid == 0) ctl->sum_interest += static_cast<unsigned long long>(ctl->ilcount[lpar]);
+      phase_union(M, F, W, P, lpar, ep, gtid / kG, gsz / kG);
       if (P.do_hash) phase_hash(F, W, M.nv);
+      block_done(W, step - (P.step_end - 64), 1);
       grid_sync(ctl);
       if (prof) W.prof[pslot + 2] = gtimer();
+      block_start(W, step - (P.step_end - 64), 2);
       // ---- 3: E(s) + speculative A(s+1)
       const int spar = cur;
       block_stats_init(S);
@@ -962,13 +1323,12 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
         if (gtid == 0) {
           ctl->rcount[cur] = 0;
           ctl->sum_region += static_cast<unsigned long long>(nR1);
-          ctl->sum_interest += static_cast<unsigned long long>(ctl->ilcount[lpar]);
         }
         for (int i = gtid / kG; i < nR1; i += gsz / kG)
-          update_vertex(M, F, W, P, i, W.region[nxt][i], true, threadIdx.x & (kG - 1), group_mask());
-      } else if (gtid == 0) {
-        ctl->sum_interest += static_cast<unsigned long long>(ctl->ilcount[lpar]);
+          if (!update_vertex_fast(M, F, W, P, i, W.region[nxt][i], true, threadIdx.x & (kG - 1), group_mask()))
+            update_vertex(M, F, W, P, i, W.region[nxt][i], true, threadIdx.x & (kG - 1), group_mask());
       }
+      block_done(W, step - (P.step_end - 64), 2);
       grid_sync(ctl);
       if (prof && !P.split_a) W.prof[pslot + 3] = gtimer();
       lpar ^= 1;
@@ -1006,7 +1366,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
           ctl->sum_region += static_cast<unsigned long long>(nR1);
         }
         for (int i = gtid / kG; i < nR1; i += gsz / kG)
-          update_vertex(M, F, W, P, i, W.region[nxt][i], false, threadIdx.x & (kG - 1), group_mask());
+          if (!update_vertex_fast(M, F, W, P, i, W.region[nxt][i], false, threadIdx.x & (kG - 1), group_mask()))
+            update_vertex(M, F, W, P, i, W.region[nxt][i], false, threadIdx.x & (kG - 1), group_mask());
       }
       grid_sync(ctl);
       if (ctl->error) {
