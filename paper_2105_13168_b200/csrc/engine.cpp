@@ -446,6 +446,15 @@ void DeviceField::setup() {
   work_.bandpair_cap = static_cast<int>(bandpairs.n);
   binfo.alloc(nv);
   view_.binfo = binfo.p;
+  // Event-time scratch (layer pulls, isoline crossings, edits): allocated once
+  // so host event handling never calls cudaMalloc/cudaFree.
+  const size_t ncap = std::max<size_t>(nv, dm_->host().ne()) + 1;
+  ai0.alloc(ncap);
+  ai1.alloc(ncap);
+  ad0.alloc(ncap);
+  ad1.alloc(ncap);
+  ad2.alloc(ncap);
+  acnt.alloc(16);
   work_.parent = parent.p;
   work_.active = active.p;
   work_.aidx = aidx.p;
@@ -470,8 +479,7 @@ void DeviceField::init(const std::vector<Index>& seeds) {
   std::vector<int> sv(seeds.begin(), seeds.end());
   std::sort(sv.begin(), sv.end());
   sv.erase(std::unique(sv.begin(), sv.end()), sv.end());
-  DevBuf<int> ds(sv.size());
-  ds.upload(sv.data(), sv.size(), s_);
+  ai0.upload(sv.data(), sv.size(), s_);
   ctl.zero(s_);
   // Versioned union-find parents / pair keys restart at epoch 0, and a reused
   // workspace may hold tags from an earlier pass: clear them.
@@ -479,7 +487,7 @@ void DeviceField::init(const std::vector<Index>& seeds) {
   pair_keys.zero(s_);
   stat.zero(s_);
   lastpos.zero(s_);
-  ck(launch_init_field(view_, work_, static_cast<int>(nv), ds.p, static_cast<int>(sv.size()), s_), "init field");
+  ck(launch_init_field(view_, work_, static_cast<int>(nv), ai0.p, static_cast<int>(sv.size()), s_), "init field");
   Ctl c{};
   c.base_one = static_cast<int>(nv - sv.size());
   ctl.upload(&c, 1, s_);
@@ -496,17 +504,20 @@ std::vector<Index> DeviceField::active_nonbase() const {
 
 void DeviceField::sync_active() {
   if (meta_.size() > static_cast<size_t>(kMaxLayers)) fail(kCapacityExceeded, "more than 65535 layers");
-  std::vector<unsigned char> act(kMaxLayers + 1, 0);
-  std::vector<int> ai(kMaxLayers + 1, -1), al;
-  for (Index id = 1; id < meta_.size(); ++id)
+  // Ids at or above layer_count() never occur in columns, so only the table
+  // prefix [0, layer_count) is uploaded.
+  const size_t lc = meta_.size();
+  std::vector<unsigned char> act(lc, 0);
+  std::vector<int> ai(lc, -1), al;
+  for (Index id = 1; id < lc; ++id)
     if (meta_[id].active) {
       act[id] = 1;
       ai[id] = static_cast<int>(al.size());
       al.push_back(static_cast<int>(id));
     }
   if (al.size() > static_cast<size_t>(kMaxActive)) fail(kCapacityExceeded, "too many simultaneously active layers");
-  active.upload(act.data(), act.size(), s_);
-  aidx.upload(ai.data(), ai.size(), s_);
+  active.upload(act.data(), lc, s_);
+  aidx.upload(ai.data(), lc, s_);
   if (!al.empty()) alist.upload(al.data(), al.size(), s_);
   cuda_check(cudaStreamSynchronize(s_), "sync_active");
 }
@@ -520,13 +531,11 @@ Ctl DeviceField::read_ctl() const {
 
 std::vector<std::pair<Index, double>> DeviceField::layer_values(Index layer) const {
   const int nv = static_cast<int>(dm_->host().nv());
-  DevBuf<int> ov(nv), on(1);
-  DevBuf<double> ox(nv);
-  on.zero(s_);
-  ck(launch_pull_layer(view_, nv, static_cast<int>(layer), ov.p, ox.p, on.p, s_), "pull layer");
-  const int n = to_host(on, 1, s_)[0];
-  std::vector<int> hv = to_host(ov, n, s_);
-  std::vector<double> hx = to_host(ox, n, s_);
+  cuda_check(cudaMemsetAsync(acnt.p, 0, sizeof(int), s_), "memset");
+  ck(launch_pull_layer(view_, nv, static_cast<int>(layer), ai0.p, ad0.p, acnt.p, s_), "pull layer");
+  const int n = to_host(acnt, 1, s_)[0];
+  std::vector<int> hv = to_host(ai0, n, s_);
+  std::vector<double> hx = to_host(ad0, n, s_);
   std::vector<std::pair<Index, double>> out(n);
   for (int i = 0; i < n; ++i) out[i] = {static_cast<Index>(hv[i]), hx[i]};
   std::sort(out.begin(), out.end());
@@ -535,27 +544,28 @@ std::vector<std::pair<Index, double>> DeviceField::layer_values(Index layer) con
 
 std::vector<double> DeviceField::dense_row(Index layer) const {
   const int nv = static_cast<int>(dm_->host().nv());
-  DevBuf<double> d(nv);
-  ck(launch_dense_row(view_, nv, static_cast<int>(layer), d.p, s_), "dense row");
-  return to_host(d, nv, s_);
+  ck(launch_dense_row(view_, nv, static_cast<int>(layer), ad0.p, s_), "dense row");
+  return to_host(ad0, nv, s_);
 }
 
 std::vector<Index> DeviceField::covered_set(double threshold) const {
   const int nv = static_cast<int>(dm_->host().nv());
-  DevBuf<int> ov(nv), on(1);
-  on.zero(s_);
-  ck(launch_covered(view_, nv, threshold, ov.p, on.p, s_), "covered");
-  const int n = to_host(on, 1, s_)[0];
-  std::vector<int> hv = to_host(ov, n, s_);
+  cuda_check(cudaMemsetAsync(acnt.p, 0, sizeof(int), s_), "memset");
+  ck(launch_covered(view_, nv, threshold, ai0.p, acnt.p, s_), "covered");
+  const int n = to_host(acnt, 1, s_)[0];
+  std::vector<int> hv = to_host(ai0, n, s_);
   std::sort(hv.begin(), hv.end());
   return std::vector<Index>(hv.begin(), hv.end());
 }
 
 unsigned long long DeviceField::hash() const {
-  DevBuf<unsigned long long> h(1);
-  h.zero(s_);
-  ck(launch_field_hash(view_, static_cast<int>(dm_->host().nv()), h.p, s_), "hash");
-  return to_host(h, 1, s_)[0];
+  unsigned long long* h = reinterpret_cast<unsigned long long*>(acnt.p + 8);
+  cuda_check(cudaMemsetAsync(h, 0, sizeof(unsigned long long), s_), "memset");
+  ck(launch_field_hash(view_, static_cast<int>(dm_->host().nv()), h, s_), "hash");
+  unsigned long long out = 0;
+  cuda_check(cudaMemcpyAsync(&out, h, sizeof out, cudaMemcpyDeviceToHost, s_), "D2H");
+  cuda_check(cudaStreamSynchronize(s_), "hash sync");
+  return out;
 }
 
 int DeviceField::base_one_count() const {
@@ -575,9 +585,8 @@ void DeviceField::normalize_columns() {
 
 void DeviceField::mark_region(const DevMesh& op_view, const std::vector<int>& verts, long stamp_value, int parity) {
   if (verts.empty()) return;
-  DevBuf<int> d(verts.size());
-  d.upload(verts.data(), verts.size(), s_);
-  ck(launch_mark_region(op_view, work_, d.p, static_cast<int>(verts.size()), stamp_value, parity, s_), "mark region");
+  ai1.upload(verts.data(), verts.size(), s_);
+  ck(launch_mark_region(op_view, work_, ai1.p, static_cast<int>(verts.size()), stamp_value, parity, s_), "mark region");
   cuda_check(cudaStreamSynchronize(s_), "mark region sync");
 }
 
@@ -614,10 +623,9 @@ std::vector<Index> DeviceField::split_layer(Index layer, const std::vector<std::
   }
   if (meta_.size() > static_cast<size_t>(kMaxLayers)) fail(kCapacityExceeded, "more than 65535 layers");
   meta_[layer].active = false;
-  DevBuf<int> dv(verts.size()), dl(newl.size());
-  dv.upload(verts.data(), verts.size(), s_);
-  dl.upload(newl.data(), newl.size(), s_);
-  ck(launch_relabel(view_, work_, dv.p, dl.p, static_cast<int>(verts.size()), static_cast<int>(layer), s_), "relabel");
+  ai0.upload(verts.data(), verts.size(), s_);
+  ai1.upload(newl.data(), newl.size(), s_);
+  ck(launch_relabel(view_, work_, ai0.p, ai1.p, static_cast<int>(verts.size()), static_cast<int>(layer), s_), "relabel");
   cuda_check(cudaStreamSynchronize(s_), "split");
   pending_moved.insert(pending_moved.end(), verts.begin(), verts.end());
   return children;
@@ -653,13 +661,12 @@ Index DeviceField::merge_layers(const std::vector<Index>& ids, long step_, std::
   std::sort(order.begin(), order.end());
   if (order != sorted_ids) fail(kInvalidMerge, "merge ids must be ascending (reference groups are sorted)");
   const int nv = static_cast<int>(dm_->host().nv());
-  DevBuf<int> g(ids.size()), t(nv), nt(1);
-  g.upload(sorted_ids.data(), ids.size(), s_);
-  nt.zero(s_);
-  ck(launch_merge(view_, work_, nv, g.p, static_cast<int>(ids.size()), static_cast<int>(result), t.p, nt.p, s_),
+  ai1.upload(sorted_ids.data(), ids.size(), s_);
+  cuda_check(cudaMemsetAsync(acnt.p, 0, sizeof(int), s_), "memset");
+  ck(launch_merge(view_, work_, nv, ai1.p, static_cast<int>(ids.size()), static_cast<int>(result), ai0.p, acnt.p, s_),
      "merge");
-  const int n = to_host(nt, 1, s_)[0];
-  std::vector<int> tv = to_host(t, n, s_);
+  const int n = to_host(acnt, 1, s_)[0];
+  std::vector<int> tv = to_host(ai0, n, s_);
   pending_moved.insert(pending_moved.end(), tv.begin(), tv.end());
   if (touched) *touched = tv;
   return result;
@@ -669,12 +676,14 @@ void DeviceField::set_inactive(Index layer) { meta_[layer].active = false; }
 
 bool DeviceField::finished(Index layer, int nunsat) const {
   if (nunsat != 0) return false;
-  DevBuf<int> flag(1);
   const int one = 1;
-  flag.upload(&one, 1, s_);
+  cuda_check(cudaMemcpyAsync(acnt.p + 1, &one, sizeof(int), cudaMemcpyHostToDevice, s_), "H2D");
   DevMesh m = dm_->view();
-  ck(launch_finished(m, view_, static_cast<int>(layer), prune_epsilon, flag.p, s_), "finished");
-  return to_host(flag, 1, s_)[0] != 0;
+  ck(launch_finished(m, view_, static_cast<int>(layer), prune_epsilon, acnt.p + 1, s_), "finished");
+  int flag = 0;
+  cuda_check(cudaMemcpyAsync(&flag, acnt.p + 1, sizeof(int), cudaMemcpyDeviceToHost, s_), "D2H");
+  cuda_check(cudaStreamSynchronize(s_), "finished sync");
+  return flag != 0;
 }
 
 long InitialPassResult::handle_estimate_count() const {
@@ -775,6 +784,9 @@ StepParams make_params(const DeviceField& field, const Config& cfg, const Coeffi
 // cost grows with the CTA count, and a step's frontier/band work rarely needs
 // more than 148 x 256 threads), fewer for small meshes.
 int engine_blocks(int nv) {
+  // One 512-thread CTA per SM regardless of mesh size: a step's work is a
+  // handful of dependent loads per frontier/band item, so more groups means
+  // fewer items per group; the grid barrier costs ~1.2 us at 148 CTAs.
   static int maxco = 0, sms = 0;
   if (!maxco) {
     ck(dev_max_coresident_blocks(&maxco), "occupancy");
@@ -782,12 +794,12 @@ int engine_blocks(int nv) {
     cuda_check(cudaGetDevice(&dev), "device");
     cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms");
   }
+  (void)nv;
   if (const char* env = std::getenv("DTB_BLOCKS")) {
     const int b = std::atoi(env);
     if (b > 0) return std::min(b, maxco);
   }
-  const int want = std::max(1, nv / 4096);
-  return std::min({want, sms, maxco});
+  return std::min(sms, maxco);
 }
 
 std::vector<std::vector<Index>> groups_from_pairs(const std::vector<unsigned>& pairs) {
@@ -1137,15 +1149,13 @@ class PassEngine {
   // layer that is not a frozen seam.
   bool front_loop(Index layer, SurfaceLoop& out) const {
     const DevMesh m = dm_->view();
-    const int ne = m.ne;
-    DevBuf<int> de(ne), dn(1);
-    DevBuf<double> dtt(ne), dba(ne), dbb(ne);
-    dn.zero(s_);
-    ck(launch_crossings(m, field_->view(), static_cast<int>(layer), 0.5, de.p, dtt.p, dba.p, dbb.p, dn.p, s_),
+    DeviceField& F = *field_;
+    cuda_check(cudaMemsetAsync(F.acnt.p, 0, sizeof(int), s_), "memset");
+    ck(launch_crossings(m, F.view(), static_cast<int>(layer), 0.5, F.ai0.p, F.ad0.p, F.ad1.p, F.ad2.p, F.acnt.p, s_),
        "crossings");
-    const int n = to_host(dn, 1, s_)[0];
-    std::vector<int> e = to_host(de, n, s_);
-    std::vector<double> t = to_host(dtt, n, s_), ba = to_host(dba, n, s_), bb = to_host(dbb, n, s_);
+    const int n = to_host(F.acnt, 1, s_)[0];
+    std::vector<int> e = to_host(F.ai0, n, s_);
+    std::vector<double> t = to_host(F.ad0, n, s_), ba = to_host(F.ad1, n, s_), bb = to_host(F.ad2, n, s_);
     std::unordered_map<Index, double> t_of, b0, b1;
     for (int i = 0; i < n; ++i) {
       t_of[static_cast<Index>(e[i])] = t[i];

@@ -37,8 +37,8 @@ void note_launch(unsigned long long n);
 
 namespace {
 
-constexpr int kCand = 16;  // candidate layers gathered over one stiffness row
-constexpr int kWork = 24;  // working column capacity before the final size check
+constexpr int kCand = 32;  // candidate layers gathered over one stiffness row
+constexpr int kWork = 48;  // working column capacity before the final size check
 constexpr unsigned long long kVertMask = (1ull << 27) - 1;  // vertex bits of a snap key
 
 __device__ __forceinline__ double clamp01(double x) { return x < 0.0 ? 0.0 : (1.0 < x ? 1.0 : x); }

@@ -68,7 +68,7 @@ __device__ __forceinline__ bool binfo_overflow(const uint4& b) { return (b.w >> 
 
 namespace dtb {
 
-constexpr int kSlots = 16;         // max owners per vertex (column capacity)
+constexpr int kSlots = 32;         // max owners per vertex (column capacity)
 constexpr int kMaxLayers = 65535;  // layer ids are u16
 constexpr int kMaxActive = 4096;   // simultaneously active non-base layers
 constexpr int kPairCap = 1 << 16;  // collision pair hash table slots

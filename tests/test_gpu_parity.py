@@ -114,3 +114,19 @@ def test_cpp_facade_runs(tmp_path):
     out = subprocess.run([str(exe), "icosphere:3:2.0"], capture_output=True, text=True)
     assert out.returncode == 0, out.stderr
     assert '"status":0' in out.stdout and "vanish" in out.stdout and "cycle_rank 0" in out.stdout
+
+
+def test_event_heavy_chaotic_torus_matches_reference():
+    """Hundreds of splits/merges/vanishes (the reference's chaotic regime on a
+    coarse torus): the trajectory must stay bit-exact through every event."""
+    spec, steps = "torus:96:32:3:1.0", 2500
+    mesh = dt.TriangleMesh.generate(spec)
+    op, _ = ref_operator(mesh, spec)
+    res = dt.run_initial_pass(mesh, op, 0, dt.default_config(max_steps=steps, record_hashes=1))
+    ref = refdata.ref_run(spec, max_steps=steps)
+    assert len(ref["events"]) > 100
+    mine, theirs = [int(h) for h in res.hashes()], [int(h) for h in ref["hashes"]]
+    first_bad = next((i for i, (a, b) in enumerate(zip(mine, theirs)) if a != b), None)
+    assert first_bad is None and len(mine) == len(theirs), first_bad
+    parity.compare_events(res.events(), ref["events"])
+    parity.compare_tracks(res.tracks(), ref["tracks"])
