@@ -20,6 +20,59 @@ void cuda_check(cudaError_t e, const char* what) {
 static void ck(int e, const char* what) { cuda_check(static_cast<cudaError_t>(e), what); }
 
 namespace {
+std::mutex g_alloc_mu;
+std::multimap<size_t, void*> g_free_blocks;  // size class -> block
+size_t g_cached_bytes = 0;
+constexpr size_t kCacheBytes = size_t(16) << 30;
+
+size_t size_class(size_t bytes) {
+  if (bytes <= 4096) return 4096;
+  size_t c = 4096;
+  while (c < bytes && c < (size_t(64) << 20)) c <<= 1;  // powers of two up to 64 MiB
+  if (c >= bytes) return c;
+  return (bytes + (size_t(8) << 20) - 1) / (size_t(8) << 20) * (size_t(8) << 20);  // then 8 MiB granules
+}
+}  // namespace
+
+void* dev_alloc(size_t bytes) {
+  const size_t c = size_class(bytes);
+  {
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    auto it = g_free_blocks.find(c);
+    if (it != g_free_blocks.end()) {
+      void* p = it->second;
+      g_free_blocks.erase(it);
+      g_cached_bytes -= c;
+      return p;
+    }
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, c);
+  if (e != cudaSuccess) {
+    // Out of memory with blocks parked in the cache: release them and retry.
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    for (auto& kv : g_free_blocks) cudaFree(kv.second);
+    g_free_blocks.clear();
+    g_cached_bytes = 0;
+    cudaGetLastError();
+    e = cudaMalloc(&p, c);
+  }
+  cuda_check(e, "cudaMalloc");
+  return p;
+}
+
+void dev_free(void* p, size_t bytes) {
+  const size_t c = size_class(bytes);
+  std::lock_guard<std::mutex> lk(g_alloc_mu);
+  if (g_cached_bytes + c > kCacheBytes) {
+    cudaFree(p);
+    return;
+  }
+  g_free_blocks.emplace(c, p);
+  g_cached_bytes += c;
+}
+
+namespace {
 
 template <class T>
 std::vector<T> to_host(const DevBuf<T>& b, size_t n, cudaStream_t s) {
@@ -118,13 +171,12 @@ DeviceMesh::DeviceMesh(std::shared_ptr<const Mesh> mesh, cudaStream_t s) : mesh_
   fb.v2f_off = f_off.p;
   fb.v2f = f_col.p;
   c_off.alloc(nv + 1);
-  int* ccol = nullptr;
   int nnzc = 0;
-  const int rc = launch_front_csr(fb, c_off.p, &ccol, &nnzc, s);
+  const int rc = launch_front_count(fb, c_off.p, &nnzc, s);
   if (rc == -1) fail(kCapacityExceeded, "vertex valence above 32");
   ck(rc, "front connectivity");
-  c_col.p = ccol;
-  c_col.n = static_cast<size_t>(std::max(1, nnzc));
+  c_col.alloc(static_cast<size_t>(std::max(1, nnzc)));
+  ck(launch_front_fill(fb, c_off.p, c_col.p, s), "front connectivity");
   cuda_check(cudaStreamSynchronize(s), "mesh upload");
 
   view_.nv = static_cast<int>(nv);

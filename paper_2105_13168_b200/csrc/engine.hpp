@@ -19,6 +19,12 @@ namespace dtb {
 
 void cuda_check(cudaError_t e, const char* what);
 
+// Caching device allocator: freed blocks are kept in size classes and handed
+// out again, so repeated passes / meshes never pay cudaMalloc + cudaFree (the
+// latter synchronises the whole device).  Bounded by kCacheBytes.
+void* dev_alloc(size_t bytes);
+void dev_free(void* p, size_t bytes);
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
@@ -45,10 +51,10 @@ struct DevBuf {
   void alloc(size_t count) {
     release();
     n = count;
-    if (count) cuda_check(cudaMalloc(reinterpret_cast<void**>(&p), sizeof(T) * count), "cudaMalloc");
+    if (count) p = static_cast<T*>(dev_alloc(sizeof(T) * count));
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) dev_free(p, sizeof(T) * n);
     p = nullptr;
     n = 0;
   }

@@ -236,7 +236,8 @@ struct FrontBuild {
 };
 int launch_positions(const double* xyz, int nv, double scale, double* px, double* py, double* pz, long long* fx,
                      long long* fy, long long* fz, void* stream);
-int launch_front_csr(const FrontBuild& b, int* c_off, int** c_col, int* nnz, void* stream);
+int launch_front_count(const FrontBuild& b, int* c_off, int* nnz, void* stream);
+int launch_front_fill(const FrontBuild& b, const int* c_off, int* c_col, void* stream);
 int launch_spmv(int nv, const int* off, const int* col, const double* val, const double* mass,
                 const double* x, double* y, void* stream);
 

@@ -1,7 +1,15 @@
 // Host mesh construction, generators and IO.  See mesh.hpp for the contract.
+//
+// Construction is parallel (OpenMP) wherever the reference's sequential
+// semantics allow it: validation scans report the first offending face, the
+// slot pairing and adjacency lists are bucketed with atomic cursors and then
+// sorted per bucket (deterministic), edge numbering is a prefix sum over
+// "first slot of its edge" flags.  Orientation is checked in parallel; only
+// an inconsistently oriented input takes the reference's sequential BFS.
 #include "mesh.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cctype>
 #include <cstring>
 #include <fstream>
@@ -14,54 +22,81 @@ namespace dtb {
 
 namespace {
 
+using U32 = std::uint32_t;
+
+// Exclusive prefix sum in place over counts[0..n] (counts[n] becomes the total).
+void exclusive_scan(std::vector<U32>& a) {
+  U32 run = 0;
+  for (auto& x : a) {
+    const U32 c = x;
+    x = run;
+    run += c;
+  }
+}
+
+// CSR of (key -> items) for items whose key is produced by key_of(i), with
+// the items of each bucket sorted by less(a, b).  Parallel: atomic counts,
+// atomic-cursor scatter, per-bucket sort.
+template <class KeyOf, class Less>
+void bucket_sort(std::size_t nitems, Index nkeys, KeyOf key_of, Less less, std::vector<U32>& off,
+                 std::vector<U32>& items) {
+  off.assign(static_cast<std::size_t>(nkeys) + 1, 0);
+  std::vector<std::atomic<U32>> cnt(static_cast<std::size_t>(nkeys));
+#pragma omp parallel for schedule(static)
+  for (long long k = 0; k < static_cast<long long>(nkeys); ++k) cnt[k].store(0, std::memory_order_relaxed);
+#pragma omp parallel for schedule(static)
+  for (long long i = 0; i < static_cast<long long>(nitems); ++i)
+    cnt[key_of(static_cast<std::size_t>(i))].fetch_add(1, std::memory_order_relaxed);
+  for (Index k = 0; k < nkeys; ++k) off[k] = cnt[k].load(std::memory_order_relaxed);
+  off[nkeys] = 0;
+  exclusive_scan(off);
+#pragma omp parallel for schedule(static)
+  for (long long k = 0; k < static_cast<long long>(nkeys); ++k) cnt[k].store(off[k], std::memory_order_relaxed);
+  items.resize(nitems);
+#pragma omp parallel for schedule(static)
+  for (long long i = 0; i < static_cast<long long>(nitems); ++i)
+    items[cnt[key_of(static_cast<std::size_t>(i))].fetch_add(1, std::memory_order_relaxed)] = static_cast<U32>(i);
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (long long k = 0; k < static_cast<long long>(nkeys); ++k)
+    std::sort(items.begin() + off[k], items.begin() + off[k + 1], less);
+}
+
 // Groups the 3F directed face slots (slot s = 3f + k is the edge from corner k
-// to corner k+1 of the ORIGINAL face) by their unordered vertex pair using a
-// counting sort on the smaller endpoint.  Reports non-manifold (>2 slots) and
-// boundary (1 slot) edges with the reference's error classes
-// (mesh.hpp:210-221), and returns partner[s] = the other slot of s's edge.
-std::vector<std::uint32_t> pair_slots(const std::vector<std::array<Index, 3>>& faces, Index nv) {
+// to corner k+1 of the ORIGINAL face) by their unordered vertex pair, bucketed
+// on the smaller endpoint.  Reports non-manifold (>2 slots) and boundary (1
+// slot) edges with the reference's error classes (mesh.hpp:210-221), and
+// returns partner[s] = the other slot of s's edge.
+std::vector<U32> pair_slots(const std::vector<std::array<Index, 3>>& faces, Index nv) {
   const std::size_t ns = faces.size() * 3;
-  std::vector<std::uint32_t> off(static_cast<std::size_t>(nv) + 1, 0);
-  auto lo_hi = [&](std::size_t s, Index& lo, Index& hi) {
+  auto lo_of = [&](std::size_t s) {
     const auto& t = faces[s / 3];
-    Index a = t[s % 3], b = t[(s % 3 + 1) % 3];
-    lo = std::min(a, b);
-    hi = std::max(a, b);
+    return std::min(t[s % 3], t[(s % 3 + 1) % 3]);
   };
-  for (std::size_t s = 0; s < ns; ++s) {
-    Index lo, hi;
-    lo_hi(s, lo, hi);
-    ++off[lo + 1];
-  }
-  for (Index v = 0; v < nv; ++v) off[v + 1] += off[v];
-  std::vector<std::uint32_t> bucket(ns);
-  {
-    std::vector<std::uint32_t> cur(off.begin(), off.end() - 1);
-    for (std::size_t s = 0; s < ns; ++s) {
-      Index lo, hi;
-      lo_hi(s, lo, hi);
-      bucket[cur[lo]++] = static_cast<std::uint32_t>(s);
-    }
-  }
-  std::vector<std::uint32_t> partner(ns, kInvalid);
-  bool nonmanifold = false, boundary = false;
-  std::vector<std::pair<Index, std::uint32_t>> tmp;
-  for (Index v = 0; v < nv; ++v) {
-    tmp.clear();
-    for (std::uint32_t i = off[v]; i < off[v + 1]; ++i) {
-      Index lo, hi;
-      lo_hi(bucket[i], lo, hi);
-      tmp.emplace_back(hi, bucket[i]);
-    }
-    std::sort(tmp.begin(), tmp.end());
-    for (std::size_t i = 0; i < tmp.size();) {
-      std::size_t j = i;
-      while (j < tmp.size() && tmp[j].first == tmp[i].first) ++j;
-      if (j - i > 2) nonmanifold = true;
-      else if (j - i == 1) boundary = true;
+  auto hi_of = [&](std::size_t s) {
+    const auto& t = faces[s / 3];
+    return std::max(t[s % 3], t[(s % 3 + 1) % 3]);
+  };
+  std::vector<U32> off, bucket;
+  bucket_sort(
+      ns, nv, lo_of,
+      [&](U32 a, U32 b) {
+        const Index ha = hi_of(a), hb = hi_of(b);
+        return ha != hb ? ha < hb : a < b;
+      },
+      off, bucket);
+  std::vector<U32> partner(ns, kInvalid);
+  int nonmanifold = 0, boundary = 0;
+#pragma omp parallel for schedule(dynamic, 4096) reduction(| : nonmanifold, boundary)
+  for (long long v = 0; v < static_cast<long long>(nv); ++v) {
+    for (U32 i = off[v]; i < off[v + 1];) {
+      U32 j = i;
+      const Index h = hi_of(bucket[i]);
+      while (j < off[v + 1] && hi_of(bucket[j]) == h) ++j;
+      if (j - i > 2) nonmanifold = 1;
+      else if (j - i == 1) boundary = 1;
       else {
-        partner[tmp[i].second] = tmp[i + 1].second;
-        partner[tmp[i + 1].second] = tmp[i].second;
+        partner[bucket[i]] = bucket[i + 1];
+        partner[bucket[i + 1]] = bucket[i];
       }
       i = j;
     }
@@ -71,25 +106,55 @@ std::vector<std::uint32_t> pair_slots(const std::vector<std::array<Index, 3>>& f
   return partner;
 }
 
+// Lock-free union-find over face indices (connectivity of the face graph).
+Index uf_root(std::vector<std::atomic<U32>>& p, U32 x) {
+  while (true) {
+    const U32 q = p[x].load(std::memory_order_relaxed);
+    if (q == x) return x;
+    const U32 r = p[q].load(std::memory_order_relaxed);
+    if (r != q) p[x].compare_exchange_weak(const_cast<U32&>(q), r, std::memory_order_relaxed);
+    x = q;
+  }
+}
+
 }  // namespace
 
 Mesh::Mesh(std::vector<V3> vertices, std::vector<std::array<Index, 3>> faces)
     : pos_(std::move(vertices)), faces_(std::move(faces)) {
   if (faces_.empty()) fail(kTopologyError, "mesh has no faces");
   const Index raw = static_cast<Index>(pos_.size());
-  for (const auto& f : faces_) {
-    for (Index v : f)
-      if (v >= raw) fail(kParseError, "face references vertex out of range");
-    if (f[0] == f[1] || f[1] == f[2] || f[0] == f[2]) fail(kDegeneracyError, "face repeats a vertex");
+  // First face (in order) that references an out-of-range vertex or repeats
+  // one; the reference checks faces in order, range before repetition.
+  {
+    long long first_bad = static_cast<long long>(faces_.size());
+#pragma omp parallel for reduction(min : first_bad)
+    for (long long i = 0; i < static_cast<long long>(faces_.size()); ++i) {
+      const auto& f = faces_[i];
+      const bool bad = f[0] >= raw || f[1] >= raw || f[2] >= raw || f[0] == f[1] || f[1] == f[2] || f[0] == f[2];
+      if (bad && i < first_bad) first_bad = i;
+    }
+    if (first_bad < static_cast<long long>(faces_.size())) {
+      const auto& f = faces_[first_bad];
+      for (Index v : f)
+        if (v >= raw) fail(kParseError, "face references vertex out of range");
+      fail(kDegeneracyError, "face repeats a vertex");
+    }
   }
   // Unreferenced vertices are dropped; survivors renumbered by first use.
   {
-    std::vector<Index> remap(pos_.size(), kInvalid);
-    Index next = 0;
-    for (const auto& f : faces_)
-      for (Index v : f)
-        if (remap[v] == kInvalid) remap[v] = next++;
-    if (next != pos_.size()) {
+    std::vector<unsigned char> used(pos_.size(), 0);
+#pragma omp parallel for
+    for (long long i = 0; i < static_cast<long long>(faces_.size()); ++i)
+      for (Index v : faces_[i]) used[v] = 1;
+    long long unused = 0;
+#pragma omp parallel for reduction(+ : unused)
+    for (long long v = 0; v < static_cast<long long>(used.size()); ++v) unused += used[v] ? 0 : 1;
+    if (unused) {
+      std::vector<Index> remap(pos_.size(), kInvalid);
+      Index next = 0;
+      for (const auto& f : faces_)
+        for (Index v : f)
+          if (remap[v] == kInvalid) remap[v] = next++;
       std::vector<V3> compact(next);
       for (Index v = 0; v < pos_.size(); ++v)
         if (remap[v] != kInvalid) compact[remap[v]] = pos_[v];
@@ -98,33 +163,35 @@ Mesh::Mesh(std::vector<V3> vertices, std::vector<std::array<Index, 3>> faces)
         for (Index& v : f) v = remap[v];
     }
   }
-  // Duplicate faces in any vertex order are rejected: bucket sorted triples by
-  // their smallest vertex and compare within the (small) buckets.
+  // Duplicate faces in any vertex order are rejected: bucket the sorted
+  // triples by their smallest vertex and compare within the buckets.
   {
-    const Index n = nv();
-    std::vector<std::uint32_t> off(static_cast<std::size_t>(n) + 1, 0);
     std::vector<std::array<Index, 3>> keys(faces_.size());
-    for (std::size_t i = 0; i < faces_.size(); ++i) {
+#pragma omp parallel for
+    for (long long i = 0; i < static_cast<long long>(faces_.size()); ++i) {
       keys[i] = faces_[i];
       std::sort(keys[i].begin(), keys[i].end());
-      ++off[keys[i][0] + 1];
     }
-    for (Index v = 0; v < n; ++v) off[v + 1] += off[v];
-    std::vector<std::pair<Index, Index>> b(faces_.size());
-    std::vector<std::uint32_t> cur(off.begin(), off.end() - 1);
-    for (const auto& k : keys) b[cur[k[0]]++] = {k[1], k[2]};
-    for (Index v = 0; v < n; ++v) {
-      auto first = b.begin() + off[v], last = b.begin() + off[v + 1];
-      std::sort(first, last);
-      if (std::adjacent_find(first, last) != last) fail(kTopologyError, "duplicate face");
-    }
+    std::vector<U32> off, items;
+    bucket_sort(
+        faces_.size(), nv(), [&](std::size_t i) { return keys[i][0]; },
+        [&](U32 a, U32 b) { return keys[a] != keys[b] ? keys[a] < keys[b] : a < b; }, off, items);
+    int dup = 0;
+#pragma omp parallel for schedule(dynamic, 4096) reduction(| : dup)
+    for (long long v = 0; v < static_cast<long long>(nv()); ++v)
+      for (U32 i = off[v]; i + 1 < off[v + 1]; ++i)
+        if (keys[items[i]] == keys[items[i + 1]]) dup = 1;
+    if (dup) fail(kTopologyError, "duplicate face");
   }
   orient();
   const double diag = bbox_diagonal();
   const double tol = 1e-12 * diag * diag;
-  for (Index f = 0; f < nf(); ++f)
-    if (face_area(f) < tol)
-      fail(kDegeneracyError, "face " + std::to_string(f) + " has near-zero area");
+  long long first_small = static_cast<long long>(nf());
+#pragma omp parallel for reduction(min : first_small)
+  for (long long f = 0; f < static_cast<long long>(nf()); ++f)
+    if (face_area(static_cast<Index>(f)) < tol && f < first_small) first_small = f;
+  if (first_small < static_cast<long long>(nf()))
+    fail(kDegeneracyError, "face " + std::to_string(first_small) + " has near-zero area");
   index();
 }
 
@@ -132,53 +199,89 @@ Mesh::Mesh(std::vector<V3> vertices, std::vector<std::array<Index, 3>> faces)
 // reached through an edge it traverses in the same direction as its
 // predecessor is flipped (swap corners 1 and 2); a conflict on an already
 // visited face means the surface is non-orientable.  The result is then
-// flipped globally if the enclosed signed volume is negative.
+// flipped globally if the enclosed signed volume is negative.  Inputs whose
+// faces are already consistent (every edge traversed in opposite directions)
+// need no flips: for them only connectivity is checked, in parallel.
 void Mesh::orient() {
   partner_ = pair_slots(faces_, nv());
-  const std::vector<std::uint32_t>& partner = partner_;
+  const std::vector<U32>& partner = partner_;
   flipped_.assign(faces_.size(), 0);
   std::vector<char>& flipped = flipped_;
-  // Current corner-pair k of face f maps to an original slot: identity when
-  // unflipped; after swap(t1,t2) the pairs (t0,t2),(t2,t1),(t1,t0) are the
-  // original slots 2,1,0.
-  auto orig_slot = [&](Index f, int k) { return 3 * f + (flipped[f] ? 2 - k : k); };
   auto forward = [&](Index g, Index a, Index b) {
     const auto& t = faces_[g];
     for (int k = 0; k < 3; ++k)
       if (t[k] == a && t[(k + 1) % 3] == b) return true;
     return false;
   };
-  std::vector<char> visited(faces_.size(), 0);
-  std::vector<Index> queue;
-  queue.reserve(faces_.size());
-  queue.push_back(0);
-  visited[0] = 1;
-  std::size_t head = 0, reached = 1;
-  while (head < queue.size()) {
-    Index f = queue[head++];
-    for (int k = 0; k < 3; ++k) {
-      Index a = faces_[f][k], b = faces_[f][(k + 1) % 3];
-      Index g = partner[orig_slot(f, k)] / 3;
-      bool same = forward(g, a, b);
-      if (!visited[g]) {
-        if (same) {
-          std::swap(faces_[g][1], faces_[g][2]);
-          flipped[g] ^= 1;
-        }
-        visited[g] = 1;
-        ++reached;
-        queue.push_back(g);
-      } else if (same) {
-        fail(kTopologyError, "inconsistent orientation: surface is non-orientable");
+  int inconsistent = 0;
+  const long long ns = static_cast<long long>(faces_.size()) * 3;
+#pragma omp parallel for reduction(| : inconsistent)
+  for (long long s = 0; s < ns; ++s) {
+    const Index f = static_cast<Index>(s / 3);
+    const int k = static_cast<int>(s % 3);
+    if (forward(partner[s] / 3, faces_[f][k], faces_[f][(k + 1) % 3])) inconsistent = 1;
+  }
+  if (!inconsistent) {
+    const Index nf = this->nf();
+    std::vector<std::atomic<U32>> p(nf);
+#pragma omp parallel for
+    for (long long f = 0; f < static_cast<long long>(nf); ++f) p[f].store(static_cast<U32>(f), std::memory_order_relaxed);
+#pragma omp parallel for
+    for (long long s = 0; s < ns; ++s) {
+      U32 a = static_cast<U32>(s / 3), b = partner[s] / 3;
+      while (true) {
+        a = uf_root(p, a);
+        b = uf_root(p, b);
+        if (a == b) break;
+        if (a < b) std::swap(a, b);
+        U32 expect = a;
+        if (p[a].compare_exchange_strong(expect, b, std::memory_order_relaxed)) break;
       }
     }
+    long long roots = 0;
+#pragma omp parallel for reduction(+ : roots)
+    for (long long f = 0; f < static_cast<long long>(nf); ++f) roots += uf_root(p, static_cast<U32>(f)) == f ? 1 : 0;
+    if (roots != 1) fail(kTopologyError, "mesh has multiple connected components");
+  } else {
+    // Current corner-pair k of face f maps to an original slot: identity
+    // when unflipped; after swap(t1,t2) the pairs (t0,t2),(t2,t1),(t1,t0) are
+    // the original slots 2,1,0.
+    auto orig_slot = [&](Index f, int k) { return 3 * f + (flipped[f] ? 2 - k : k); };
+    std::vector<char> visited(faces_.size(), 0);
+    std::vector<Index> queue;
+    queue.reserve(faces_.size());
+    queue.push_back(0);
+    visited[0] = 1;
+    std::size_t head = 0, reached = 1;
+    while (head < queue.size()) {
+      Index f = queue[head++];
+      for (int k = 0; k < 3; ++k) {
+        Index a = faces_[f][k], b = faces_[f][(k + 1) % 3];
+        Index g = partner[orig_slot(f, k)] / 3;
+        bool same = forward(g, a, b);
+        if (!visited[g]) {
+          if (same) {
+            std::swap(faces_[g][1], faces_[g][2]);
+            flipped[g] ^= 1;
+          }
+          visited[g] = 1;
+          ++reached;
+          queue.push_back(g);
+        } else if (same) {
+          fail(kTopologyError, "inconsistent orientation: surface is non-orientable");
+        }
+      }
+    }
+    if (reached != faces_.size()) fail(kTopologyError, "mesh has multiple connected components");
   }
-  if (reached != faces_.size()) fail(kTopologyError, "mesh has multiple connected components");
-  double vol = 0;
+  double vol = 0;  // sequential, in face order (the reference's rounding)
   for (const auto& t : faces_) vol += dot(pos_[t[0]], cross(pos_[t[1]], pos_[t[2]])) / 6.0;
   if (vol < 0) {
-    for (auto& t : faces_) std::swap(t[1], t[2]);
-    for (char& fl : flipped_) fl ^= 1;
+#pragma omp parallel for
+    for (long long f = 0; f < static_cast<long long>(faces_.size()); ++f) {
+      std::swap(faces_[f][1], faces_[f][2]);
+      flipped_[f] ^= 1;
+    }
   }
 }
 
@@ -190,62 +293,66 @@ void Mesh::index() {
   // the input corners: final corner pair k of face f is input slot
   // 3f + (flipped ? 2 - k : k).
   const std::size_t ns = faces_.size() * 3;
-  std::vector<std::uint32_t> partner(ns);
-  for (std::size_t s = 0; s < ns; ++s) {
-    const std::size_t f = s / 3;
+  std::vector<U32> partner(ns);
+#pragma omp parallel for
+  for (long long s = 0; s < static_cast<long long>(ns); ++s) {
+    const std::size_t f = static_cast<std::size_t>(s) / 3;
     const int k = static_cast<int>(s % 3);
-    const std::uint32_t orig = static_cast<std::uint32_t>(3 * f + (flipped_[f] ? 2 - k : k));
-    const std::uint32_t po = partner_[orig];
-    const std::uint32_t g = po / 3, kg = po % 3;
+    const U32 orig = static_cast<U32>(3 * f + (flipped_[f] ? 2 - k : k));
+    const U32 po = partner_[orig];
+    const U32 g = po / 3, kg = po % 3;
     partner[s] = 3 * g + (flipped_[g] ? 2 - kg : kg);
   }
-  std::vector<std::uint32_t>().swap(partner_);
+  std::vector<U32>().swap(partner_);
   std::vector<char>().swap(flipped_);
-  std::vector<Index> slot_edge(ns, kInvalid);
-  edge_v_.clear();
-  edge_f_.clear();
-  edge_v_.reserve(ns / 2);
-  edge_f_.reserve(ns / 2);
+  // A slot opens its edge iff its partner comes later; edge ids are the
+  // prefix count of opening slots (first appearance order).
+  const int nthreads = 64;
+  const std::size_t chunk = (ns + nthreads - 1) / nthreads;
+  std::vector<U32> base(nthreads + 1, 0);
+#pragma omp parallel for
+  for (int t = 0; t < nthreads; ++t) {
+    U32 c = 0;
+    for (std::size_t s = t * chunk; s < std::min(ns, (t + 1) * chunk); ++s) c += partner[s] > s;
+    base[t] = c;
+  }
+  base[nthreads] = 0;
+  exclusive_scan(base);
+  const Index ne = base[nthreads];
+  edge_v_.resize(ne);
+  edge_f_.resize(ne);
   face_e_.assign(faces_.size(), {kInvalid, kInvalid, kInvalid});
-  for (std::size_t s = 0; s < ns; ++s) {
-    Index f = static_cast<Index>(s / 3);
-    int k = static_cast<int>(s % 3);
-    if (slot_edge[s] == kInvalid) {
-      Index e = static_cast<Index>(edge_v_.size());
-      Index a = faces_[f][k], b = faces_[f][(k + 1) % 3];
-      edge_v_.push_back({std::min(a, b), std::max(a, b)});
-      edge_f_.push_back({f, static_cast<Index>(partner[s] / 3)});
-      slot_edge[s] = e;
-      slot_edge[partner[s]] = e;
-    }
-    face_e_[f][k] = slot_edge[s];
+  std::vector<U32> slot_edge(ns);
+#pragma omp parallel for
+  for (int t = 0; t < nthreads; ++t) {
+    U32 e = base[t];
+    for (std::size_t s = t * chunk; s < std::min(ns, (t + 1) * chunk); ++s)
+      if (partner[s] > s) {
+        const Index f = static_cast<Index>(s / 3);
+        const int k = static_cast<int>(s % 3);
+        const Index a = faces_[f][k], b = faces_[f][(k + 1) % 3];
+        edge_v_[e] = {std::min(a, b), std::max(a, b)};
+        edge_f_[e] = {f, static_cast<Index>(partner[s] / 3)};
+        slot_edge[s] = e++;
+      }
+  }
+#pragma omp parallel for
+  for (long long s = 0; s < static_cast<long long>(ns); ++s) {
+    const U32 e = partner[s] > static_cast<U32>(s) ? slot_edge[s] : slot_edge[partner[s]];
+    face_e_[s / 3][s % 3] = e;
   }
   const Index n = nv();
-  v2f_off_.assign(static_cast<std::size_t>(n) + 1, 0);
-  for (const auto& t : faces_)
-    for (Index v : t) ++v2f_off_[v + 1];
-  for (Index v = 0; v < n; ++v) v2f_off_[v + 1] += v2f_off_[v];
-  v2f_.resize(ns);
-  {
-    std::vector<std::uint32_t> cur(v2f_off_.begin(), v2f_off_.end() - 1);
-    for (Index f = 0; f < nf(); ++f)
-      for (Index v : faces_[f]) v2f_[cur[v]++] = f;
-  }
-  v2v_off_.assign(static_cast<std::size_t>(n) + 1, 0);
-  for (const auto& e : edge_v_) {
-    ++v2v_off_[e[0] + 1];
-    ++v2v_off_[e[1] + 1];
-  }
-  for (Index v = 0; v < n; ++v) v2v_off_[v + 1] += v2v_off_[v];
-  v2v_.resize(edge_v_.size() * 2);
-  {
-    std::vector<std::uint32_t> cur(v2v_off_.begin(), v2v_off_.end() - 1);
-    for (const auto& e : edge_v_) {
-      v2v_[cur[e[0]]++] = e[1];
-      v2v_[cur[e[1]]++] = e[0];
-    }
-  }
-  for (Index v = 0; v < n; ++v) std::sort(v2v_.begin() + v2v_off_[v], v2v_.begin() + v2v_off_[v + 1]);
+  bucket_sort(
+      ns, n, [&](std::size_t s) { return faces_[s / 3][s % 3]; }, [](U32 a, U32 b) { return a < b; }, v2f_off_,
+      v2f_);
+#pragma omp parallel for
+  for (long long i = 0; i < static_cast<long long>(ns); ++i) v2f_[i] /= 3;  // slot -> face (face order kept)
+  bucket_sort(
+      2 * static_cast<std::size_t>(ne), n,
+      [&](std::size_t h) { return edge_v_[h / 2][h % 2]; },
+      [&](U32 a, U32 b) { return edge_v_[a / 2][1 - a % 2] < edge_v_[b / 2][1 - b % 2]; }, v2v_off_, v2v_);
+#pragma omp parallel for
+  for (long long i = 0; i < static_cast<long long>(v2v_.size()); ++i) v2v_[i] = edge_v_[v2v_[i] / 2][1 - v2v_[i] % 2];
 }
 
 long Mesh::genus() const {

@@ -96,9 +96,9 @@ int launch_positions(const double* xyz, int nv, double scale, double* px, double
   return static_cast<int>(cudaGetLastError());
 }
 
-// Two passes (count, fill) around an exclusive scan; returns the column
-// count through *nnz, or -1 when a vertex has more than kMaxRel relations.
-int launch_front_csr(const FrontBuild& b, int* c_off, int** c_col, int* nnz, void* stream) {
+// Count pass + exclusive scan into c_off; returns the column count through
+// *nnz, or -1 when a vertex has more than kMaxRel relations.
+int launch_front_count(const FrontBuild& b, int* c_off, int* nnz, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int *counts = nullptr, *over = nullptr;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&counts), sizeof(int) * (b.nv + 1), s);
@@ -113,22 +113,24 @@ int launch_front_csr(const FrontBuild& b, int* c_off, int** c_col, int* nnz, voi
   void* tmp = nullptr;
   cudaMallocAsync(&tmp, tmp_bytes, s);
   cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, c_off, b.nv + 1, s);
+  note_launch(3);
   int h[2] = {0, 0};
   cudaMemcpyAsync(&h[0], c_off + b.nv, sizeof(int), cudaMemcpyDeviceToHost, s);
   cudaMemcpyAsync(&h[1], over, sizeof(int), cudaMemcpyDeviceToHost, s);
-  e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return static_cast<int>(e);
-  if (h[1]) return -1;
-  *nnz = h[0];
-  e = cudaMalloc(reinterpret_cast<void**>(c_col), sizeof(int) * static_cast<size_t>(h[0] > 0 ? h[0] : 1));
-  if (e != cudaSuccess) return static_cast<int>(e);
-  k_front_fill<<<blocks, 128, 0, s>>>(b, c_off, *c_col);
-  note_launch(4);
   cudaFreeAsync(tmp, s);
   cudaFreeAsync(counts, s);
   cudaFreeAsync(over, s);
   e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return static_cast<int>(e);
+  if (h[1]) return -1;
+  *nnz = h[0];
+  return static_cast<int>(cudaGetLastError());
+}
+
+int launch_front_fill(const FrontBuild& b, const int* c_off, int* c_col, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  k_front_fill<<<(b.nv + 127) / 128, 128, 0, s>>>(b, c_off, c_col);
+  note_launch();
   return static_cast<int>(cudaGetLastError());
 }
 
