@@ -146,8 +146,10 @@ int dtb_result_work(const dtb_result* r, uint64_t* sum_region, uint64_t* sum_int
 double dtb_bench_barrier(int blocks, int n, int mode);
 /* Kernels launched by this library so far (process-wide counter). */
 unsigned long long dtb_launch_count(void);
-/* Bytes the mesh's device copy occupies (the H2D volume of uploading it). */
+/* Bytes the mesh's device copy occupies (uploaded and device-derived arrays). */
 int dtb_mesh_device_bytes(const dtb_mesh* m, uint64_t* bytes);
+/* Bytes copied host->device to build the mesh's device copy. */
+int dtb_mesh_upload_bytes(const dtb_mesh* m, uint64_t* bytes);
 /* build_reeb (SPEC reeb): nodes = events, arcs = layer lifetimes. */
 int dtb_result_reeb(const dtb_result* r, int64_t* n_nodes, int64_t* n_arcs, int64_t* cycle_rank);
 int dtb_result_reeb_arcs(const dtb_result* r, uint32_t* from, uint32_t* to, uint32_t* layer);

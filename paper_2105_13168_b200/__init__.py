@@ -18,7 +18,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libdifftopo_b200.so")
+LIB_PATH = os.environ.get("DTB_LIBRARY") or os.path.join(_HERE, "lib", "libdifftopo_b200.so")  # override: A/B runs
 
 ERRORS = {
     1: "ParseError", 2: "TopologyError", 3: "DegeneracyError", 4: "InvalidParameter",
@@ -114,6 +114,7 @@ def load_library(path: str = LIB_PATH):
         "dtb_launch_count": (C.c_ulonglong, []),
         "dtb_bench_barrier": (C.c_double, [C.c_int, C.c_int, C.c_int]),
         "dtb_mesh_device_bytes": (C.c_int, [P, pU64]),
+        "dtb_mesh_upload_bytes": (C.c_int, [P, pU64]),
         "dtb_result_reeb_arcs": (C.c_int, [P, pU32, pU32, pU32]),
         "dtb_field_init": (C.c_int, [P, pU32, U32, pP]),
         "dtb_field_free": (None, [P]),
@@ -130,6 +131,8 @@ def load_library(path: str = LIB_PATH):
         "dtb_extract_isoline": (C.c_int, [P, pD, D, pU32, pU32, pI64, pD, pI64, pD, U32]),
     }
     for name, (res, args) in sig.items():
+        if os.environ.get("DTB_LIBRARY") and not hasattr(lib, name):
+            continue  # an older build under A/B comparison
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
@@ -215,6 +218,12 @@ class TriangleMesh:
     def device_bytes(self) -> int:
         b = C.c_uint64()
         _check(_lib.dtb_mesh_device_bytes(self._h, C.byref(b)))
+        return b.value
+
+    def upload_bytes(self) -> int:
+        """Host->device bytes of this mesh's device copy (builds it if needed)."""
+        b = C.c_uint64()
+        _check(_lib.dtb_mesh_upload_bytes(self._h, C.byref(b)))
         return b.value
 
     def save(self, path: str):

@@ -536,6 +536,14 @@ int dtb_mesh_device_bytes(const dtb_mesh* m, uint64_t* bytes) {
   });
 }
 
+int dtb_mesh_upload_bytes(const dtb_mesh* m, uint64_t* bytes) {
+  return guard([&] {
+    need(m, "mesh");
+    need(bytes, "bytes");
+    *bytes = m->device().h2d_bytes;
+  });
+}
+
 int dtb_result_work(const dtb_result* r, uint64_t* sum_region, uint64_t* sum_interest, double* t_pass_device,
                     double* t_kernel) {
   return guard([&] {

@@ -178,6 +178,7 @@ DeviceMesh::DeviceMesh(std::shared_ptr<const Mesh> mesh, cudaStream_t s) : mesh_
   c_col.alloc(static_cast<size_t>(std::max(1, nnzc)));
   ck(launch_front_fill(fb, c_off.p, c_col.p, s), "front connectivity");
   cuda_check(cudaStreamSynchronize(s), "mesh upload");
+  h2d_bytes = 8 * xyz.n + 4 * (faces.n + edges.n + fe.n + ef.n + n_off.n + m.v2v().size() + f_off.n + m.v2f().size());
 
   view_.nv = static_cast<int>(nv);
   view_.nf = static_cast<int>(nf);
@@ -448,6 +449,7 @@ std::shared_ptr<DeviceField> DeviceMesh::acquire_field(cudaStream_t s) {
 
 void DeviceField::setup() {
   const size_t nv = dm_->host().nv();
+  if (nv * kSlots >= 0xFFFFFFFFull) fail(kCapacityExceeded, "more than 134M vertices (32-bit union-find items)");
   cap_ = nv;
   cnt.alloc(nv);
   interest.alloc(nv);

@@ -87,6 +87,7 @@ class DeviceMesh : public std::enable_shared_from_this<DeviceMesh> {
   DevBuf<double> px, py, pz;
   DevBuf<long long> fx, fy, fz;
   DevBuf<unsigned> faces, edges;
+  size_t h2d_bytes = 0;  // host->device bytes of the upload
   DevBuf<int> c_off, c_col, n_off, n_col, f_off, f_col;  // front connectivity, neighbours, v2f
 
  private:

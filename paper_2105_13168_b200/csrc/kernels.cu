@@ -775,6 +775,13 @@ __device__ __forceinline__ unsigned uf_find(unsigned long long* par, unsigned x,
   }
 }
 
+// Parent words are read with plain (L1-cacheable) loads: a CTA's items share
+// hot roots, and measured alternatives that read through L2 (__ldcg) or
+// switch to L2 reads after a lost CAS are 1.7x slower on this phase.  A
+// stale L1 line can only make a non-root look like a root; the CAS against
+// it then fails, the atomic evicts the line from this SM's L1, and the
+// retry reads the current word.
+//
 // Randomised linking: the root with the smaller (hash, id) key is hooked
 // under the other.  Linking by plain id turns concurrently united bands (ring
 // paths with increasing ids) into pointer chains as long as the ring; random
