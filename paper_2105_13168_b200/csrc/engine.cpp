@@ -1021,7 +1021,10 @@ class PassEngine {
       res_.message = e.what();
     }
     res_.steps = step;
-    if (prof_.p) report_phases();
+    if (prof_.p) {
+      report_phases();
+      instr_report();
+    }
     {
       const Ctl c = field_->read_ctl();
       res_.sum_region = c.sum_region;
@@ -1054,6 +1057,10 @@ class PassEngine {
     p.stop_every_check = cfg_.on_check ? 1 : 0;
     if (const char* env = std::getenv("DTB_SPLIT_A"); env && env[0] == '1') p.split_a = 1;
     if (const char* env = std::getenv("DTB_NO_UNITE"); env && env[0] == '1') p.split_a_no_unite = 1;
+    // E and D spread round-robin over the CTAs, A filled from each CTA's last
+    // warp so it overlaps E (measured: E+A 14.4 -> 13.4 us per step).
+    p.map_mode = 1 | 2 | 8;
+    if (const char* env = std::getenv("DTB_MAP")) p.map_mode = std::atoi(env);
     return p;
   }
 

@@ -1,3 +1,5 @@
+#include <cstdio>
+#include <cstring>
 // Persistent diffusion-front engine for sm_100a.
 //
 // One cooperative launch executes many explicit-Euler steps of the initial
@@ -64,6 +66,40 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+// Build-time diagnostics (-DDTB_INSTR): per-item latency histograms of the
+// step phases (B commit, D union, E stats, A fast, A slow), 128 ns * 2^b
+// buckets, staged in shared memory and summed at kernel exit.
+#ifdef DTB_INSTR
+__device__ unsigned long long g_hist[6][16];
+__shared__ unsigned s_hist[6][16];
+__device__ __forceinline__ void instr_rec(int ph, unsigned long long t0) {
+  const unsigned long long dt = gtimer() - t0;
+  int b = 0;
+  while (b < 15 && (128ull << b) < dt) ++b;
+  atomicAdd(&s_hist[ph][b], 1u);
+}
+__device__ unsigned long long g_cp[16][2];
+__shared__ unsigned s_cp[16][2];  // 32-bit: native shared atomics (64-bit ones are CAS loops)
+__device__ __forceinline__ void instr_cp(int idx, unsigned long long t0) {
+  if ((threadIdx.x & 7) == 0) {
+    atomicAdd(&s_cp[idx][0], static_cast<unsigned>((static_cast<unsigned long long>(clock64()) - t0) >> 4));
+    atomicAdd(&s_cp[idx][1], 1u);
+  }
+}
+#define INSTR_CP(idx, t0) instr_cp(idx, t0)
+#define INSTR_C0(name) const unsigned long long name = static_cast<unsigned long long>(clock64())
+#define INSTR_T0(name) const unsigned long long name = gtimer()
+#define INSTR_REC(ph, name, cond) \
+  do {                            \
+    if (cond) instr_rec(ph, name); \
+  } while (0)
+#else
+#define INSTR_T0(name)
+#define INSTR_REC(ph, name, cond)
+#define INSTR_CP(idx, t0)
+#define INSTR_C0(name)
+#endif
+
 // Diagnostics (DTB_PHASE_PROF): per-CTA completion time of phase `ph` of the
 // first 64 steps of a launch, recorded just before the grid barrier.
 __device__ __forceinline__ unsigned long long gtimer_raw() {
@@ -90,6 +126,33 @@ __device__ __forceinline__ void grid_sync(Ctl*) {
   // cooperative_groups' grid barrier measured 1.2 us vs 2.6 us for a
   // counter/generation barrier with gpu-scope fences (148 CTAs, B200).
   cooperative_groups::this_grid().sync();
+}
+
+// The control words every thread needs after a barrier (list sizes, error
+// flags).  One thread per CTA reads them and shares them through shared
+// memory: 148 requests to the control line instead of one per warp (2,368),
+// which the L2 slice holding that line would serve one by one.
+struct CtlSnap {
+  int rcount[2];
+  int ilcount[2];
+  int lpar;
+  int error;
+  int error_vertex;
+  int spec_error;
+};
+static_assert(sizeof(CtlSnap) == 32, "CtlSnap mirrors the first 32 bytes of Ctl");
+__device__ __forceinline__ void ctl_snap(const Ctl* ctl, CtlSnap& sc) {
+  if (threadIdx.x == 0) {
+    const int4* src = reinterpret_cast<const int4*>(ctl);
+    int4* dst = reinterpret_cast<int4*>(&sc);
+    dst[0] = __ldcg(src);
+    dst[1] = __ldcg(src + 1);
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void grid_sync_snap(Ctl* ctl, CtlSnap& sc) {
+  cooperative_groups::this_grid().sync();
+  ctl_snap(ctl, sc);
 }
 
 // set_value semantics (layer_field.hpp:102): clamp above 1, prune below the
@@ -139,9 +202,19 @@ __device__ __forceinline__ bool col_set(unsigned short* nl, double* nx, int& nn,
 // ascending column order through width-8 shuffles -- the reference's
 // summation order -- so all lanes hold the same results.
 constexpr int kG = 8;    // lanes per vertex group
-constexpr int kReg = 4;  // neighbour-column slots kept in registers
+constexpr int kReg = 4;  // neighbour-column slots kept in registers (packed as 2x2 u16 below)
 
 __device__ __forceinline__ unsigned group_mask() { return 0xFFu << (threadIdx.x & 24); }
+
+// Work-to-CTA maps.  Rank r of a group (or thread) is spread round-robin over
+// the CTAs so every SM gets an equal share of a short list; the "high" map
+// fills each CTA from its last warp so that it does not collide with work
+// mapped from the first warp in the same phase.
+__device__ __forceinline__ int group_rank(int mode) {
+  const int gpb = blockDim.x / kG, gl = threadIdx.x / kG;
+  if (mode == 0) return (blockIdx.x * blockDim.x + threadIdx.x) / kG;
+  return (mode == 2 ? gpb - 1 - gl : gl) * gridDim.x + blockIdx.x;
+}
 
 __device__ __forceinline__ void cand_add(unsigned short* cl, double* ca, int& nc, bool& overflow, int l, double t) {
   int c = 0;
@@ -402,18 +475,148 @@ __device__ __forceinline__ void reg_insert(int (&El)[kN], double (&Ex)[kN], int&
   ++n;
 }
 
+// Staging for the ordered neighbour folds of update_vertex_fold: lane j of a
+// group parks its contributions here and lanes 0..5 each fold one column.
+constexpr int kFoldCols = kF + 2;  // kF candidate layers, base laplacian, total laplacian
+constexpr int kFoldSmem = kBlock * kFoldCols * static_cast<int>(sizeof(double));  // dynamic shared memory
+extern __shared__ double s_dyn[];
+__device__ __forceinline__ double (*fold_buf())[kFoldCols] { return reinterpret_cast<double(*)[kFoldCols]>(s_dyn); }
+
+// Gather of the fast path for rows of at most kG stiffness entries whose
+// neighbour columns fit kReg slots (the bulk of a front).  The candidate
+// layers are found first (group-wide ascending union of the active layers of
+// v and its neighbours), then every per-layer sum is one ordered fold: lane j
+// contributes s_j * x_j, and lane c adds the group's contributions for its
+// column in ascending neighbour order, exactly the reference's order.  This
+// replaces the per-(neighbour, slot) candidate insertion of the generic loop
+// (the longest dependent instruction chain of the step).  Returns false, with
+// no side effects, when the case does not fit.
+__device__ __forceinline__ bool gather_fold(const DevMesh& M, const DevField& F, const DevWork& W, int v, int cv,
+                                            const int (&Ol)[kF], int k0, int k1, int lane, unsigned gm, int (&Cl)[kF],
+                                            double (&Ca)[kF], int& nc, double& lapb, double& lapt, bool& bnear) {
+  const int k = k0 + lane;
+  const bool valid = k < k1;
+  double s = 0.0, bu = 0.0, au = 0.0;
+  int cu = 0;
+  unsigned short L[kReg];
+  double X[kReg];
+  unsigned amask = 0;
+#pragma unroll
+  for (int q = 0; q < kReg; ++q) {
+    L[q] = 0;
+    X[q] = 0.0;
+  }
+  if (valid) {
+    const int u = __ldg(M.s_col + k);
+    s = __ldg(M.s_val + k);
+    const size_t b = static_cast<size_t>(u) * kSlots;
+    cu = F.cnt[u];
+#pragma unroll
+    for (int q = 0; q < kReg; ++q) {
+      L[q] = F.lay[b + q];
+      X[q] = F.val[b + q];
+    }
+#pragma unroll
+    for (int q = 0; q < kReg; ++q)
+      if (q < cu) {
+        if (L[q] == 0) {
+          bu = X[q];
+        } else if (W.active[L[q]]) {
+          au = au + X[q];
+          amask |= 1u << q;
+        }
+      }
+  }
+  if (__any_sync(gm, cu > kReg)) return false;
+  unsigned omask = 0;
+#pragma unroll
+  for (int q = 0; q < kF; ++q)
+    if (q < cv && Ol[q] != 0 && W.active[Ol[q]]) omask |= 1u << q;
+  // Candidate layers, ascending.
+  nc = 0;
+  unsigned last = 0;
+#pragma unroll
+  for (int c = 0; c <= kF; ++c) {
+    unsigned m = 0xFFFFFFFFu;
+#pragma unroll
+    for (int q = 0; q < kReg; ++q)
+      if (((amask >> q) & 1) && L[q] > last) m = min(m, static_cast<unsigned>(L[q]));
+#pragma unroll
+    for (int q = 0; q < kF; ++q)
+      if (((omask >> q) & 1) && static_cast<unsigned>(Ol[q]) > last) m = min(m, static_cast<unsigned>(Ol[q]));
+    m = __reduce_min_sync(gm, m);
+    if (m == 0xFFFFFFFFu) break;
+    if (c == kF) return false;  // more than kF candidates
+    Cl[c] = static_cast<int>(m);
+    last = m;
+    ++nc;
+  }
+  // Contributions, staged per lane.
+  double(*s_fold)[kFoldCols] = fold_buf();
+  const int base = threadIdx.x & ~(kG - 1);
+  const int gshift = threadIdx.x & 24;
+  unsigned pm[kF];
+#pragma unroll
+  for (int c = 0; c < kF; ++c) {
+    double t = 0.0;
+    bool present = false;
+#pragma unroll
+    for (int q = 0; q < kReg; ++q)
+      if (c < nc && ((amask >> q) & 1) && L[q] == Cl[c]) {
+        t = s * X[q];
+        present = true;
+      }
+    s_fold[threadIdx.x][c] = t;
+    pm[c] = (__ballot_sync(gm, present) >> gshift) & 0xFFu;
+  }
+  s_fold[threadIdx.x][kF] = s * bu;
+  s_fold[threadIdx.x][kF + 1] = s * au;
+  const unsigned vm = (__ballot_sync(gm, valid) >> gshift) & 0xFFu;
+  bnear = bnear || ((__ballot_sync(gm, valid && bu > 0.0) >> gshift) & 0xFFu) != 0;
+  __syncwarp(gm);
+  double acc = 0.0;
+  if (lane < kFoldCols) {
+    unsigned use = vm;
+#pragma unroll
+    for (int c = 0; c < kF; ++c)
+      if (lane == c) use = pm[c];
+#pragma unroll
+    for (int jj = 0; jj < kG; ++jj)
+      if ((use >> jj) & 1) acc = acc + s_fold[base + jj][lane];
+  }
+  __syncwarp(gm);  // s_fold is reused by the group's next vertex
+#pragma unroll
+  for (int c = 0; c < kF; ++c) Ca[c] = __shfl_sync(gm, acc, c, kG);
+  lapb = __shfl_sync(gm, acc, kF, kG);
+  lapt = __shfl_sync(gm, acc, kF + 1, kG);
+  return true;
+}
+
 __device__ bool update_vertex_fast(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P, int i,
                                    int v, bool spec, int lane, unsigned gm) {
+  INSTR_C0(tA);
+  // Every load below is independent of the counts it is masked with, so the
+  // column, stiffness row and neighbour columns arrive in three dependent
+  // rounds (columns hold kSlots entries; slots past the count are ignored).
   const int cv = F.cnt[v];
-  if (cv > kF) return false;
   const size_t vb = static_cast<size_t>(v) * kSlots;
   int Ol[kF];
   double Ox[kF];
 #pragma unroll
   for (int q = 0; q < kF; ++q) {
-    Ol[q] = q < cv ? static_cast<int>(F.lay[vb + q]) : kNoLayer;
-    Ox[q] = q < cv ? F.val[vb + q] : 0.0;
+    Ol[q] = static_cast<int>(F.lay[vb + q]);
+    Ox[q] = F.val[vb + q];
   }
+  const int k0 = __ldg(M.s_off + v), k1 = __ldg(M.s_off + v + 1);
+  const double mass = __ldg(M.mass + v);
+  if (cv > kF) return false;
+  INSTR_CP(0, tA);
+#pragma unroll
+  for (int q = 0; q < kF; ++q)
+    if (q >= cv) {
+      Ol[q] = kNoLayer;
+      Ox[q] = 0.0;
+    }
   const double phib = (cv > 0 && Ol[0] == 0) ? Ox[0] : 0.0;
 
   int Cl[kF];
@@ -427,7 +630,10 @@ __device__ bool update_vertex_fast(const DevMesh& M, const DevField& F, const De
   bool over = false;
   double lapb = 0.0, lapt = 0.0;
   bool bnear = phib > 0.0;
-  const int k0 = __ldg(M.s_off + v), k1 = __ldg(M.s_off + v + 1);
+  const bool folded =
+      k1 - k0 <= kG && gather_fold(M, F, W, v, cv, Ol, k0, k1, lane, gm, Cl, Ca, nc, lapb, lapt, bnear);
+  INSTR_CP(1, tA);
+  if (!folded) {
   for (int kb = k0; kb < k1; kb += kG) {
     const int k = kb + lane;
     const bool valid = k < k1;
@@ -440,22 +646,26 @@ __device__ bool update_vertex_fast(const DevMesh& M, const DevField& F, const De
       L[q] = 0;
       X[q] = 0.0;
     }
+    unsigned amask = 0;  // bit q: neighbour slot q < cu holds an active layer
     if (valid) {
       u = __ldg(M.s_col + k);
       s = __ldg(M.s_val + k);
-      cu = F.cnt[u];
       const size_t b = static_cast<size_t>(u) * kSlots;
+      cu = F.cnt[u];
+#pragma unroll
+      for (int q = 0; q < kReg; ++q) {
+        L[q] = F.lay[b + q];
+        X[q] = F.val[b + q];
+      }
 #pragma unroll
       for (int q = 0; q < kReg; ++q)
         if (q < cu) {
-          L[q] = F.lay[b + q];
-          X[q] = F.val[b + q];
-        }
-#pragma unroll
-      for (int q = 0; q < kReg; ++q)
-        if (q < cu) {
-          if (L[q] == 0) bu = X[q];
-          else if (W.active[L[q]]) au = au + X[q];
+          if (L[q] == 0) {
+            bu = X[q];
+          } else if (W.active[L[q]]) {
+            au = au + X[q];
+            amask |= 1u << q;
+          }
         }
       for (int q = kReg; q < cu; ++q) {
         const int l = F.lay[b + q];
@@ -464,21 +674,35 @@ __device__ bool update_vertex_fast(const DevMesh& M, const DevField& F, const De
         else if (W.active[l]) au = au + x;
       }
     }
+    // Fold the group's neighbours in ascending column order (the reference's
+    // summation order).  Unrolled with group-uniform predicates so the
+    // shuffles issue ahead of the dependent additions.
     const int nvalid = min(kG, k1 - kb);
-    for (int jj = 0; jj < nvalid; ++jj) {
+    const unsigned l01 = static_cast<unsigned>(L[0]) | (static_cast<unsigned>(L[1]) << 16);
+    const unsigned l23 = static_cast<unsigned>(L[2]) | (static_cast<unsigned>(L[3]) << 16);
+    const unsigned meta = static_cast<unsigned>(cu) | (amask << 8);
+#pragma unroll
+    for (int jj = 0; jj < kG; ++jj) {
+      if (jj >= nvalid) break;
       const double s_ = __shfl_sync(gm, s, jj, kG);
-      const int cu_ = __shfl_sync(gm, cu, jj, kG);
+      const unsigned meta_ = __shfl_sync(gm, meta, jj, kG);
       const double bu_ = __shfl_sync(gm, bu, jj, kG);
       const double au_ = __shfl_sync(gm, au, jj, kG);
+      const unsigned l01_ = __shfl_sync(gm, l01, jj, kG);
+      const unsigned l23_ = __shfl_sync(gm, l23, jj, kG);
+      double x_[kReg];
+#pragma unroll
+      for (int q = 0; q < kReg; ++q) x_[q] = __shfl_sync(gm, X[q], jj, kG);
+      const int cu_ = static_cast<int>(meta_ & 0xFF);
+      const unsigned am_ = meta_ >> 8;
       lapb = lapb + s_ * bu_;
       lapt = lapt + s_ * au_;
       if (bu_ > 0.0) bnear = true;
+      const int lq[kReg] = {static_cast<int>(l01_ & 0xFFFF), static_cast<int>(l01_ >> 16),
+                            static_cast<int>(l23_ & 0xFFFF), static_cast<int>(l23_ >> 16)};
 #pragma unroll
-      for (int q = 0; q < kReg; ++q) {
-        const int l_ = __shfl_sync(gm, static_cast<int>(L[q]), jj, kG);
-        const double x_ = __shfl_sync(gm, X[q], jj, kG);
-        if (q < cu_ && l_ != 0 && W.active[l_]) cand_add_reg(Cl, Ca, nc, over, l_, s_ * x_);
-      }
+      for (int q = 0; q < kReg; ++q)
+        if ((am_ >> q) & 1) cand_add_reg(Cl, Ca, nc, over, lq[q], s_ * x_[q]);
       if (cu_ > kReg) {
         const int u_ = __shfl_sync(gm, u, jj, kG);
         const size_t b = static_cast<size_t>(u_) * kSlots;
@@ -497,9 +721,9 @@ __device__ bool update_vertex_fast(const DevMesh& M, const DevField& F, const De
       for (int c = 0; c < kF; ++c) found |= (c < nc && Cl[c] == Ol[q]);
       if (!found) cand_add_reg(Cl, Ca, nc, over, Ol[q], 0.0);
     }
+  }  // generic gather
   if (over) return false;
 
-  const double mass = __ldg(M.mass + v);
   const double lap_b = lapb / mass;
   bool touched = false;
   bool Cupd[kF];
@@ -552,6 +776,7 @@ __device__ bool update_vertex_fast(const DevMesh& M, const DevField& F, const De
       bnext = next;
     }
   }
+  INSTR_CP(2, tA);
   // Apply the updates with set_value semantics into a sorted register column.
   bool changed = false;
   int El[kN];
@@ -652,6 +877,7 @@ __device__ bool update_vertex_fast(const DevMesh& M, const DevField& F, const De
       n = m;
     }
   }
+  INSTR_CP(3, tA);
   const bool old_one = cv > 0 && Ol[0] == 0 && Ox[0] == 1.0;
   const bool new_one = n > 0 && El[0] == 0 && Ex[0] == 1.0;
   const size_t o = static_cast<size_t>(i) * kSlots;
@@ -732,31 +958,74 @@ __device__ __forceinline__ void queue_region(const DevWork& W, int u, int stamp,
 // one-ring (lane j queues entries j, j+8, ... of {v} U row(v)).
 __device__ void commit_vertex(const DevMesh& M, const DevField& F, const DevWork& W, int i, int v, int stamp,
                               int nxt, int lpar, int lane, unsigned gm, BlockQueue& Q) {
-  const int flag = W.sflag[i];
-  if (!(flag & 1)) return;
-  const int nn = W.scnt[i];
+  INSTR_C0(tB);
+  // Every load that depends only on (i, v) is issued up front: the scratch
+  // header and this lane's scratch slot, the stiffness row bounds and the
+  // band-list flag.  The commit then needs two more dependent rounds (row
+  // entries, stamp exchange) instead of six.
   const size_t o = static_cast<size_t>(i) * kSlots, d = static_cast<size_t>(v) * kSlots;
+  const int flag = W.sflag[i];
+  const int nn = W.scnt[i];
+  const unsigned short sl = W.slay[o + lane];
+  const double sx = W.sval[o + lane];
+  const int k0 = __ldg(M.s_off + v), k1 = __ldg(M.s_off + v + 1);
+  const unsigned char listed = W.in_list[v];
+  if (!(flag & 1)) return;
+  INSTR_CP(4, tB);
+  const int t0 = lane;  // first row entry of this lane: t = 0 is v itself
+  const int u0 = t0 == 0 ? v : (t0 <= k1 - k0 ? __ldg(M.s_col + k0 + t0 - 1) : -1);
   bool inter = false;
-  for (int j = lane; j < nn; j += kG) {
+  if (lane < nn) {
+    F.lay[d + lane] = sl;
+    F.val[d + lane] = sx;
+    inter = sx > 0.0 && sx < 1.0;
+  }
+  for (int j = lane + kG; j < nn; j += kG) {  // columns longer than kG (slow-path results)
     const double x = W.sval[o + j];
     F.lay[d + j] = W.slay[o + j];
     F.val[d + j] = x;
     inter |= (x > 0.0 && x < 1.0);
   }
   inter = __ballot_sync(gm, inter) != 0;
+  // Band index from the lanes' slots (make_binfo's definition) when the
+  // column fits the group; longer columns rescan scratch.
+  uint4 bi = make_uint4(0, 0, 0, 0);
+  if (inter) {
+    if (nn <= kG) {
+      const bool bd = lane < nn && sl != 0 && sx > W.band_lo && sx < W.sat;
+      const unsigned bm = (__ballot_sync(gm, bd) >> (threadIdx.x & 24)) & 0xFFu;
+      unsigned L[4], S[4], rest = bm;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int src = rest ? __ffs(rest) - 1 : 0;
+        const unsigned l = __shfl_sync(gm, static_cast<unsigned>(sl), src, kG);
+        L[t] = rest ? l : 0;
+        S[t] = rest ? static_cast<unsigned>(src) : 0;
+        rest &= rest - 1;
+      }
+      bi.x = L[0] | (L[1] << 16);
+      bi.y = L[2] | (L[3] << 16);
+      bi.z = S[0] | (S[1] << 16);
+      bi.w = S[2] | ((rest ? kBandOverflow : S[3]) << 16);
+    } else if (lane == 0) {
+      bi = make_binfo(W.slay + o, W.sval + o, nn, W.band_lo, W.sat);
+    }
+  }
   if (lane == 0) {
     F.cnt[v] = static_cast<unsigned char>(nn);
     F.interest[v] = inter ? 1 : 0;
-    F.binfo[v] = inter ? make_binfo(W.slay + o, W.sval + o, nn, W.band_lo, W.sat) : make_uint4(0, 0, 0, 0);
-    if (inter && !W.in_list[v]) {
+    F.binfo[v] = bi;
+    if (inter && !listed) {
       W.in_list[v] = 1;
       W.ilist[lpar][atomicAdd(&W.ctl->ilcount[lpar], 1)] = v;
     }
     const int delta = ((flag >> 2) & 1) - ((flag >> 1) & 1);
     if (delta) atomicAdd(&W.ctl->base_one, delta);
   }
-  const int k0 = __ldg(M.s_off + v), k1 = __ldg(M.s_off + v + 1);
-  for (int t = lane; t <= k1 - k0; t += kG) queue_region(W, t == 0 ? v : __ldg(M.s_col + k0 + t - 1), stamp, nxt, Q);
+  INSTR_CP(5, tB);
+  if (u0 >= 0) queue_region(W, u0, stamp, nxt, Q);
+  for (int t = lane + kG; t <= k1 - k0; t += kG) queue_region(W, __ldg(M.s_col + k0 + t - 1), stamp, nxt, Q);
+  INSTR_CP(7, tB);
 }
 
 __device__ __forceinline__ bool is_band(const DevWork& W, const StepParams& P, int l, double x) {
@@ -895,14 +1164,14 @@ __device__ __forceinline__ int band_slot_of(const DevField& F, const DevWork& W,
 }
 
 __device__ void phase_union(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P, int lpar,
-                            unsigned long long ep, int g0, int ng) {
-  const int n = W.ctl->ilcount[lpar];
+                            unsigned long long ep, int g0, int ng, int n) {
   const int* list = W.ilist[lpar];
   const int lane = threadIdx.x & (kG - 1);
   const bool trace = W.prof && blockIdx.x == 0 && threadIdx.x == 0;
   unsigned long long* tr = trace ? W.prof + (W.prof_cap - 64LL * 3 * gridDim.x - 16) : nullptr;
   if (trace) tr[0] = gtimer_raw();
   for (int idx = g0; idx < n; idx += ng) {
+    INSTR_T0(t0);
     const int v = list[idx];
     if (!F.interest[v]) continue;
     const uint4 bv = F.binfo[v];
@@ -933,6 +1202,7 @@ __device__ void phase_union(const DevMesh& M, const DevField& F, const DevWork& 
         if (trace) tr[4] = gtimer_raw();
       }
     }
+    INSTR_REC(1, t0, lane == 0);
   }
 }
 
@@ -997,23 +1267,41 @@ __device__ __forceinline__ unsigned long long seg_max_u64(unsigned peers, unsign
 // vertex's slots in lock step so contributions can be combined per warp.
 __device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P, int lpar,
                             int spar, unsigned long long ep, bool compact, BlockStats& S, BlockQueue& Q,
-                            PairQueue& QB) {
+                            PairQueue& QB, int n) {
   LayerStat* g = W.stat + static_cast<size_t>(spar) * kMaxActive;
-  const int n = W.ctl->ilcount[lpar];
   const int* list = W.ilist[lpar];
   const int lane = threadIdx.x & 31;
   const int trip = (n + gridDim.x * blockDim.x - 1) / (gridDim.x * blockDim.x);
   for (int r = 0; r < trip; ++r) {
-    const int idx = (r * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+    const int idx = (P.map_mode & 1) ? (r * blockDim.x + threadIdx.x) * gridDim.x + blockIdx.x
+                                     : (r * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+    INSTR_T0(t0);
+    INSTR_C0(tE);
     const int v = idx < n ? list[idx] : -1;
-    const bool live = v >= 0 && F.interest[v];
+    // One round of loads for everything the vertex contributes: flags, the
+    // first four column slots with their union-find words, the position.
+    const int vs = v >= 0 ? v : 0;
+    const size_t b = static_cast<size_t>(vs) * kSlots;
+    const unsigned char inter_v = F.interest[vs];
+    const int cnt_v = F.cnt[vs];
+    const uint2 lw = *reinterpret_cast<const uint2*>(F.lay + b);
+    const double2 x01 = *reinterpret_cast<const double2*>(F.val + b);
+    const double2 x23 = *reinterpret_cast<const double2*>(F.val + b + 2);
+    const ulonglong2 p01 = *reinterpret_cast<const ulonglong2*>(W.parent + b);
+    const ulonglong2 p23 = *reinterpret_cast<const ulonglong2*>(W.parent + b + 2);
+    const long long fxv = __ldg(M.fx + vs), fyv = __ldg(M.fy + vs), fzv = __ldg(M.fz + vs);
+    const int L4[4] = {static_cast<int>(lw.x & 0xFFFF), static_cast<int>(lw.x >> 16), static_cast<int>(lw.y & 0xFFFF),
+                       static_cast<int>(lw.y >> 16)};
+    const double X4[4] = {x01.x, x01.y, x23.x, x23.y};
+    const unsigned long long P4[4] = {p01.x, p01.y, p23.x, p23.y};
+    const bool live = v >= 0 && inter_v;
+    if (live) INSTR_CP(8, tE);
     if (compact) {
       if (live) bq_push(Q, &W.ctl->ilcount[lpar ^ 1], W.ilist[lpar ^ 1], v);
       else if (v >= 0) W.in_list[v] = 0;
     }
-    const int cv = live ? F.cnt[v] : 0;
-    const size_t b = static_cast<size_t>(live ? v : 0) * kSlots;
-    const double base = (cv > 0 && F.lay[b] == 0) ? F.val[b] : 0.0;
+    const int cv = live ? cnt_v : 0;
+    const double base = (cv > 0 && L4[0] == 0) ? X4[0] : 0.0;
     {
       const bool has = base > 0.0 && base < 1.0;
       const unsigned m = __ballot_sync(0xffffffffu, has);
@@ -1023,20 +1311,30 @@ __device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& 
         if (lane == __ffs(m) - 1) atomicMax(&S.bmax, bm);
       }
     }
-    long long px = 0, py = 0, pz = 0;
-    if (live) {
-      px = __ldg(M.fx + v);
-      py = __ldg(M.fy + v);
-      pz = __ldg(M.fz + v);
-    }
+    const long long px = live ? fxv : 0, py = live ? fyv : 0, pz = live ? fzv : 0;
+    if (live) INSTR_CP(9, tE);
     bool cand = false;
     const int kmax = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(cv));
     for (int k = 0; k < kmax; ++k) {
       int a = -1;
       bool band = false, unsat = false, root = false;
       if (k < cv) {
-        const int l = F.lay[b + k];
-        const double x = F.val[b + k];
+        int l = 0;
+        double x = 0.0;
+        unsigned long long pw = 0;
+        if (k < 4) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q == k) {
+              l = L4[q];
+              x = X4[q];
+              pw = P4[q];
+            }
+        } else {
+          l = F.lay[b + k];
+          x = F.val[b + k];
+          pw = W.parent[b + k];
+        }
         if (l != 0 && W.active[l]) {
           a = W.aidx[l];
           unsat = x > 0.0 && x < 1.0;
@@ -1046,8 +1344,7 @@ __device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& 
             // Unions are complete, so an item is a root iff its parent entry
             // is stale (never linked this epoch) or points to itself.
             const unsigned item = static_cast<unsigned>(v) * kSlots + k;
-            const unsigned long long p = W.parent[item];
-            root = (p >> 32) != ep || static_cast<unsigned>(p) == item;
+            root = (pw >> 32) != ep || static_cast<unsigned>(pw) == item;
             if (P.record_trails)
               bq_push(QB, &W.ctl->nbandpairs, W.bandpairs, make_int2(v, a), W.bandpair_cap, &W.ctl->bandpair_overflow);
           }
@@ -1082,6 +1379,7 @@ __device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& 
         }
       }
     }
+    if (live) INSTR_CP(10, tE);
     if (cand && !(base > P.coll_base_limit)) {
       int first = -1;
       for (int k = 0; k < cv; ++k) {
@@ -1092,6 +1390,8 @@ __device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& 
         else insert_pair(W, (static_cast<unsigned>(first) << 16) | static_cast<unsigned>(l), ep);
       }
     }
+    INSTR_REC(2, t0, live);
+    if (live) INSTR_CP(11, tE);
   }
 }
 
@@ -1200,11 +1500,16 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
   __shared__ BlockStats S;
   __shared__ BlockQueue Q;
   __shared__ PairQueue QB;
+  __shared__ CtlSnap SC;
   Ctl* ctl = W.ctl;
   if (threadIdx.x == 0) {
     Q.n = 0;
     QB.n = 0;
   }
+#ifdef DTB_INSTR
+  for (int i = threadIdx.x; i < 6 * 16; i += blockDim.x) s_hist[i / 16][i % 16] = 0;
+  for (int i = threadIdx.x; i < 32; i += blockDim.x) s_cp[i / 2][i % 2] = 0;
+#endif
   __syncthreads();
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int gsz = gridDim.x * blockDim.x;
@@ -1222,12 +1527,12 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       ctl->nbandpairs = 0;
       ctl->bandpair_overflow = 0;
     }
-    grid_sync(ctl);
+    grid_sync_snap(ctl, SC);
     ++ep;
-    phase_union(M, F, W, P, lpar, ep, gtid / kG, gsz / kG);
-    grid_sync(ctl);
+    phase_union(M, F, W, P, lpar, ep, group_rank(P.map_mode & 8 ? 1 : 0), gsz / kG, SC.ilcount[lpar]);
+    grid_sync_snap(ctl, SC);
     block_stats_init(S);
-    phase_stats(M, F, W, P, lpar, spar, ep, false, S, Q, QB);
+    phase_stats(M, F, W, P, lpar, spar, ep, false, S, Q, QB, SC.ilcount[lpar]);
     block_stats_flush(S, g, P.n_active, ctl);
     bq_flush(QB, &ctl->nbandpairs, W.bandpairs, W.bandpair_cap, &ctl->bandpair_overflow);
     grid_sync(ctl);
@@ -1258,16 +1563,17 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
   long long pend_step = 0;
   {  // prologue: A(step_begin)
     const int cur = static_cast<int>(step & 1);
-    const int nR = ctl->rcount[cur];
+    ctl_snap(ctl, SC);
+    const int nR = SC.rcount[cur];
     if (gtid == 0) {
       ctl->rcount[cur ^ 1] = 0;
       ctl->sum_region += static_cast<unsigned long long>(nR);
     }
-    for (int i = gtid / kG; i < nR; i += gsz / kG)
+    for (int i = group_rank(P.map_mode & 2 ? 2 : 0); i < nR; i += gsz / kG)
       if (!update_vertex_fast(M, F, W, P, i, W.region[cur][i], false, threadIdx.x & (kG - 1), group_mask()))
         update_vertex(M, F, W, P, i, W.region[cur][i], false, threadIdx.x & (kG - 1), group_mask());
-    grid_sync(ctl);
-    if (ctl->error) stop = kStopError;
+    grid_sync_snap(ctl, SC);
+    if (SC.error) stop = kStopError;
   }
   for (; stop == 0 && step < P.step_end; ++step) {
     const int cur = static_cast<int>(step & 1), nxt = cur ^ 1;
@@ -1276,12 +1582,16 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
     const long long pslot = (step - P.step_begin) * 4;
     const bool prof = W.prof && gtid == 0 && pslot + 3 < W.prof_cap;
     if (prof) W.prof[pslot] = gtimer();
-    // ---- 1: B(s)
+    // ---- 1: B(s)   (SC: snapshot taken after the previous barrier)
     {
-      const int nR = ctl->rcount[cur];
-      for (int i = gtid / kG; i < nR; i += gsz / kG)
+      const int nR = SC.rcount[cur];
+      for (int i = group_rank(P.map_mode & 4 ? 1 : 0); i < nR; i += gsz / kG)
+      {
+        INSTR_T0(t0);
         commit_vertex(M, F, W, i, W.region[cur][i], static_cast<int>(step), nxt, lpar, threadIdx.x & (kG - 1),
                       group_mask(), Q);
+        INSTR_REC(0, t0, (threadIdx.x & (kG - 1)) == 0);
+      }
       bq_flush(Q, &ctl->rcount[nxt], W.region[nxt]);
       block_stats_init(S);
       if (pend && P.record_trails) phase_snap(M, W, static_cast<int>(pend_step & 1), S);
@@ -1291,7 +1601,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
         ctl->hash_acc = 0;
       }
     }
-    grid_sync(ctl);
+    grid_sync_snap(ctl, SC);
     if (prof) W.prof[pslot + 1] = gtimer();
     block_start(W, step - (P.step_end - 64), 1);
     if (check) {
@@ -1307,8 +1617,10 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
         ctl->base_max_bits = 0;
         ctl->nbandpairs = 0;
       }
-      if (gtid == 0) ctl->sum_interest += static_cast<unsigned long long>(ctl->ilcount[lpar]);
-      phase_union(M, F, W, P, lpar, ep, gtid / kG, gsz / kG);
+      const int nband = SC.ilcount[lpar];
+      const int nR1 = SC.rcount[nxt];  // final since B(s)
+      if (gtid == 0) ctl->sum_interest += static_cast<unsigned long long>(nband);
+      phase_union(M, F, W, P, lpar, ep, group_rank(P.map_mode & 8 ? 1 : 0), gsz / kG, nband);
       if (P.do_hash) phase_hash(F, W, M.nv);
       block_done(W, step - (P.step_end - 64), 1);
       grid_sync(ctl);
@@ -1317,7 +1629,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       // ---- 3: E(s) + speculative A(s+1)
       const int spar = cur;
       block_stats_init(S);
-      phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, QB);
+      phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, QB, nband);
       block_stats_flush(S, W.stat + static_cast<size_t>(spar) * kMaxActive, P.n_active, ctl);
       bq_flush(Q, &ctl->ilcount[lpar ^ 1], W.ilist[lpar ^ 1]);
       bq_flush(QB, &ctl->nbandpairs, W.bandpairs, W.bandpair_cap, &ctl->bandpair_overflow);
@@ -1326,17 +1638,22 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
           grid_sync(ctl);
           if (prof) W.prof[pslot + 3] = gtimer();
         }
-        const int nR1 = ctl->rcount[nxt];
         if (gtid == 0) {
           ctl->rcount[cur] = 0;
           ctl->sum_region += static_cast<unsigned long long>(nR1);
         }
-        for (int i = gtid / kG; i < nR1; i += gsz / kG)
-          if (!update_vertex_fast(M, F, W, P, i, W.region[nxt][i], true, threadIdx.x & (kG - 1), group_mask()))
+        for (int i = group_rank(P.map_mode & 2 ? 2 : 0); i < nR1; i += gsz / kG) {
+          INSTR_T0(t0);
+          if (!update_vertex_fast(M, F, W, P, i, W.region[nxt][i], true, threadIdx.x & (kG - 1), group_mask())) {
             update_vertex(M, F, W, P, i, W.region[nxt][i], true, threadIdx.x & (kG - 1), group_mask());
+            INSTR_REC(4, t0, (threadIdx.x & (kG - 1)) == 0);
+          } else {
+            INSTR_REC(3, t0, (threadIdx.x & (kG - 1)) == 0);
+          }
+        }
       }
       block_done(W, step - (P.step_end - 64), 2);
-      grid_sync(ctl);
+      grid_sync_snap(ctl, SC);
       if (prof && !P.split_a) W.prof[pslot + 3] = gtimer();
       lpar ^= 1;
       if (P.do_hash && gtid == 0) {
@@ -1349,7 +1666,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
         stop = bits;
         break;  // the speculative A(s+1) is discarded; the host relaunches at s+1
       }
-      if (ctl->spec_error) {
+      if (SC.spec_error) {
         if (gtid == 0) {
           ctl->error = ctl->spec_error;
           ctl->error_vertex = ctl->spec_error_vertex;
@@ -1367,17 +1684,17 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
         for (int a = gtid; a < P.n_active; a += gsz) flush_stat(M, W, P, a, static_cast<int>(pend_step & 1), pend_step, true);
       pend = false;
       if (more) {
-        const int nR1 = ctl->rcount[nxt];
+        const int nR1 = SC.rcount[nxt];  // snapshot after B(s)
         if (gtid == 0) {
           ctl->rcount[cur] = 0;
           ctl->sum_region += static_cast<unsigned long long>(nR1);
         }
-        for (int i = gtid / kG; i < nR1; i += gsz / kG)
+        for (int i = group_rank(P.map_mode & 2 ? 2 : 0); i < nR1; i += gsz / kG)
           if (!update_vertex_fast(M, F, W, P, i, W.region[nxt][i], false, threadIdx.x & (kG - 1), group_mask()))
             update_vertex(M, F, W, P, i, W.region[nxt][i], false, threadIdx.x & (kG - 1), group_mask());
       }
-      grid_sync(ctl);
-      if (ctl->error) {
+      grid_sync_snap(ctl, SC);
+      if (SC.error) {
         stop = kStopError;
         ++step;
         break;
@@ -1398,6 +1715,13 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
     ctl->epoch = static_cast<long long>(ep);
     ctl->lpar = lpar;
   }
+#ifdef DTB_INSTR
+  __syncthreads();
+  for (int i = threadIdx.x; i < 6 * 16; i += blockDim.x)
+    if (s_hist[i / 16][i % 16]) atomicAdd(&g_hist[i / 16][i % 16], s_hist[i / 16][i % 16]);
+  for (int i = threadIdx.x; i < 32; i += blockDim.x)
+    if (s_cp[i / 2][i % 2]) atomicAdd(&g_cp[i / 2][i % 2], static_cast<unsigned long long>(s_cp[i / 2][i % 2]));
+#endif
 }
 
 // Barrier microbenchmark (diagnostics): n grid barriers, no work.
@@ -1410,6 +1734,20 @@ __global__ void __launch_bounds__(kBlock, 1) k_barrier_bench(Ctl* ctl, int n, in
   }
 }
 
+// Shared memory above the 48 KB static limit must be opted into per kernel.
+cudaError_t engine_attributes() {
+  static cudaError_t done = [] {
+    const void* fns[] = {reinterpret_cast<const void*>(&k_engine<0>), reinterpret_cast<const void*>(&k_engine<1>),
+                         reinterpret_cast<const void*>(&k_engine<2>), reinterpret_cast<const void*>(&k_engine<3>)};
+    for (const void* fn : fns) {
+      const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kFoldSmem);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }();
+  return done;
+}
+
 int coop_launch(const void* fn, int blocks, const DevMesh& m, const DevField& f, const DevWork& w,
                 const StepParams& p, void* stream) {
   DevMesh mm = m;
@@ -1417,8 +1755,10 @@ int coop_launch(const void* fn, int blocks, const DevMesh& m, const DevField& f,
   DevWork ww = w;
   StepParams pp = p;
   void* args[] = {&mm, &ff, &ww, &pp};
+  const cudaError_t ea = engine_attributes();
+  if (ea != cudaSuccess) return static_cast<int>(ea);
   note_launch();
-  return static_cast<int>(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kBlock), args, 0,
+  return static_cast<int>(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kBlock), args, kFoldSmem,
                                                       static_cast<cudaStream_t>(stream)));
 }
 
@@ -1434,13 +1774,40 @@ int dev_max_coresident_blocks(int* out) {
   if (e != cudaSuccess) return static_cast<int>(e);
   e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return static_cast<int>(e);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_engine<0>, kBlock, 0);
+  e = engine_attributes();
+  if (e != cudaSuccess) return static_cast<int>(e);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_engine<0>, kBlock, kFoldSmem);
   if (e != cudaSuccess) return static_cast<int>(e);
   int per1 = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k_engine<1>, kBlock, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k_engine<1>, kBlock, kFoldSmem);
   if (per1 < per) per = per1;
   *out = sms * (per < 1 ? 1 : per);
   return 0;
+}
+
+void instr_report() {
+#ifdef DTB_INSTR
+  unsigned long long h[6][16];
+  cudaMemcpyFromSymbol(h, g_hist, sizeof(h));
+  static const char* names[6] = {"B commit", "D union", "E stats", "A fast", "A slow", "-"};
+  for (int p = 0; p < 5; ++p) {
+    unsigned long long n = 0;
+    for (int b = 0; b < 16; ++b) n += h[p][b];
+    std::fprintf(stderr, "[dtb] instr %-8s n=%10llu  buckets(128ns*2^b):", names[p], n);
+    for (int b = 0; b < 16; ++b) std::fprintf(stderr, " %llu", h[p][b]);
+    std::fprintf(stderr, "\n");
+  }
+  std::memset(h, 0, sizeof(h));
+  cudaMemcpyToSymbol(g_hist, h, sizeof(h));
+  unsigned long long c[16][2];
+  cudaMemcpyFromSymbol(c, g_cp, sizeof(c));
+  std::fprintf(stderr, "[dtb] instr checkpoints (avg SM cycles since item start):");
+  for (int i = 0; i < 16; ++i)
+    if (c[i][1]) std::fprintf(stderr, " cp%d=%.0f", i, 16.0 * static_cast<double>(c[i][0]) / c[i][1]);
+  std::fprintf(stderr, "\n");
+  std::memset(c, 0, sizeof(c));
+  cudaMemcpyToSymbol(g_cp, c, sizeof(c));
+#endif
 }
 
 int launch_run(const DevMesh& m, const DevField& f, const DevWork& w, const StepParams& p, int blocks,
@@ -1454,16 +1821,18 @@ int launch_check(const DevMesh& m, const DevField& f, const DevWork& w, const St
 }
 
 int launch_snap(const DevMesh& m, const DevField& f, const DevWork& w, const StepParams& p, void* stream) {
+  if (const cudaError_t ea = engine_attributes(); ea != cudaSuccess) return static_cast<int>(ea);
   note_launch();
-  k_engine<2><<<148 * 4, kBlock, 0, static_cast<cudaStream_t>(stream)>>>(m, f, w, p);
+  k_engine<2><<<148 * 4, kBlock, kFoldSmem, static_cast<cudaStream_t>(stream)>>>(m, f, w, p);
   return static_cast<int>(cudaGetLastError());
 }
 
 int launch_flush(const DevMesh& m, const DevField& f, const DevWork& w, const StepParams& p, void* stream) {
   const int blocks = (p.n_active + kBlock - 1) / kBlock;
   if (blocks == 0) return 0;
+  if (const cudaError_t ea = engine_attributes(); ea != cudaSuccess) return static_cast<int>(ea);
   note_launch();
-  k_engine<3><<<blocks, kBlock, 0, static_cast<cudaStream_t>(stream)>>>(m, f, w, p);
+  k_engine<3><<<blocks, kBlock, kFoldSmem, static_cast<cudaStream_t>(stream)>>>(m, f, w, p);
   return static_cast<int>(cudaGetLastError());
 }
 

@@ -196,6 +196,7 @@ struct StepParams {
   int do_check;  // 0: advance only (one-shot step())
   int split_a;   // diagnostics: run the next step's update in its own phase
   int split_a_no_unite;  // diagnostics only: skip unions (wrong results; timing)
+  int map_mode;          // work-to-CTA maps, bits: 1 spread E, 2 A from the last warp, 4 spread B, 8 spread D
 };
 
 // --- launchers (kernels.cu) -------------------------------------------------
@@ -236,6 +237,7 @@ struct FrontBuild {
 };
 int launch_positions(const double* xyz, int nv, double scale, double* px, double* py, double* pz, long long* fx,
                      long long* fy, long long* fz, void* stream);
+void instr_report();  // -DDTB_INSTR builds: latency histograms
 int launch_front_count(const FrontBuild& b, int* c_off, int* nnz, void* stream);
 int launch_front_fill(const FrontBuild& b, const int* c_off, int* c_col, void* stream);
 int launch_spmv(int nv, const int* off, const int* col, const double* val, const double* mass,
