@@ -88,6 +88,9 @@ int dtb_mesh_vertices(const dtb_mesh* m, double* xyz);                   /* 3 nv
 int dtb_mesh_faces(const dtb_mesh* m, uint32_t* faces);                  /* 3 nf */
 int dtb_mesh_edges(const dtb_mesh* m, uint32_t* ev, uint32_t* ef);       /* 2 ne each */
 int dtb_mesh_face_edges(const dtb_mesh* m, uint32_t* fe);                /* 3 nf */
+/* CSR adjacency: vertex_neighbors (sorted) and vertex_faces (face order),
+   mesh.hpp:57-62.  Offsets have nv+1 entries; v2v has 2 ne, v2f 3 nf. */
+int dtb_mesh_adjacency(const dtb_mesh* m, uint32_t* v2v_off, uint32_t* v2v, uint32_t* v2f_off, uint32_t* v2f);
 /* seed_region (diffusion.hpp:134); two-call. */
 int dtb_seed_region(const dtb_mesh* m, uint32_t seed, double radius, uint32_t* out, uint32_t cap, uint32_t* n);
 

@@ -84,6 +84,7 @@ def load_library(path: str = LIB_PATH):
         "dtb_mesh_faces": (C.c_int, [P, pU32]),
         "dtb_mesh_edges": (C.c_int, [P, pU32, pU32]),
         "dtb_mesh_face_edges": (C.c_int, [P, pU32]),
+        "dtb_mesh_adjacency": (C.c_int, [P, pU32, pU32, pU32, pU32]),
         "dtb_seed_region": (C.c_int, [P, U32, D, pU32, U32, pU32]),
         "dtb_laplacian_assemble": (C.c_int, [P, pP]),
         "dtb_laplacian_from_csr": (C.c_int, [P, pI32, pI32, pD, pD, I64, D, pP]),
@@ -264,6 +265,16 @@ class TriangleMesh:
         out = np.empty((self.info()["F"], 3), np.uint32)
         _check(_lib.dtb_mesh_face_edges(self._h, _ptr(out, C.c_uint32)))
         return out
+
+    def adjacency(self):
+        """(v2v_off, v2v, v2f_off, v2f): sorted vertex neighbours and incident
+        faces in face order (mesh.hpp:57-62)."""
+        i = self.info()
+        vo, vv = np.empty(i["V"] + 1, np.uint32), np.empty(2 * i["E"], np.uint32)
+        fo, ff = np.empty(i["V"] + 1, np.uint32), np.empty(3 * i["F"], np.uint32)
+        _check(_lib.dtb_mesh_adjacency(self._h, _ptr(vo, C.c_uint32), _ptr(vv, C.c_uint32), _ptr(fo, C.c_uint32),
+                                       _ptr(ff, C.c_uint32)))
+        return vo, vv, fo, ff
 
     def seed_region(self, seed: int, radius: float) -> np.ndarray:
         n = C.c_uint32()

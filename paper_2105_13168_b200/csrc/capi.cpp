@@ -2,6 +2,8 @@
 // into error codes and keeps a per-thread message.
 #include "../../include/difftopo_b200.h"
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -14,14 +16,21 @@ double bench_barrier(int blocks, int n, int mode);
 
 using namespace dtb;
 
+// A mesh is built on the host (generators, files, unusual soups) or on the
+// device (dtb_mesh_from_arrays on a GPU box); the other side is derived on
+// first use.
 struct dtb_mesh {
-  std::shared_ptr<const Mesh> host;
+  std::shared_ptr<const Mesh> host_mesh;
   mutable std::shared_ptr<DeviceMesh> dev;
   mutable cudaStream_t stream = nullptr;
+  const Mesh& host() const { return host_mesh ? *host_mesh : dev->host(); }
+  Index nv() const { return host_mesh ? host_mesh->nv() : dev->nv(); }
+  Index nf() const { return host_mesh ? host_mesh->nf() : dev->nf(); }
+  Index ne() const { return host_mesh ? host_mesh->ne() : dev->ne(); }
   DeviceMesh& device() const {
     if (!dev) {
       if (!stream) cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
-      dev = std::make_shared<DeviceMesh>(host, stream);
+      dev = std::make_shared<DeviceMesh>(host_mesh, stream);
     }
     return *dev;
   }
@@ -176,12 +185,25 @@ int dtb_mesh_from_arrays(const double* xyz, uint32_t nv, const uint32_t* faces, 
     need(out, "out");
     need(xyz, "xyz");
     need(faces, "faces");
-    std::vector<V3> v(nv);
-    for (uint32_t i = 0; i < nv; ++i) v[i] = {xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]};
-    std::vector<std::array<Index, 3>> f(nf);
-    std::memcpy(f.data(), faces, sizeof(uint32_t) * 3 * static_cast<size_t>(nf));
     auto m = std::make_unique<dtb_mesh>();
-    m->host = std::make_shared<Mesh>(std::move(v), std::move(f));
+    // On a GPU box the soup is validated, oriented and indexed on the device;
+    // the host builds it when there is no device or the input is unusual
+    // (which includes every invalid input: the host raises the reference's
+    // exact error).
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0 && !std::getenv("DTB_HOST_MESH")) {
+      cuda_check(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking), "stream");
+      m->dev = DeviceMesh::from_soup(xyz, nv, faces, nf, m->stream);
+    } else {
+      cudaGetLastError();  // clear the no-device status
+    }
+    if (!m->dev) {
+      std::vector<V3> v(nv);
+      for (uint32_t i = 0; i < nv; ++i) v[i] = {xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]};
+      std::vector<std::array<Index, 3>> f(nf);
+      std::memcpy(f.data(), faces, sizeof(uint32_t) * 3 * static_cast<size_t>(nf));
+      m->host_mesh = std::make_shared<Mesh>(std::move(v), std::move(f));
+    }
     *out = m.release();
   });
 }
@@ -191,7 +213,7 @@ int dtb_mesh_generate(const char* spec, dtb_mesh** out) {
     need(out, "out");
     need(spec, "spec");
     auto m = std::make_unique<dtb_mesh>();
-    m->host = std::make_shared<Mesh>(make_mesh(spec));
+    m->host_mesh = std::make_shared<Mesh>(make_mesh(spec));
     *out = m.release();
   });
 }
@@ -201,7 +223,7 @@ int dtb_mesh_load(const char* path, int32_t format, dtb_mesh** out) {
     need(out, "out");
     need(path, "path");
     auto m = std::make_unique<dtb_mesh>();
-    m->host = std::make_shared<Mesh>(load_mesh(path, format));
+    m->host_mesh = std::make_shared<Mesh>(load_mesh(path, format));
     *out = m.release();
   });
 }
@@ -212,9 +234,9 @@ int dtb_mesh_save(const dtb_mesh* m, const char* path) {
     need(path, "path");
     std::string p(path);
     auto ext = p.substr(p.find_last_of('.') + 1);
-    if (ext == "dtm") write_dtm(*m->host, p);
-    else if (ext == "ply") save_ply(*m->host, p, nullptr, true);
-    else if (ext == "obj") save_obj(*m->host, p);
+    if (ext == "dtm") write_dtm(m->host(), p);
+    else if (ext == "ply") save_ply(m->host(), p, nullptr, true);
+    else if (ext == "obj") save_obj(m->host(), p);
     else fail(kParseError, "unsupported mesh extension ." + ext);
   });
 }
@@ -224,11 +246,17 @@ void dtb_mesh_free(dtb_mesh* m) { delete m; }
 int dtb_mesh_info(const dtb_mesh* m, uint32_t* nv, uint32_t* ne, uint32_t* nf, int64_t* euler, int64_t* genus) {
   return guard([&] {
     need(m, "mesh");
-    if (nv) *nv = m->host->nv();
-    if (ne) *ne = m->host->ne();
-    if (nf) *nf = m->host->nf();
-    if (euler) *euler = m->host->euler();
-    if (genus) *genus = m->host->genus();
+    if (nv) *nv = m->nv();
+    if (ne) *ne = m->ne();
+    if (nf) *nf = m->nf();
+    const long chi = static_cast<long>(m->nv()) - static_cast<long>(m->ne()) + static_cast<long>(m->nf());
+    if (euler) *euler = chi;
+    if (genus) {
+      if ((2 - chi) % 2 != 0 || chi > 2)  // Mesh::genus
+        fail(kTopologyError,
+             "euler characteristic " + std::to_string(chi) + " is not that of a closed orientable surface");
+      *genus = (2 - chi) / 2;
+    }
   });
 }
 
@@ -236,27 +264,30 @@ int dtb_mesh_vertices(const dtb_mesh* m, double* xyz) {
   return guard([&] {
     need(m, "mesh");
     need(xyz, "xyz");
-    std::memcpy(xyz, m->host->positions().data(), sizeof(double) * 3 * m->host->nv());
+    const Mesh& h = m->host();
+    std::memcpy(xyz, h.positions().data(), sizeof(double) * 3 * h.nv());
   });
 }
 int dtb_mesh_faces(const dtb_mesh* m, uint32_t* f) {
   return guard([&] {
     need(m, "mesh");
     need(f, "faces");
-    std::memcpy(f, m->host->faces().data(), sizeof(uint32_t) * 3 * m->host->nf());
+    const Mesh& h = m->host();
+    std::memcpy(f, h.faces().data(), sizeof(uint32_t) * 3 * h.nf());
   });
 }
 int dtb_mesh_edges(const dtb_mesh* m, uint32_t* ev, uint32_t* ef) {
   return guard([&] {
     need(m, "mesh");
-    for (Index e = 0; e < m->host->ne(); ++e) {
+    const Mesh& h = m->host();
+    for (Index e = 0; e < h.ne(); ++e) {
       if (ev) {
-        ev[2 * e] = m->host->edge_vertices(e)[0];
-        ev[2 * e + 1] = m->host->edge_vertices(e)[1];
+        ev[2 * e] = h.edge_vertices(e)[0];
+        ev[2 * e + 1] = h.edge_vertices(e)[1];
       }
       if (ef) {
-        ef[2 * e] = m->host->edge_faces(e)[0];
-        ef[2 * e + 1] = m->host->edge_faces(e)[1];
+        ef[2 * e] = h.edge_faces(e)[0];
+        ef[2 * e + 1] = h.edge_faces(e)[1];
       }
     }
   });
@@ -265,15 +296,45 @@ int dtb_mesh_face_edges(const dtb_mesh* m, uint32_t* fe) {
   return guard([&] {
     need(m, "mesh");
     need(fe, "fe");
-    for (Index f = 0; f < m->host->nf(); ++f)
-      for (int k = 0; k < 3; ++k) fe[3 * f + k] = m->host->face_edges(f)[k];
+    const Mesh& h = m->host();
+    for (Index f = 0; f < h.nf(); ++f)
+      for (int k = 0; k < 3; ++k) fe[3 * f + k] = h.face_edges(f)[k];
   });
 }
+int dtb_mesh_adjacency(const dtb_mesh* m, uint32_t* v2v_off, uint32_t* v2v, uint32_t* v2f_off, uint32_t* v2f) {
+  return guard([&] {
+    need(m, "mesh");
+    const Mesh& h = m->host();
+    auto put = [](uint32_t* dst, const std::vector<uint32_t>& src) {
+      if (dst) std::memcpy(dst, src.data(), sizeof(uint32_t) * src.size());
+    };
+    put(v2v_off, h.v2v_off());
+    put(v2v, h.v2v());
+    put(v2f_off, h.v2f_off());
+    put(v2f, h.v2f());
+  });
+}
+
 int dtb_seed_region(const dtb_mesh* m, uint32_t seed, double radius, uint32_t* out, uint32_t cap, uint32_t* n) {
   return guard([&] {
     need(m, "mesh");
-    if (seed >= m->host->nv()) fail(kInvalidParameter, "seed vertex out of range");
-    auto s = seed_region(*m->host, seed, radius);
+    if (seed >= m->nv()) fail(kInvalidParameter, "seed vertex out of range");
+    std::vector<Index> s;
+    bool done = false;
+    if (const char* e = std::getenv("DTB_SEED_DEVICE"); e && e[0] == '1') {  // parity tests of the device Dijkstra
+      std::vector<unsigned> buf(8192);
+      int cnt = 0;
+      const DeviceMesh& d = m->device();
+      cuda_check(static_cast<cudaError_t>(launch_seed_region(d.view(), seed, radius, buf.data(),
+                                                             static_cast<int>(buf.size()), &cnt, m->stream)),
+                 "seed region");
+      if (cnt >= 0) {
+        s.assign(buf.begin(), buf.begin() + cnt);
+        std::sort(s.begin(), s.end());
+        done = true;
+      }
+    }
+    if (!done) s = seed_region(m->host(), seed, radius);
     if (n) *n = static_cast<uint32_t>(s.size());
     if (out && cap >= s.size()) std::memcpy(out, s.data(), sizeof(uint32_t) * s.size());
   });
@@ -299,7 +360,7 @@ int dtb_laplacian_from_csr(const dtb_mesh* m, const int32_t* off, const int32_t*
     need(out, "out");
     need(off, "off");
     need(mass, "mass");
-    const size_t nv = m->host->nv();
+    const size_t nv = m->nv();
     auto L = std::make_unique<dtb_laplacian>();
     cuda_check(cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking), "stream");
     m->device();
@@ -724,8 +785,8 @@ int dtb_extract_isoline(const dtb_mesh* m, const double* values, double level, u
   return guard([&] {
     need(m, "mesh");
     need(values, "values");
-    std::vector<double> vals(values, values + m->host->nv());
-    auto loops = extract_isoline(*m->host, vals, level);
+    std::vector<double> vals(values, values + m->nv());
+    auto loops = extract_isoline(m->host(), vals, level);
     if (n_loops) *n_loops = static_cast<uint32_t>(loops.size());
     size_t total = 0;
     for (size_t i = 0; i < loops.size(); ++i) {

@@ -34,7 +34,25 @@ size_t size_class(size_t bytes) {
 }
 }  // namespace
 
+// Stream-ordered allocations (cub temporaries) come from the default memory
+// pool; keep its memory mapped between synchronizations instead of returning
+// it to the driver every time (a re-map costs milliseconds for large blocks).
+void keep_default_pool() {
+  static const bool done = [] {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      std::uint64_t keep = 8ull << 30;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+    return true;
+  }();
+  (void)done;
+}
+
 void* dev_alloc(size_t bytes) {
+  keep_default_pool();
   const size_t c = size_class(bytes);
   {
     std::lock_guard<std::mutex> lk(g_alloc_mu);
@@ -120,32 +138,25 @@ V3 mean_of(const Mesh& m, const std::vector<Index>& verts) {
 
 DeviceMesh::DeviceMesh(std::shared_ptr<const Mesh> mesh, cudaStream_t s) : mesh_(std::move(mesh)) {
   const Mesh& m = *mesh_;
-  const Index nv = m.nv(), nf = m.nf(), ne = m.ne();
+  nv_ = m.nv();
+  nf_ = m.nf();
+  ne_ = m.ne();
+  const Index nv = nv_, nf = nf_, ne = ne_;
   static_assert(sizeof(V3) == 24 && sizeof(std::array<Index, 3>) == 12 && sizeof(std::array<Index, 2>) == 8,
                 "packed host arrays are uploaded as-is");
   double maxabs = 1e-300;
   for (const V3& q : m.positions()) maxabs = std::max({maxabs, std::abs(q.x), std::abs(q.y), std::abs(q.z)});
-  // Fixed point with |coord| * 2^k <= 2^38: band sums of up to 2^25 vertices
-  // stay exact in int64 (order-independent device reductions).
-  const int k = 38 - static_cast<int>(std::ceil(std::log2(maxabs)));
   // Host arrays go up unchanged; SoA / fixed-point positions and the
   // front-connectivity CSR are derived on the device.
   DevBuf<double> xyz(3 * static_cast<size_t>(nv));
   xyz.upload(reinterpret_cast<const double*>(m.positions().data()), xyz.n, s);
-  px.alloc(nv);
-  py.alloc(nv);
-  pz.alloc(nv);
-  fx.alloc(nv);
-  fy.alloc(nv);
-  fz.alloc(nv);
-  ck(launch_positions(xyz.p, static_cast<int>(nv), std::ldexp(1.0, k), px.p, py.p, pz.p, fx.p, fy.p, fz.p, s),
-     "positions");
   faces.alloc(3 * static_cast<size_t>(nf));
   faces.upload(reinterpret_cast<const unsigned*>(m.faces().data()), faces.n, s);
   edges.alloc(2 * static_cast<size_t>(ne));
   edges.upload(reinterpret_cast<const unsigned*>(&m.edge_vertices(0)[0]), edges.n, s);
-  DevBuf<unsigned> fe(3 * static_cast<size_t>(nf)), ef(2 * static_cast<size_t>(ne));
+  fe.alloc(3 * static_cast<size_t>(nf));
   fe.upload(reinterpret_cast<const unsigned*>(&m.face_edges(0)[0]), fe.n, s);
+  ef.alloc(2 * static_cast<size_t>(ne));
   ef.upload(reinterpret_cast<const unsigned*>(&m.edge_faces(0)[0]), ef.n, s);
   n_off.alloc(nv + 1);
   n_off.upload(reinterpret_cast<const int*>(m.v2v_off().data()), n_off.n, s);
@@ -155,6 +166,88 @@ DeviceMesh::DeviceMesh(std::shared_ptr<const Mesh> mesh, cudaStream_t s) : mesh_
   f_off.upload(reinterpret_cast<const int*>(m.v2f_off().data()), f_off.n, s);
   f_col.alloc(std::max<size_t>(1, m.v2f().size()));
   f_col.upload(reinterpret_cast<const int*>(m.v2f().data()), m.v2f().size(), s);
+  h2d_bytes = 8 * xyz.n + 4 * (faces.n + edges.n + fe.n + ef.n + n_off.n + m.v2v().size() + f_off.n + m.v2f().size());
+  derive(xyz.p, maxabs, s);
+}
+
+namespace {
+// DTB_TIMING=1: stage times of mesh construction on stderr (diagnostics).
+struct StageTimer {
+  bool on = false;
+  cudaStream_t s;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  explicit StageTimer(cudaStream_t st) : s(st) {
+    const char* e = std::getenv("DTB_TIMING");
+    on = e && e[0] == '1';
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[dtb] %-14s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+}  // namespace
+
+std::shared_ptr<DeviceMesh> DeviceMesh::from_soup(const double* xyz, size_t nv, const std::uint32_t* soup, size_t nf,
+                                                  cudaStream_t s) {
+  if (nv == 0 || nf == 0 || nv >= (1u << 31) || 3 * nf >= (1u << 31)) return nullptr;
+  StageTimer tm(s);
+  std::shared_ptr<DeviceMesh> d(new DeviceMesh());
+  d->xyz_.alloc(3 * nv);
+  d->xyz_.upload(xyz, 3 * nv, s);
+  DevBuf<unsigned> in(3 * nf);
+  in.upload(soup, 3 * nf, s);
+  const size_t ne = 3 * nf / 2;
+  d->faces.alloc(3 * nf);
+  d->edges.alloc(2 * ne);
+  d->ef.alloc(2 * ne);
+  d->fe.alloc(3 * nf);
+  d->f_off.alloc(nv + 1);
+  d->f_col.alloc(3 * nf);
+  d->n_off.alloc(nv + 1);
+  d->n_col.alloc(2 * ne);
+  tm.mark("upload");
+  MeshBuild b;
+  b.nv = static_cast<int>(nv);
+  b.nf = static_cast<int>(nf);
+  b.xyz = d->xyz_.p;
+  b.soup = in.p;
+  b.faces = d->faces.p;
+  b.edges = d->edges.p;
+  b.edge_faces = d->ef.p;
+  b.face_edges = d->fe.p;
+  b.v2f_off = d->f_off.p;
+  b.v2f = d->f_col.p;
+  b.v2v_off = d->n_off.p;
+  b.v2v = d->n_col.p;
+  const int rc = build_mesh(b, s);
+  tm.mark("build");
+  if (rc == 1) return nullptr;
+  ck(rc, "device mesh construction");
+  d->nv_ = static_cast<Index>(nv);
+  d->nf_ = static_cast<Index>(nf);
+  d->ne_ = static_cast<Index>(b.ne);
+  d->h2d_bytes = 8 * 3 * nv + 4 * 3 * nf;
+  d->derive(d->xyz_.p, std::max(1e-300, b.maxabs), s);
+  tm.mark("derive");
+  return d;
+}
+
+void DeviceMesh::derive(const double* d_xyz, double maxabs, cudaStream_t s) {
+  const Index nv = nv_, nf = nf_, ne = ne_;
+  // Fixed point with |coord| * 2^k <= 2^38: band sums of up to 2^25 vertices
+  // stay exact in int64 (order-independent device reductions).
+  const int k = 38 - static_cast<int>(std::ceil(std::log2(maxabs)));
+  px.alloc(nv);
+  py.alloc(nv);
+  pz.alloc(nv);
+  fx.alloc(nv);
+  fy.alloc(nv);
+  fz.alloc(nv);
+  ck(launch_positions(d_xyz, static_cast<int>(nv), std::ldexp(1.0, k), px.p, py.p, pz.p, fx.p, fy.p, fz.p, s),
+     "positions");
   // Front connectivity: for each vertex the higher-numbered mesh neighbours
   // and apexes of the faces across its link edges.  Two band vertices are
   // related iff their stars contain edge-adjacent faces, which makes
@@ -178,7 +271,6 @@ DeviceMesh::DeviceMesh(std::shared_ptr<const Mesh> mesh, cudaStream_t s) : mesh_
   c_col.alloc(static_cast<size_t>(std::max(1, nnzc)));
   ck(launch_front_fill(fb, c_off.p, c_col.p, s), "front connectivity");
   cuda_check(cudaStreamSynchronize(s), "mesh upload");
-  h2d_bytes = 8 * xyz.n + 4 * (faces.n + edges.n + fe.n + ef.n + n_off.n + m.v2v().size() + f_off.n + m.v2f().size());
 
   view_.nv = static_cast<int>(nv);
   view_.nf = static_cast<int>(nf);
@@ -198,21 +290,67 @@ DeviceMesh::DeviceMesh(std::shared_ptr<const Mesh> mesh, cudaStream_t s) : mesh_
   view_.n_col = n_col.p;
 }
 
+std::shared_ptr<const Mesh> DeviceMesh::host_ptr() const {
+  std::lock_guard<std::mutex> lk(host_mu_);
+  if (mesh_) return mesh_;
+  // Device-built mesh: download its arrays once (own stream, pinned staging
+  // is not worth it for a one-off copy).
+  if (const char* e = std::getenv("DTB_TIMING"); e && e[0] == '1') std::fprintf(stderr, "[dtb] host mesh download\n");
+  cudaStream_t s = nullptr;
+  cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  std::vector<V3> pos(nv_);
+  std::vector<std::array<Index, 3>> fcs(nf_), fed(nf_);
+  std::vector<std::array<Index, 2>> ev(ne_), efs(ne_);
+  std::vector<std::uint32_t> v2f_off(nv_ + 1), v2v_off(nv_ + 1);
+  std::vector<Index> v2f(3 * static_cast<size_t>(nf_)), v2v(2 * static_cast<size_t>(ne_));
+  auto get = [&](void* dst, const void* src, size_t bytes) {
+    cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s), "mesh download");
+  };
+  get(pos.data(), xyz_.p, sizeof(V3) * nv_);
+  get(fcs.data(), faces.p, 12 * static_cast<size_t>(nf_));
+  get(fed.data(), fe.p, 12 * static_cast<size_t>(nf_));
+  get(ev.data(), edges.p, 8 * static_cast<size_t>(ne_));
+  get(efs.data(), ef.p, 8 * static_cast<size_t>(ne_));
+  get(v2f_off.data(), f_off.p, 4 * (static_cast<size_t>(nv_) + 1));
+  get(v2v_off.data(), n_off.p, 4 * (static_cast<size_t>(nv_) + 1));
+  get(v2f.data(), f_col.p, 4 * v2f.size());
+  get(v2v.data(), n_col.p, 4 * v2v.size());
+  const cudaError_t e = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  cuda_check(e, "mesh download");
+  mesh_ = std::make_shared<const Mesh>(Mesh::from_index(std::move(pos), std::move(fcs), std::move(ev), std::move(efs),
+                                                        std::move(fed), std::move(v2f_off), std::move(v2f),
+                                                        std::move(v2v_off), std::move(v2v)));
+  return mesh_;
+}
+
+V3 DeviceMesh::position(Index v) const {
+  {
+    std::lock_guard<std::mutex> lk(host_mu_);
+    if (mesh_) return mesh_->p(v);
+  }
+  V3 q;
+  const size_t i = v;
+  cuda_check(cudaMemcpy(&q.x, px.p + i, sizeof(double), cudaMemcpyDeviceToHost), "position");
+  cuda_check(cudaMemcpy(&q.y, py.p + i, sizeof(double), cudaMemcpyDeviceToHost), "position");
+  cuda_check(cudaMemcpy(&q.z, pz.p + i, sizeof(double), cudaMemcpyDeviceToHost), "position");
+  return q;
+}
+
 // ---------------------------------------------------------------------------
 // DeviceLaplacian
 
 DeviceLaplacian::DeviceLaplacian(std::shared_ptr<DeviceMesh> dm, cudaStream_t s) : dm_(std::move(dm)) {
-  const Mesh& m = dm_->host();
-  const int nv = static_cast<int>(m.nv());
+  const int nv = static_cast<int>(dm_->nv());
   off.alloc(nv + 1);
-  col.alloc(static_cast<size_t>(nv) + 2 * static_cast<size_t>(m.ne()));
+  col.alloc(static_cast<size_t>(nv) + 2 * static_cast<size_t>(dm_->ne()));
   val.alloc(col.n);
   mass.alloc(nv);
   DevBuf<double> grow(nv);
   DevBuf<int> dnnz(1);
   LapBuild b{};
   b.nv = nv;
-  b.nf = static_cast<int>(m.nf());
+  b.nf = static_cast<int>(dm_->nf());
   b.px = dm_->px.p;
   b.py = dm_->py.p;
   b.pz = dm_->pz.p;
@@ -240,7 +378,7 @@ DeviceLaplacian::DeviceLaplacian(std::shared_ptr<DeviceMesh> dm, const std::vect
                                  const std::vector<double>& v, const std::vector<double>& ms, double gershgorin,
                                  cudaStream_t s)
     : dm_(std::move(dm)), nnz_(static_cast<int>(c.size())), gersh_(gershgorin) {
-  const size_t nv = dm_->host().nv();
+  const size_t nv = dm_->nv();
   if (o.size() != nv + 1 || ms.size() != nv || c.size() != v.size() || o.back() != static_cast<int>(c.size()))
     fail(kDimensionMismatch, "operator does not match the mesh");
   off.alloc(o.size());
@@ -256,7 +394,7 @@ DeviceLaplacian::DeviceLaplacian(std::shared_ptr<DeviceMesh> dm, const std::vect
 
 void DeviceLaplacian::download(std::vector<int>& o, std::vector<int>& c, std::vector<double>& v, std::vector<double>& ms,
                                cudaStream_t s) const {
-  const size_t nv = dm_->host().nv();
+  const size_t nv = dm_->nv();
   o = to_host(off, nv + 1, s);
   c = to_host(col, nnz_, s);
   v = to_host(val, nnz_, s);
@@ -264,7 +402,7 @@ void DeviceLaplacian::download(std::vector<int>& o, std::vector<int>& c, std::ve
 }
 
 void DeviceLaplacian::apply(const double* xh, double* yh, cudaStream_t s) const {
-  const int nv = static_cast<int>(dm_->host().nv());
+  const int nv = static_cast<int>(dm_->nv());
   DevBuf<double> x(nv), y(nv);
   x.upload(xh, nv, s);
   ck(launch_spmv(nv, off.p, col.p, val.p, mass.p, x.p, y.p, s), "spmv");
@@ -420,7 +558,7 @@ constexpr size_t kPoolKeep = 4;
 
 std::shared_ptr<DeviceField> DeviceMesh::acquire_field(cudaStream_t s) {
   DeviceField* f = nullptr;
-  const size_t need = host().nv();
+  const size_t need = nv();
   {
     std::lock_guard<std::mutex> lk(g_pool_mu);
     size_t best = g_pool.size();
@@ -448,7 +586,7 @@ std::shared_ptr<DeviceField> DeviceMesh::acquire_field(cudaStream_t s) {
 }
 
 void DeviceField::setup() {
-  const size_t nv = dm_->host().nv();
+  const size_t nv = dm_->nv();
   if (nv * kSlots >= 0xFFFFFFFFull) fail(kCapacityExceeded, "more than 134M vertices (32-bit union-find items)");
   cap_ = nv;
   cnt.alloc(nv);
@@ -502,7 +640,7 @@ void DeviceField::setup() {
   view_.binfo = binfo.p;
   // Event-time scratch (layer pulls, isoline crossings, edits): allocated once
   // so host event handling never calls cudaMalloc/cudaFree.
-  const size_t ncap = std::max<size_t>(nv, dm_->host().ne()) + 1;
+  const size_t ncap = std::max<size_t>(nv, dm_->ne()) + 1;
   ai0.alloc(ncap);
   ai1.alloc(ncap);
   ad0.alloc(ncap);
@@ -523,7 +661,7 @@ void DeviceField::setup() {
 
 void DeviceField::init(const std::vector<Index>& seeds) {
   if (seeds.empty()) fail(kEmptySeed, "seed set is empty");
-  const Index nv = dm_->host().nv();
+  const Index nv = dm_->nv();
   for (Index v : seeds)
     if (v >= nv) fail(kInvalidParameter, "seed vertex out of range");
   meta_.clear();
@@ -584,7 +722,7 @@ Ctl DeviceField::read_ctl() const {
 }
 
 std::vector<std::pair<Index, double>> DeviceField::layer_values(Index layer) const {
-  const int nv = static_cast<int>(dm_->host().nv());
+  const int nv = static_cast<int>(dm_->nv());
   cuda_check(cudaMemsetAsync(acnt.p, 0, sizeof(int), s_), "memset");
   ck(launch_pull_layer(view_, nv, static_cast<int>(layer), ai0.p, ad0.p, acnt.p, s_), "pull layer");
   const int n = to_host(acnt, 1, s_)[0];
@@ -597,13 +735,13 @@ std::vector<std::pair<Index, double>> DeviceField::layer_values(Index layer) con
 }
 
 std::vector<double> DeviceField::dense_row(Index layer) const {
-  const int nv = static_cast<int>(dm_->host().nv());
+  const int nv = static_cast<int>(dm_->nv());
   ck(launch_dense_row(view_, nv, static_cast<int>(layer), ad0.p, s_), "dense row");
   return to_host(ad0, nv, s_);
 }
 
 std::vector<Index> DeviceField::covered_set(double threshold) const {
-  const int nv = static_cast<int>(dm_->host().nv());
+  const int nv = static_cast<int>(dm_->nv());
   cuda_check(cudaMemsetAsync(acnt.p, 0, sizeof(int), s_), "memset");
   ck(launch_covered(view_, nv, threshold, ai0.p, acnt.p, s_), "covered");
   const int n = to_host(acnt, 1, s_)[0];
@@ -615,7 +753,7 @@ std::vector<Index> DeviceField::covered_set(double threshold) const {
 unsigned long long DeviceField::hash() const {
   unsigned long long* h = reinterpret_cast<unsigned long long*>(acnt.p + 8);
   cuda_check(cudaMemsetAsync(h, 0, sizeof(unsigned long long), s_), "memset");
-  ck(launch_field_hash(view_, static_cast<int>(dm_->host().nv()), h, s_), "hash");
+  ck(launch_field_hash(view_, static_cast<int>(dm_->nv()), h, s_), "hash");
   unsigned long long out = 0;
   cuda_check(cudaMemcpyAsync(&out, h, sizeof out, cudaMemcpyDeviceToHost, s_), "D2H");
   cuda_check(cudaStreamSynchronize(s_), "hash sync");
@@ -625,7 +763,7 @@ unsigned long long DeviceField::hash() const {
 int DeviceField::base_one_count() const {
   DevBuf<int> h(1);
   h.zero(s_);
-  ck(launch_base_one_count(view_, static_cast<int>(dm_->host().nv()), h.p, s_), "base one");
+  ck(launch_base_one_count(view_, static_cast<int>(dm_->nv()), h.p, s_), "base one");
   return to_host(h, 1, s_)[0];
 }
 
@@ -633,7 +771,7 @@ void DeviceField::normalize_columns() {
   Ctl c = read_ctl();
   c.error = 0;
   ctl.upload(&c, 1, s_);
-  ck(launch_normalize_all(view_, work_, static_cast<int>(dm_->host().nv()), prune_epsilon, s_), "normalize");
+  ck(launch_normalize_all(view_, work_, static_cast<int>(dm_->nv()), prune_epsilon, s_), "normalize");
   if (read_ctl().error == kDevZeroColumn) fail(kZeroColumn, "total field extinction at a vertex");
 }
 
@@ -714,7 +852,7 @@ Index DeviceField::merge_layers(const std::vector<Index>& ids, long step_, std::
   std::vector<int> order(sorted_ids);
   std::sort(order.begin(), order.end());
   if (order != sorted_ids) fail(kInvalidMerge, "merge ids must be ascending (reference groups are sorted)");
-  const int nv = static_cast<int>(dm_->host().nv());
+  const int nv = static_cast<int>(dm_->nv());
   ai1.upload(sorted_ids.data(), ids.size(), s_);
   cuda_check(cudaMemsetAsync(acnt.p, 0, sizeof(int), s_), "memset");
   ck(launch_merge(view_, work_, nv, ai1.p, static_cast<int>(ids.size()), static_cast<int>(result), ai0.p, acnt.p, s_),
@@ -889,7 +1027,7 @@ void run_check_kernel(DeviceField& field, const Config& cfg, const Coefficients&
   p.step_begin = s;
   static int maxco = 0;
   if (!maxco) ck(dev_max_coresident_blocks(&maxco), "occupancy");
-  const int blocks = std::min(maxco, engine_blocks(static_cast<int>(field.mesh().host().nv())));
+  const int blocks = std::min(maxco, engine_blocks(static_cast<int>(field.mesh().nv())));
   ck(launch_check(field.mesh().view(), field.view(), field.work(), p, blocks, field.stream()), "check kernel");
   cuda_check(cudaStreamSynchronize(field.stream()), "check sync");
 }
@@ -953,9 +1091,9 @@ class PassEngine {
  public:
   PassEngine(std::shared_ptr<DeviceMesh> dm, const DeviceLaplacian& op, Index seed, const Config& cfg,
              const Coefficients& co)
-      : dm_(std::move(dm)), mesh_(dm_->host()), op_(op), cfg_(cfg), co_(co) {
+      : dm_(std::move(dm)), op_(op), cfg_(cfg), co_(co) {
     cfg_.validate();
-    if (seed >= mesh_.nv()) fail(kInvalidParameter, "seed vertex out of range");
+    if (seed >= dm_->nv()) fail(kInvalidParameter, "seed vertex out of range");
     cuda_check(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking), "stream");
     cuda_check(cudaEventCreate(&ev0_), "event");
     cuda_check(cudaEventCreate(&ev1_), "event");
@@ -968,7 +1106,22 @@ class PassEngine {
     res_.seed_vertex = seed;
     const double radius =
         cfg_.seed_radius > 0 ? cfg_.seed_radius : 1.5 * (co_.gradient_energy / std::sqrt(co_.penalty));
-    const std::vector<Index> seeds = seed_region(mesh_, seed, radius);
+    // A device-built mesh runs the Dijkstra on the device rather than
+    // downloading its host copy; capacity overflow falls back to the host.
+    std::vector<Index> seeds;
+    bool seeded = false;
+    if (!dm_->has_host()) {
+      std::vector<unsigned> buf(8192);
+      int n = 0;
+      ck(launch_seed_region(dm_->view(), seed, radius, buf.data(), static_cast<int>(buf.size()), &n, s_),
+         "seed region");
+      if (n >= 0) {
+        seeds.assign(buf.begin(), buf.begin() + n);
+        std::sort(seeds.begin(), seeds.end());
+        seeded = true;
+      }
+    }
+    if (!seeded) seeds = seed_region(mesh(), seed, radius);
     field_->init(seeds);
     dt_ = cfg_.dt > 0 ? cfg_.dt : stable_time_step(op_, co_);
     res_.dt_used = dt_;
@@ -980,12 +1133,12 @@ class PassEngine {
     ev.kind = EventKind::Seed;
     ev.step = 0;
     ev.layers = {1};
-    ev.position = mesh_.p(seed);
+    ev.position = dm_->position(seed);
     res_.events.push_back(ev);
     track(1).created_event = 0;
     std::vector<int> sv(seeds.begin(), seeds.end());
     field_->mark_region(op_.view(), sv, 0, 1);
-    blocks_ = engine_blocks(static_cast<int>(mesh_.nv()));
+    blocks_ = engine_blocks(static_cast<int>(dm_->nv()));
     if (const char* env = std::getenv("DTB_PHASE_PROF"); env && env[0] == '1') {
       prof_.alloc(4 * static_cast<size_t>(std::min<long>(cfg_.max_steps, 100000)) + 8 + 2 * 64 * 3 * 160 + 64);
       prof_.zero(s_);
@@ -1127,7 +1280,7 @@ class PassEngine {
       return a.step != b.step ? a.step < b.step : a.layer < b.layer;
     });
     for (const auto& r : recs) {
-      if (cfg_.record_trails) track(static_cast<Index>(r.layer)).trail.push_back(mesh_.p(static_cast<Index>(r.vertex)));
+      if (cfg_.record_trails) track(static_cast<Index>(r.layer)).trail.push_back(V3{r.vx, r.vy, r.vz});
     }
     const int zero = 0;
     cuda_check(cudaMemcpyAsync(&field_->ctl.p->ntrail, &zero, sizeof(int), cudaMemcpyHostToDevice, s_), "ntrail");
@@ -1175,8 +1328,8 @@ class PassEngine {
     for (size_t head = 0; head < queue.size(); ++head) {
       const Index v = queue[head];
       const Index c = label.at(v);
-      for (Index o = mesh_.v2v_off()[v]; o < mesh_.v2v_off()[v + 1]; ++o) {
-        const Index u = mesh_.v2v()[o];
+      for (Index o = mesh().v2v_off()[v]; o < mesh().v2v_off()[v + 1]; ++o) {
+        const Index u = mesh().v2v()[o];
         if (!is_unsat(u)) continue;
         if (label.emplace(u, c).second) queue.push_back(u);
       }
@@ -1198,7 +1351,7 @@ class PassEngine {
     ev.step = s;
     ev.layers = {layer};
     ev.produced = children;
-    ev.position = mean_of(mesh_, parent_band);
+    ev.position = mean_of(mesh(), parent_band);
     const Index idx = static_cast<Index>(res_.events.size());
     res_.events.push_back(std::move(ev));
     track(layer).consumed_event = idx;
@@ -1224,7 +1377,7 @@ class PassEngine {
       b1[static_cast<Index>(e[i])] = bb[i];
     }
     std::sort(e.begin(), e.end());
-    std::vector<SurfaceLoop> loops = chain_crossings(mesh_, e, t_of);
+    std::vector<SurfaceLoop> loops = chain_crossings(mesh(), e, t_of);
     double best = -1;
     for (auto& loop : loops) {
       double base_mass = 0;
@@ -1271,7 +1424,7 @@ class PassEngine {
     ev.kind = EventKind::Merge;
     ev.step = s;
     ev.layers = group;
-    ev.position = mean_of(mesh_, union_band);
+    ev.position = mean_of(mesh(), union_band);
     ev.covered_snapshot = field_->covered_set(cfg_.covered_threshold);
     const Index idx = static_cast<Index>(res_.events.size());
     if (!loops.empty()) {
@@ -1311,7 +1464,7 @@ class PassEngine {
     if (!get_lastpos(layer, p)) {
       std::vector<Index> support;
       for (const auto& [v, x] : field_->layer_values(layer)) support.push_back(v);
-      p = mean_of(mesh_, support);
+      p = mean_of(mesh(), support);
     }
     ev.position = p;
     const Index idx = static_cast<Index>(res_.events.size());
@@ -1457,7 +1610,7 @@ class PassEngine {
   }
 
   std::shared_ptr<DeviceMesh> dm_;
-  const Mesh& mesh_;
+  const Mesh& mesh() const { return dm_->host(); }  // downloaded on first use for device-built meshes
   const DeviceLaplacian& op_;
   Config cfg_;
   Coefficients co_;

@@ -76,22 +76,43 @@ class DeviceField;
 // passes on one mesh do not re-allocate hundreds of MB.
 class DeviceMesh : public std::enable_shared_from_this<DeviceMesh> {
  public:
+  // Uploads a host-built mesh.
   explicit DeviceMesh(std::shared_ptr<const Mesh> mesh, cudaStream_t s);
+  // Builds the mesh on the device from a triangle soup (csrc/meshbuild.cu);
+  // nullptr when the host must build it (unusual or invalid input).
+  static std::shared_ptr<DeviceMesh> from_soup(const double* xyz, size_t nv, const std::uint32_t* faces, size_t nf,
+                                               cudaStream_t s);
   ~DeviceMesh();
   // A field workspace for this mesh from the process-wide pool.
   std::shared_ptr<DeviceField> acquire_field(cudaStream_t s);
-  const Mesh& host() const { return *mesh_; }
-  std::shared_ptr<const Mesh> host_ptr() const { return mesh_; }
+  Index nv() const { return nv_; }
+  Index nf() const { return nf_; }
+  Index ne() const { return ne_; }
+  // The host mesh; for a device-built mesh it is downloaded on first use.
+  const Mesh& host() const { return *host_ptr(); }
+  std::shared_ptr<const Mesh> host_ptr() const;
+  V3 position(Index v) const;  // one vertex position, without the host mesh
+  bool has_host() const {
+    std::lock_guard<std::mutex> lk(host_mu_);
+    return static_cast<bool>(mesh_);
+  }
   DevMesh view() const { return view_; }  // stiffness fields are filled by DeviceLaplacian::view()
 
   DevBuf<double> px, py, pz;
   DevBuf<long long> fx, fy, fz;
-  DevBuf<unsigned> faces, edges;
+  DevBuf<unsigned> faces, edges, fe, ef;  // faces, edge vertices, face->edges, edge->faces
   size_t h2d_bytes = 0;  // host->device bytes of the upload
   DevBuf<int> c_off, c_col, n_off, n_col, f_off, f_col;  // front connectivity, neighbours, v2f
 
  private:
-  std::shared_ptr<const Mesh> mesh_;
+  DeviceMesh() = default;
+  // Positions (SoA + fixed point) and the front-connectivity CSR from the
+  // uploaded or device-built arrays.
+  void derive(const double* d_xyz, double maxabs, cudaStream_t s);
+  mutable std::mutex host_mu_;
+  mutable std::shared_ptr<const Mesh> mesh_;
+  DevBuf<double> xyz_;  // device-built meshes keep their positions for the host download
+  Index nv_ = 0, nf_ = 0, ne_ = 0;
   DevMesh view_;
 };
 

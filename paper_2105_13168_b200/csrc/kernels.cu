@@ -1463,6 +1463,9 @@ __device__ void flush_stat(const DevMesh& M, const DevWork& W, const StepParams&
       r.mx = mx;
       r.my = my;
       r.mz = mz;
+      r.vx = M.px[r.vertex];
+      r.vy = M.py[r.vertex];
+      r.vz = M.pz[r.vertex];
       W.trail[pos & (kTrailCap - 1)] = r;
     }
   }

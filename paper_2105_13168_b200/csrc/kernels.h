@@ -143,6 +143,7 @@ struct TrailRec {
   long long step;
   int layer, vertex;
   double mx, my, mz;  // band mean (last_band_position_)
+  double vx, vy, vz;  // position of `vertex` (the trail point)
 };
 
 struct DevField {
@@ -237,7 +238,26 @@ struct FrontBuild {
 };
 int launch_positions(const double* xyz, int nv, double scale, double* px, double* py, double* pz, long long* fx,
                      long long* fy, long long* fz, void* stream);
-void instr_report();  // -DDTB_INSTR builds: latency histograms
+void instr_report();
+// seed_region on the device: *n = -1 when a capacity is exceeded (use the host).
+int launch_seed_region(const DevMesh& m, unsigned seed, double radius, unsigned* out, int cap, int* n, void* stream);  // -DDTB_INSTR builds: latency histograms
+// Device mesh construction (csrc/meshbuild.cu).  Returns 0 when the soup is a
+// valid closed, connected, consistently oriented manifold without unused
+// vertices (outputs filled, ne = 3nf/2), 1 when the host must build it (any
+// other input, including every error case), else a CUDA error.
+struct MeshBuild {
+  int nv = 0, nf = 0, ne = 0;
+  const double* xyz = nullptr;     // 3nv, device
+  const unsigned* soup = nullptr;  // 3nf input faces, device
+  unsigned *faces = nullptr, *edges = nullptr, *edge_faces = nullptr, *face_edges = nullptr;  // 3F, 2E, 2E, 3F
+  int *v2f_off = nullptr, *v2f = nullptr, *v2v_off = nullptr, *v2v = nullptr;              // V+1, 3F, V+1, 2E
+  double maxabs = 0;  // out: max |coordinate|
+  int flipped = 0;    // out: faces were flipped to face outward
+};
+int build_mesh(MeshBuild& b, void* stream);
+// Caching device allocator (engine.cpp), shared with the kernel-side helpers.
+void* dev_alloc(size_t bytes);
+void dev_free(void* p, size_t bytes);
 int launch_front_count(const FrontBuild& b, int* c_off, int* nnz, void* stream);
 int launch_front_fill(const FrontBuild& b, const int* c_off, int* c_col, void* stream);
 int launch_spmv(int nv, const int* off, const int* col, const double* val, const double* mass,

@@ -77,6 +77,25 @@ class Mesh {
   // outward, then builds edge, face-edge, vertex-face and vertex-vertex indices.
   Mesh(std::vector<V3> vertices, std::vector<std::array<Index, 3>> faces);
 
+  // Trusted assembly from indices built elsewhere (the device builder,
+  // csrc/meshbuild.cu), with the same numbering; no validation.
+  static Mesh from_index(std::vector<V3> pos, std::vector<std::array<Index, 3>> faces,
+                         std::vector<std::array<Index, 2>> edge_v, std::vector<std::array<Index, 2>> edge_f,
+                         std::vector<std::array<Index, 3>> face_e, std::vector<std::uint32_t> v2f_off,
+                         std::vector<Index> v2f, std::vector<std::uint32_t> v2v_off, std::vector<Index> v2v) {
+    Mesh m;
+    m.pos_ = std::move(pos);
+    m.faces_ = std::move(faces);
+    m.edge_v_ = std::move(edge_v);
+    m.edge_f_ = std::move(edge_f);
+    m.face_e_ = std::move(face_e);
+    m.v2f_off_ = std::move(v2f_off);
+    m.v2f_ = std::move(v2f);
+    m.v2v_off_ = std::move(v2v_off);
+    m.v2v_ = std::move(v2v);
+    return m;
+  }
+
   Index nv() const { return static_cast<Index>(pos_.size()); }
   Index nf() const { return static_cast<Index>(faces_.size()); }
   Index ne() const { return static_cast<Index>(edge_v_.size()); }

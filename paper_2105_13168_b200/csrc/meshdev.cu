@@ -89,6 +89,105 @@ __global__ void k_front_fill(FrontBuild B, const int* off, int* col) {
 
 }  // namespace
 
+// seed_region (diffusion.hpp:134) on the device.  The reference pops a
+// Dijkstra queue until the distance exceeds the radius, so its result is
+// {u : d(u) <= radius} with d the least fixed point of
+//   d(u) = min over neighbours v of fl(d(v) + |p(v) - p(u)|),  d(seed) = 0
+// (floating-point addition of a non-negative length is monotone, so that is
+// what Dijkstra computes).  One CTA reaches the same fixed point by
+// frontier-based Bellman-Ford relaxation with atomicMin on the distance bits
+// (non-negative doubles order like their bit patterns); relaxations beyond the
+// radius are skipped since they cannot lead back inside it.  Overflowing a
+// capacity reports -1 and the caller uses the host.
+constexpr int kSeedCap = 1 << 15;  // touched vertices / frontier entries
+constexpr unsigned long long kFar = 0x7F7F7F7F7F7F7F7Full;  // 3.4e306, the memset pattern
+struct SeedScratch {
+  int front[2][kSeedCap];
+  int touched[kSeedCap];
+  int nfront[2], ntouched, overflow;
+};
+
+__global__ void __launch_bounds__(1024) k_seed_region(const int* off, const int* col, const double* px,
+                                                      const double* py, const double* pz, unsigned seed, double radius,
+                                                      unsigned long long* dist, SeedScratch* S, unsigned* out,
+                                                      int cap, int* out_n) {
+  if (threadIdx.x == 0) {
+    dist[seed] = static_cast<unsigned long long>(__double_as_longlong(0.0));
+    S->front[0][0] = static_cast<int>(seed);
+    S->nfront[0] = 1;
+    S->nfront[1] = 0;
+    S->touched[0] = static_cast<int>(seed);
+    S->ntouched = 1;
+    S->overflow = 0;
+  }
+  __syncthreads();
+  int cur = 0;
+  while (true) {
+    const int n = S->nfront[cur];
+    if (n == 0 || S->overflow) break;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int v = S->front[cur][i];
+      const double dv = __longlong_as_double(static_cast<long long>(__ldcg(dist + v)));
+      const double vx = px[v], vy = py[v], vz = pz[v];
+      for (int o = off[v]; o < off[v + 1]; ++o) {
+        const int u = col[o];
+        const double dx = vx - px[u], dy = vy - py[u], dz = vz - pz[u];
+        const double nd = dv + sqrt(dx * dx + dy * dy + dz * dz);
+        if (!(nd <= radius)) continue;
+        const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(nd));
+        const unsigned long long old = atomicMin(dist + u, bits);
+        if (bits < old) {
+          if (old == kFar) {
+            const int t = atomicAdd(&S->ntouched, 1);
+            if (t < kSeedCap) S->touched[t] = u;
+            else S->overflow = 1;
+          }
+          const int q = atomicAdd(&S->nfront[cur ^ 1], 1);
+          if (q < kSeedCap) S->front[cur ^ 1][q] = u;
+          else S->overflow = 1;
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) S->nfront[cur] = 0;
+    cur ^= 1;
+    __syncthreads();
+  }
+  // Every touched vertex ended at d <= radius (only such values are stored).
+  const int nt = min(S->ntouched, kSeedCap);
+  for (int i = threadIdx.x; i < nt && i < cap; i += blockDim.x) out[i] = static_cast<unsigned>(S->touched[i]);
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) dist[S->touched[i]] = kFar;  // reset for the next call
+  if (threadIdx.x == 0) *out_n = (S->overflow || nt > cap) ? -1 : nt;
+}
+
+int launch_seed_region(const DevMesh& m, unsigned seed, double radius, unsigned* out, int cap, int* n, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!(radius >= 0.0)) {  // NaN radius: the reference's loop breaks at once... let the host decide
+    *n = -1;
+    return 0;
+  }
+  static_assert(kFar == 0x7F7F7F7F7F7F7F7Full, "distance reset value is a memset byte pattern");
+  const size_t dbytes = sizeof(unsigned long long) * static_cast<size_t>(m.nv);
+  unsigned long long* dist = static_cast<unsigned long long*>(dev_alloc(dbytes));
+  SeedScratch* S = static_cast<SeedScratch*>(dev_alloc(sizeof(SeedScratch)));
+  unsigned* dout = static_cast<unsigned*>(dev_alloc(sizeof(unsigned) * (cap > 0 ? cap : 1)));
+  int* dn = static_cast<int*>(dev_alloc(sizeof(int)));
+  cudaMemsetAsync(dist, 0x7F, dbytes, s);
+  k_seed_region<<<1, 1024, 0, s>>>(m.n_off, m.n_col, m.px, m.py, m.pz, seed, radius, dist, S, dout, cap, dn);
+  note_launch();
+  cudaMemcpyAsync(n, dn, sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess && *n > 0) {
+    cudaMemcpyAsync(out, dout, sizeof(unsigned) * (*n), cudaMemcpyDeviceToHost, s);
+    e = cudaStreamSynchronize(s);
+  }
+  dev_free(dn, sizeof(int));
+  dev_free(dout, sizeof(unsigned) * (cap > 0 ? cap : 1));
+  dev_free(S, sizeof(SeedScratch));
+  dev_free(dist, dbytes);
+  return static_cast<int>(e);
+}
+
 int launch_positions(const double* xyz, int nv, double scale, double* px, double* py, double* pz, long long* fx,
                      long long* fy, long long* fz, void* stream) {
   k_positions<<<(nv + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(xyz, nv, scale, px, py, pz, fx, fy, fz);
