@@ -157,6 +157,16 @@ def cpu_reference_sample(spec, steps):
     return json.loads(out.stdout.strip().splitlines()[-1])
 
 
+def measured_traffic(args):
+    """DRAM bytes per k_engine launch from the committed ncu --set full capture
+    (profiles/traffic_k_engine.json), when it was taken on this workload."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic_k_engine.json")
+    if args.mesh != "genus:8:45" or args.pass_steps != 3000 or not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        return json.load(fh)["dram_bytes_per_launch"]  # bytes per launch, like alg_bytes_per_launch
+
+
 def peaks():
     try:
         with open(PEAKS) as f:
@@ -293,8 +303,8 @@ def main():
         e2e = {"value": world * V * args.pass_steps * args.steps / e2e_total / 1e6, "unit": "Mvert-steps/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_mesh": 1e3 * e2e_total / args.steps,
-               "includes": "host mesh validation/indexing, H2D, device Laplacian assembly, initial pass, "
-                           "D2H of events/estimates/covered sets/trails"}
+               "includes": "H2D of the vertex/face arrays, device mesh validation/orientation/indexing, device "
+                           "Laplacian assembly, initial pass, D2H of events/estimates/covered sets/trails"}
 
     line = {
         "metric": METRIC, "value": value, "unit": "Mvert-steps/s", "n_gpus": world, "steps": args.steps,
@@ -308,7 +318,9 @@ def main():
         "ms_per_mesh": 1e3 * total / args.steps,
         "gpu_launches": int(gpu_launches),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "peak_kind": peak_kind, "kernel": "k_engine<0> (persistent step kernel)",
+                     "traffic": measured_traffic(args), "traffic_unit": "DRAM bytes per launch (ncu)",
+                     "peak_kind": peak_kind,
+                     "kernel": "k_engine<0> (persistent step kernel)",
                      "kernel_seconds": k_time, "kernel_launches": k_launches,
                      "alg_bytes_per_launch": alg_bytes / max(1, k_launches),
                      "avg_frontier_vertices_per_step": sum_region / (args.pass_steps * args.steps),
