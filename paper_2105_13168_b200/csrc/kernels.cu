@@ -494,6 +494,7 @@ __device__ __forceinline__ double (*fold_buf())[kFoldCols] { return reinterpret_
 __device__ __forceinline__ bool gather_fold(const DevMesh& M, const DevField& F, const DevWork& W, int v, int cv,
                                             const int (&Ol)[kF], int k0, int k1, int lane, unsigned gm, int (&Cl)[kF],
                                             double (&Ca)[kF], int& nc, double& lapb, double& lapt, bool& bnear) {
+  INSTR_C0(tG);
   const int k = k0 + lane;
   const bool valid = k < k1;
   double s = 0.0, bu = 0.0, au = 0.0;
@@ -511,11 +512,17 @@ __device__ __forceinline__ bool gather_fold(const DevMesh& M, const DevField& F,
     s = __ldg(M.s_val + k);
     const size_t b = static_cast<size_t>(u) * kSlots;
     cu = F.cnt[u];
-#pragma unroll
-    for (int q = 0; q < kReg; ++q) {
-      L[q] = F.lay[b + q];
-      X[q] = F.val[b + q];
-    }
+    const uint2 lw = *reinterpret_cast<const uint2*>(F.lay + b);
+    const double2 x01 = *reinterpret_cast<const double2*>(F.val + b);
+    const double2 x23 = *reinterpret_cast<const double2*>(F.val + b + 2);
+    L[0] = static_cast<unsigned short>(lw.x & 0xFFFF);
+    L[1] = static_cast<unsigned short>(lw.x >> 16);
+    L[2] = static_cast<unsigned short>(lw.y & 0xFFFF);
+    L[3] = static_cast<unsigned short>(lw.y >> 16);
+    X[0] = x01.x;
+    X[1] = x01.y;
+    X[2] = x23.x;
+    X[3] = x23.y;
 #pragma unroll
     for (int q = 0; q < kReg; ++q)
       if (q < cu) {
@@ -528,6 +535,7 @@ __device__ __forceinline__ bool gather_fold(const DevMesh& M, const DevField& F,
       }
   }
   if (__any_sync(gm, cu > kReg)) return false;
+  INSTR_CP(12, tG);
   unsigned omask = 0;
 #pragma unroll
   for (int q = 0; q < kF; ++q)
@@ -551,6 +559,7 @@ __device__ __forceinline__ bool gather_fold(const DevMesh& M, const DevField& F,
     last = m;
     ++nc;
   }
+  INSTR_CP(13, tG);
   // Contributions, staged per lane.
   double(*s_fold)[kFoldCols] = fold_buf();
   const int base = threadIdx.x & ~(kG - 1);
@@ -585,6 +594,7 @@ __device__ __forceinline__ bool gather_fold(const DevMesh& M, const DevField& F,
       if ((use >> jj) & 1) acc = acc + s_fold[base + jj][lane];
   }
   __syncwarp(gm);  // s_fold is reused by the group's next vertex
+  INSTR_CP(14, tG);
 #pragma unroll
   for (int c = 0; c < kF; ++c) Ca[c] = __shfl_sync(gm, acc, c, kG);
   lapb = __shfl_sync(gm, acc, kF, kG);
@@ -602,10 +612,19 @@ __device__ bool update_vertex_fast(const DevMesh& M, const DevField& F, const De
   const size_t vb = static_cast<size_t>(v) * kSlots;
   int Ol[kF];
   double Ox[kF];
-#pragma unroll
-  for (int q = 0; q < kF; ++q) {
-    Ol[q] = static_cast<int>(F.lay[vb + q]);
-    Ox[q] = F.val[vb + q];
+  static_assert(kF == 4, "the column head is loaded as one 8 B and two 16 B vectors");
+  {
+    const uint2 lw = *reinterpret_cast<const uint2*>(F.lay + vb);
+    const double2 x01 = *reinterpret_cast<const double2*>(F.val + vb);
+    const double2 x23 = *reinterpret_cast<const double2*>(F.val + vb + 2);
+    Ol[0] = static_cast<int>(lw.x & 0xFFFF);
+    Ol[1] = static_cast<int>(lw.x >> 16);
+    Ol[2] = static_cast<int>(lw.y & 0xFFFF);
+    Ol[3] = static_cast<int>(lw.y >> 16);
+    Ox[0] = x01.x;
+    Ox[1] = x01.y;
+    Ox[2] = x23.x;
+    Ox[3] = x23.y;
   }
   const int k0 = __ldg(M.s_off + v), k1 = __ldg(M.s_off + v + 1);
   const double mass = __ldg(M.mass + v);
@@ -725,57 +744,91 @@ __device__ bool update_vertex_fast(const DevMesh& M, const DevField& F, const De
   if (over) return false;
 
   const double lap_b = lapb / mass;
-  bool touched = false;
-  bool Cupd[kF];
-  double Cn[kF];
+  // Candidate updates run one per lane (lanes 0..nc-1) and the base update on
+  // lane kF, so the divisions and square roots of different layers proceed in
+  // parallel instead of as one predicated chain.  Every expression is the
+  // sequential code's, term for term.
+  bool my_upd = false, my_blow = false;
+  double my_next = 0.0;
+  if (lane < nc) {
+    int cl = 0;
+    double ca = 0.0;
 #pragma unroll
-  for (int c = 0; c < kF; ++c) {
-    Cupd[c] = false;
-    Cn[c] = 0.0;
-    if (c >= nc) continue;
+    for (int c = 0; c < kF; ++c)
+      if (c == lane) {
+        cl = Cl[c];
+        ca = Ca[c];
+      }
     double phi = 0.0;
 #pragma unroll
     for (int q = 0; q < kF; ++q)
-      if (Ol[q] == Cl[c]) phi = Ox[q];
-    if (phi == 0.0 && phib <= P.prune) continue;
-    const double lap_i = Ca[c] / mass;
-    const double inner = P.w * (phib - phi) + P.half_a2 * (lap_b - lap_i) - P.e * sqrt(max0(phi * phib));
-    const double rate = -P.mu_n * inner;
-    if (!isfinite(rate)) {
-      raise_error(W.ctl, kDevBlowup, v, spec);
-      return true;
-    }
-    const double next = clamp01(phi + P.dt * rate);
-    if (next != phi) {
-      touched = true;
-      Cupd[c] = true;
-      Cn[c] = next;
+      if (Ol[q] == cl) phi = Ox[q];
+    if (!(phi == 0.0 && phib <= P.prune)) {
+      const double lap_i = ca / mass;
+      const double inner = P.w * (phib - phi) + P.half_a2 * (lap_b - lap_i) - P.e * sqrt(max0(phi * phib));
+      const double rate = -P.mu_n * inner;
+      if (!isfinite(rate)) {
+        my_blow = true;
+      } else {
+        const double next = clamp01(phi + P.dt * rate);
+        if (next != phi) {
+          my_upd = true;
+          my_next = next;
+        }
+      }
     }
   }
-  bool bupd = false;
-  double bnext = 0.0;
-  if (bnear) {
-    double total = 0.0, contact = 0.0;
+  // Contact terms of the base update, one own slot per lane kF..kF+3.
+  unsigned amask_own = 0;
+#pragma unroll
+  for (int q = 0; q < kF; ++q)
+    if (q < cv && Ol[q] != 0 && W.active[Ol[q]]) amask_own |= 1u << q;
+  double cterm = 0.0;
+  if (bnear && lane >= kF) {
 #pragma unroll
     for (int q = 0; q < kF; ++q)
-      if (q < cv && Ol[q] != 0 && W.active[Ol[q]]) total = total + Ox[q];
+      if (lane - kF == q && ((amask_own >> q) & 1)) cterm = sqrt(max0(phib * Ox[q]));
+  }
+  double contact = 0.0;
+#pragma unroll
+  for (int q = 0; q < kF; ++q) {
+    const double t = __shfl_sync(gm, cterm, kF + q, kG);
+    if ((amask_own >> q) & 1) contact = contact + t;
+  }
+  if (bnear && lane == kF) {
+    double total = 0.0;
 #pragma unroll
     for (int q = 0; q < kF; ++q)
-      if (q < cv && Ol[q] != 0 && W.active[Ol[q]]) contact = contact + sqrt(max0(phib * Ox[q]));
+      if ((amask_own >> q) & 1) total = total + Ox[q];
     const double lap_total = lapt / mass;
     const double rate = -P.mu_n * (P.w * total + P.half_a2 * lap_total + P.e * contact) +
                         P.m_mu_n * (P.w * phib + P.half_a2 * lap_b);
     if (!isfinite(rate)) {
-      raise_error(W.ctl, kDevBlowup, v, spec);
-      return true;
-    }
-    const double next = clamp01(phib + P.dt * rate);
-    if (next != phib) {
-      touched = true;
-      bupd = true;
-      bnext = next;
+      my_blow = true;
+    } else {
+      const double next = clamp01(phib + P.dt * rate);
+      if (next != phib) {
+        my_upd = true;
+        my_next = next;
+      }
     }
   }
+  if (__any_sync(gm, my_blow)) {  // every path raises the same error for v
+    if (lane == 0) raise_error(W.ctl, kDevBlowup, v, spec);
+    return true;
+  }
+  bool Cupd[kF];
+  double Cn[kF];
+#pragma unroll
+  for (int c = 0; c < kF; ++c) {
+    Cupd[c] = __shfl_sync(gm, my_upd, c, kG);
+    Cn[c] = __shfl_sync(gm, my_next, c, kG);
+  }
+  const bool bupd = __shfl_sync(gm, my_upd, kF, kG);
+  const double bnext = __shfl_sync(gm, my_next, kF, kG);
+  bool touched = bupd;
+#pragma unroll
+  for (int c = 0; c < kF; ++c) touched |= Cupd[c];
   INSTR_CP(2, tA);
   // Apply the updates with set_value semantics into a sorted register column.
   bool changed = false;
@@ -855,26 +908,45 @@ __device__ bool update_vertex_fast(const DevMesh& M, const DevField& F, const De
       return true;
     }
     if (!(fabs(ssum - 1.0) < 1e-15)) {
-      int m = 0;
+      // One entry per lane (n <= kN == kG): divide, clamp, prune, then drop
+      // zeros by ballot compaction -- the sequential loop's result.
+      static_assert(kN == kG, "normalisation maps one column entry to each lane");
+      int el = kNoLayer;
+      double ex = 0.0;
 #pragma unroll
-      for (int j = 0; j < kN; ++j) {
-        if (j >= n) continue;
-        double q = Ex[j] / ssum;
+      for (int j = 0; j < kN; ++j)
+        if (j == lane) {
+          el = El[j];
+          ex = Ex[j];
+        }
+      double q = 0.0;
+      bool ch = false;
+      if (lane < n) {
+        q = ex / ssum;
         if (q > 1.0) q = 1.0;
         if (q < P.prune) q = 0.0;
-        if (q != Ex[j]) changed = true;
-        if (q != 0.0) {
-          const int l = El[j];
-#pragma unroll
-          for (int t = 0; t < kN; ++t)
-            if (t == m) {
-              El[t] = l;
-              Ex[t] = q;
-            }
-          ++m;
-        }
+        ch = q != ex;
       }
-      n = m;
+      const int gshift = threadIdx.x & 24;
+      const unsigned keep = (__ballot_sync(gm, lane < n && q != 0.0) >> gshift) & 0xFFu;
+      changed = changed || ((__ballot_sync(gm, ch) >> gshift) & 0xFFu) != 0;
+      // Lane t takes the t-th surviving entry.
+      const int src = __fns(keep, 0, lane + 1);
+      const int srcl = src < 0 ? 0 : src & (kG - 1);
+      const int nl = __shfl_sync(gm, el, srcl, kG);
+      const double nx = __shfl_sync(gm, q, srcl, kG);
+#pragma unroll
+      for (int j = 0; j < kN; ++j) {
+        El[j] = __shfl_sync(gm, nl, j, kG);
+        Ex[j] = __shfl_sync(gm, nx, j, kG);
+      }
+      n = __popc(keep);
+#pragma unroll
+      for (int j = 0; j < kN; ++j)
+        if (j >= n) {
+          El[j] = kNoLayer;
+          Ex[j] = 0.0;
+        }
     }
   }
   INSTR_CP(3, tA);
@@ -1633,9 +1705,14 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       const int spar = cur;
       block_stats_init(S);
       phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, QB, nband);
-      block_stats_flush(S, W.stat + static_cast<size_t>(spar) * kMaxActive, P.n_active, ctl);
-      bq_flush(Q, &ctl->ilcount[lpar ^ 1], W.ilist[lpar ^ 1]);
-      bq_flush(QB, &ctl->nbandpairs, W.bandpairs, W.bandpair_cap, &ctl->bandpair_overflow);
+      // The CTA-level flushes of E (each a __syncthreads) come after A, so
+      // the warps running A do not wait for the warps running E.
+      auto flush_e = [&] {
+        block_stats_flush(S, W.stat + static_cast<size_t>(spar) * kMaxActive, P.n_active, ctl);
+        bq_flush(Q, &ctl->ilcount[lpar ^ 1], W.ilist[lpar ^ 1]);
+        bq_flush(QB, &ctl->nbandpairs, W.bandpairs, W.bandpair_cap, &ctl->bandpair_overflow);
+      };
+      if (!more || P.split_a) flush_e();
       if (more) {
         if (P.split_a) {
           grid_sync(ctl);
@@ -1654,6 +1731,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
             INSTR_REC(3, t0, (threadIdx.x & (kG - 1)) == 0);
           }
         }
+        if (!P.split_a) flush_e();
       }
       block_done(W, step - (P.step_end - 64), 2);
       grid_sync_snap(ctl, SC);
