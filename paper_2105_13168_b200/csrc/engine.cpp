@@ -605,6 +605,8 @@ void DeviceField::setup() {
   in_list.alloc(nv);
   bandpairs.alloc(2 * nv + 4096);
   parent.alloc(nv * kSlots);
+  added.alloc(nv / 8 + 4096);
+  add_stamp.alloc(nv);
   active.alloc(kMaxLayers + 1);
   aidx.alloc(kMaxLayers + 1);
   alist.alloc(kMaxActive);
@@ -648,6 +650,9 @@ void DeviceField::setup() {
   ad2.alloc(ncap);
   acnt.alloc(16);
   work_.parent = parent.p;
+  work_.added = added.p;
+  work_.added_cap = static_cast<int>(added.n);
+  work_.add_stamp = add_stamp.p;
   work_.active = active.p;
   work_.aidx = aidx.p;
   work_.alist = alist.p;
@@ -679,6 +684,8 @@ void DeviceField::init(const std::vector<Index>& seeds) {
   pair_keys.zero(s_);
   stat.zero(s_);
   lastpos.zero(s_);
+  // Step stamps of gained band items: -1 never matches a step.
+  cuda_check(cudaMemsetAsync(add_stamp.p, 0xFF, sizeof(int) * add_stamp.n, s_), "memset");
   ck(launch_init_field(view_, work_, static_cast<int>(nv), ai0.p, static_cast<int>(sv.size()), s_), "init field");
   Ctl c{};
   c.base_one = static_cast<int>(nv - sv.size());
@@ -1210,6 +1217,7 @@ class PassEngine {
     p.stop_every_check = cfg_.on_check ? 1 : 0;
     if (const char* env = std::getenv("DTB_SPLIT_A"); env && env[0] == '1') p.split_a = 1;
     if (const char* env = std::getenv("DTB_NO_UNITE"); env && env[0] == '1') p.split_a_no_unite = 1;
+    if (const char* env = std::getenv("DTB_D_FULL"); env && env[0] == '1') p.d_full = 1;
     // E and D spread round-robin over the CTAs, A filled from each CTA's last
     // warp so it overlaps E (measured: E+A 14.4 -> 13.4 us per step).
     p.map_mode = 1 | 2 | 8;

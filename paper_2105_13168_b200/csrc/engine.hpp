@@ -267,6 +267,8 @@ class DeviceField {
   DevBuf<double> ad0, ad1, ad2;
   DevBuf<uint4> binfo;
   DevBuf<unsigned long long> parent, pair_keys, hashes;
+  DevBuf<int2> added;   // band items gained this step (split certificate)
+  DevBuf<int> add_stamp;  // per vertex: last step it gained a band item
   DevBuf<unsigned> pairs;
   DevBuf<LayerStat> stat;
   DevBuf<TrailRec> trail;

@@ -139,14 +139,19 @@ struct CtlSnap {
   int error;
   int error_vertex;
   int spec_error;
+  int dchange;
+  int nadded;
+  int anchor_fail;
+  int pad_;
 };
-static_assert(sizeof(CtlSnap) == 32, "CtlSnap mirrors the first 32 bytes of Ctl");
+static_assert(sizeof(CtlSnap) == 48, "CtlSnap mirrors the first 48 bytes of Ctl");
 __device__ __forceinline__ void ctl_snap(const Ctl* ctl, CtlSnap& sc) {
   if (threadIdx.x == 0) {
     const int4* src = reinterpret_cast<const int4*>(ctl);
     int4* dst = reinterpret_cast<int4*>(&sc);
     dst[0] = __ldcg(src);
     dst[1] = __ldcg(src + 1);
+    dst[2] = __ldcg(src + 2);
   }
   __syncthreads();
 }
@@ -1042,6 +1047,7 @@ __device__ void commit_vertex(const DevMesh& M, const DevField& F, const DevWork
   const double sx = W.sval[o + lane];
   const int k0 = __ldg(M.s_off + v), k1 = __ldg(M.s_off + v + 1);
   const unsigned char listed = W.in_list[v];
+  const uint4 old_bi = F.binfo[v];  // band layers before this commit (change tracking)
   if (!(flag & 1)) return;
   INSTR_CP(4, tB);
   const int t0 = lane;  // first row entry of this lane: t = 0 is v itself
@@ -1084,6 +1090,30 @@ __device__ void commit_vertex(const DevMesh& M, const DevField& F, const DevWork
     }
   }
   if (lane == 0) {
+    // Band-item changes for the split certificate of phase D (see
+    // skip_union_ok): a lost band layer (or an overflowing band index) marks
+    // the step; gained layers are listed.
+    if (binfo_overflow(old_bi) || binfo_overflow(bi)) {
+      W.ctl->dchange = 1;
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const unsigned lo = binfo_layer(old_bi, t), ln = binfo_layer(bi, t);
+        bool lo_kept = false, ln_old = false;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          lo_kept |= lo != 0 && binfo_layer(bi, q) == lo;
+          ln_old |= ln != 0 && binfo_layer(old_bi, q) == ln;
+        }
+        if (lo != 0 && !lo_kept) W.ctl->dchange = 1;
+        if (ln != 0 && !ln_old) {
+          W.add_stamp[v] = stamp;
+          const int pos = atomicAdd(&W.ctl->nadded, 1);
+          if (pos < W.added_cap) W.added[pos] = make_int2(v, static_cast<int>(ln));
+          else W.ctl->dchange = 1;
+        }
+      }
+    }
     F.cnt[v] = static_cast<unsigned char>(nn);
     F.interest[v] = inter ? 1 : 0;
     F.binfo[v] = bi;
@@ -1332,6 +1362,29 @@ __device__ __forceinline__ unsigned long long seg_max_u64(unsigned peers, unsign
   return (static_cast<unsigned long long>(hi) << 32) | lo;
 }
 
+// Split certificate (phase D is skipped when it holds).  With every check at
+// consecutive steps, the previous check left each layer's band connected (or
+// empty).  If this step removed no band item and every added item has a mesh
+// neighbour that was a band item of its layer before the step, each layer's
+// band is still connected or empty, so no split can occur and the union-find
+// is not needed.  This marks the added items that are not so anchored.
+__device__ void anchor_test(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P, int nadded,
+                            int stamp) {
+  const int n = min(nadded, W.added_cap);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int2 a = W.added[i];
+    const int v = a.x;
+    const unsigned l = static_cast<unsigned>(a.y);
+    if (!W.active[l]) continue;
+    bool anchored = false;
+    for (int o = M.n_off[v]; o < M.n_off[v + 1] && !anchored; ++o) {
+      const int u = M.n_col[o];
+      anchored = W.add_stamp[u] != stamp && band_slot_of(F, W, P, u, l) >= 0;
+    }
+    if (!anchored) W.ctl->anchor_fail = 1;
+  }
+}
+
 // Phase E: per-layer statistics (roots = front components, band counts and
 // fixed-point position sums, unsaturated counts), collision pairs, base
 // extinction data, band items for the trail snap, and compaction of the band
@@ -1339,7 +1392,7 @@ __device__ __forceinline__ unsigned long long seg_max_u64(unsigned peers, unsign
 // vertex's slots in lock step so contributions can be combined per warp.
 __device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P, int lpar,
                             int spar, unsigned long long ep, bool compact, BlockStats& S, BlockQueue& Q,
-                            PairQueue& QB, int n) {
+                            PairQueue& QB, int n, bool count_roots = true) {
   LayerStat* g = W.stat + static_cast<size_t>(spar) * kMaxActive;
   const int* list = W.ilist[lpar];
   const int lane = threadIdx.x & 31;
@@ -1416,7 +1469,7 @@ __device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& 
             // Unions are complete, so an item is a root iff its parent entry
             // is stale (never linked this epoch) or points to itself.
             const unsigned item = static_cast<unsigned>(v) * kSlots + k;
-            root = (pw >> 32) != ep || static_cast<unsigned>(pw) == item;
+            root = count_roots && ((pw >> 32) != ep || static_cast<unsigned>(pw) == item);
             if (P.record_trails)
               bq_push(QB, &W.ctl->nbandpairs, W.bandpairs, make_int2(v, a), W.bandpair_cap, &W.ctl->bandpair_overflow);
           }
@@ -1635,6 +1688,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
   long long step = P.step_begin;
   int stop = 0;
   bool pend = false;
+  bool first_check = true;  // the first check of a launch follows host edits: always the union-find
   long long pend_step = 0;
   {  // prologue: A(step_begin)
     const int cur = static_cast<int>(step & 1);
@@ -1643,6 +1697,9 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
     if (gtid == 0) {
       ctl->rcount[cur ^ 1] = 0;
       ctl->sum_region += static_cast<unsigned long long>(nR);
+      ctl->dchange = 0;
+      ctl->nadded = 0;
+      ctl->anchor_fail = 0;
     }
     for (int i = group_rank(P.map_mode & 2 ? 2 : 0); i < nR; i += gsz / kG)
       if (!update_vertex_fast(M, F, W, P, i, W.region[cur][i], false, threadIdx.x & (kG - 1), group_mask()))
@@ -1695,29 +1752,11 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       const int nband = SC.ilcount[lpar];
       const int nR1 = SC.rcount[nxt];  // final since B(s)
       if (gtid == 0) ctl->sum_interest += static_cast<unsigned long long>(nband);
-      phase_union(M, F, W, P, lpar, ep, group_rank(P.map_mode & 8 ? 1 : 0), gsz / kG, nband);
-      if (P.do_hash) phase_hash(F, W, M.nv);
-      block_done(W, step - (P.step_end - 64), 1);
-      grid_sync(ctl);
-      if (prof) W.prof[pslot + 2] = gtimer();
-      block_start(W, step - (P.step_end - 64), 2);
-      // ---- 3: E(s) + speculative A(s+1)
-      const int spar = cur;
-      block_stats_init(S);
-      phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, QB, nband);
-      // The CTA-level flushes of E (each a __syncthreads) come after A, so
-      // the warps running A do not wait for the warps running E.
-      auto flush_e = [&] {
-        block_stats_flush(S, W.stat + static_cast<size_t>(spar) * kMaxActive, P.n_active, ctl);
-        bq_flush(Q, &ctl->ilcount[lpar ^ 1], W.ilist[lpar ^ 1]);
-        bq_flush(QB, &ctl->nbandpairs, W.bandpairs, W.bandpair_cap, &ctl->bandpair_overflow);
-      };
-      if (!more || P.split_a) flush_e();
-      if (more) {
-        if (P.split_a) {
-          grid_sync(ctl);
-          if (prof) W.prof[pslot + 3] = gtimer();
-        }
+      // The split certificate (anchor_test) replaces the union-find when it
+      // holds; its slot then runs the speculative A(s+1).
+      bool skip = !P.d_full && P.check_interval == 1 && !first_check && !SC.dchange;
+      bool a_done = false;
+      auto run_a = [&] {
         if (gtid == 0) {
           ctl->rcount[cur] = 0;
           ctl->sum_region += static_cast<unsigned long long>(nR1);
@@ -1731,7 +1770,51 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
             INSTR_REC(3, t0, (threadIdx.x & (kG - 1)) == 0);
           }
         }
+      };
+      if (skip) {
+        anchor_test(M, F, W, P, SC.nadded, static_cast<int>(step));
+        if (more) {
+          run_a();
+          a_done = true;
+        }
+      } else {
+        phase_union(M, F, W, P, lpar, ep, group_rank(P.map_mode & 8 ? 1 : 0), gsz / kG, nband);
+      }
+      if (P.do_hash) phase_hash(F, W, M.nv);
+      block_done(W, step - (P.step_end - 64), 1);
+      grid_sync_snap(ctl, SC);
+      if (skip && SC.anchor_fail) {  // an unanchored new band item: run the union-find after all
+        skip = false;
+        phase_union(M, F, W, P, lpar, ep, group_rank(P.map_mode & 8 ? 1 : 0), gsz / kG, nband);
+        grid_sync(ctl);
+      }
+      if (prof) W.prof[pslot + 2] = gtimer();
+      block_start(W, step - (P.step_end - 64), 2);
+      // ---- 3: E(s) + speculative A(s+1) (unless it ran in the D slot)
+      const int spar = cur;
+      block_stats_init(S);
+      phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, QB, nband, !skip);
+      // The CTA-level flushes of E (each a __syncthreads) come after A, so
+      // the warps running A do not wait for the warps running E.
+      auto flush_e = [&] {
+        block_stats_flush(S, W.stat + static_cast<size_t>(spar) * kMaxActive, P.n_active, ctl);
+        bq_flush(Q, &ctl->ilcount[lpar ^ 1], W.ilist[lpar ^ 1]);
+        bq_flush(QB, &ctl->nbandpairs, W.bandpairs, W.bandpair_cap, &ctl->bandpair_overflow);
+      };
+      if (!more || P.split_a || a_done) flush_e();
+      if (more && !a_done) {
+        if (P.split_a) {
+          grid_sync(ctl);
+          if (prof) W.prof[pslot + 3] = gtimer();
+        }
+        run_a();
         if (!P.split_a) flush_e();
+      }
+      // Change tracking of B(s+1) starts from zero (read after the barrier).
+      if (gtid == 0) {
+        ctl->dchange = 0;
+        ctl->nadded = 0;
+        ctl->anchor_fail = 0;
       }
       block_done(W, step - (P.step_end - 64), 2);
       grid_sync_snap(ctl, SC);
@@ -1758,12 +1841,18 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       }
       pend = true;
       pend_step = step;
+      first_check = false;
     } else {
       // ---- 3': trail flush of the previous check (its stats parity is
       // reused two steps later) + A(s+1)
       if (pend)
         for (int a = gtid; a < P.n_active; a += gsz) flush_stat(M, W, P, a, static_cast<int>(pend_step & 1), pend_step, true);
       pend = false;
+      if (gtid == 0) {
+        ctl->dchange = 0;
+        ctl->nadded = 0;
+        ctl->anchor_fail = 0;
+      }
       if (more) {
         const int nR1 = SC.rcount[nxt];  // snapshot after B(s)
         if (gtid == 0) {

@@ -115,6 +115,10 @@ struct Ctl {
   int error;                 // DevError of a committed step
   int error_vertex;
   int spec_error;            // error raised by a speculative update (next step)
+  int dchange;               // this step removed a band item (or overflowed a band index / the added list)
+  int nadded;                // band items added this step (W.added)
+  int anchor_fail;           // an added band item has no related band item of the previous step
+  int pad_;
   int spec_error_vertex;
   int stop_bits;
   long long stop_step;       // last step executed by the kernel
@@ -168,6 +172,9 @@ struct DevWork {
   int2 *bandpairs = nullptr;            // (vertex, dense active index) band items of the last check
   int bandpair_cap = 0;
   unsigned long long *parent = nullptr; // nv * kSlots versioned UF parents
+  int2 *added = nullptr;                // band items (vertex, layer) added this step
+  int added_cap = 0;
+  int *add_stamp = nullptr;             // per vertex: last step at which it gained a band item
   unsigned char *active = nullptr;      // kMaxLayers + 1
   int *aidx = nullptr;                  // layer -> dense active index or -1
   int *alist = nullptr;                 // dense active index -> layer
@@ -197,6 +204,7 @@ struct StepParams {
   int do_check;  // 0: advance only (one-shot step())
   int split_a;   // diagnostics: run the next step's update in its own phase
   int split_a_no_unite;  // diagnostics only: skip unions (wrong results; timing)
+  int d_full;            // diagnostics: never skip the front union-find (DTB_D_FULL=1)
   int map_mode;          // work-to-CTA maps, bits: 1 spread E, 2 A from the last warp, 4 spread B, 8 spread D
 };
 
