@@ -605,7 +605,7 @@ void DeviceField::setup() {
   in_list.alloc(nv);
   bandpairs.alloc(2 * nv + 4096);
   parent.alloc(nv * kSlots);
-  added.alloc(nv / 8 + 4096);
+  added.alloc(2 * (nv / 8 + 4096));  // two step-parity halves
   add_stamp.alloc(nv);
   active.alloc(kMaxLayers + 1);
   aidx.alloc(kMaxLayers + 1);
@@ -651,7 +651,7 @@ void DeviceField::setup() {
   acnt.alloc(16);
   work_.parent = parent.p;
   work_.added = added.p;
-  work_.added_cap = static_cast<int>(added.n);
+  work_.added_cap = static_cast<int>(added.n / 2);
   work_.add_stamp = add_stamp.p;
   work_.active = active.p;
   work_.aidx = aidx.p;

@@ -139,12 +139,12 @@ struct CtlSnap {
   int error;
   int error_vertex;
   int spec_error;
-  int dchange;
-  int nadded;
-  int anchor_fail;
-  int pad_;
+  int dchange[2];
+  int nadded[2];
+  int anchor_fail[2];
+  int pad_[2];
 };
-static_assert(sizeof(CtlSnap) == 48, "CtlSnap mirrors the first 48 bytes of Ctl");
+static_assert(sizeof(CtlSnap) == 64, "CtlSnap mirrors the first 64 bytes of Ctl");
 __device__ __forceinline__ void ctl_snap(const Ctl* ctl, CtlSnap& sc) {
   if (threadIdx.x == 0) {
     const int4* src = reinterpret_cast<const int4*>(ctl);
@@ -152,6 +152,7 @@ __device__ __forceinline__ void ctl_snap(const Ctl* ctl, CtlSnap& sc) {
     dst[0] = __ldcg(src);
     dst[1] = __ldcg(src + 1);
     dst[2] = __ldcg(src + 2);
+    dst[3] = __ldcg(src + 3);
   }
   __syncthreads();
 }
@@ -1093,8 +1094,9 @@ __device__ void commit_vertex(const DevMesh& M, const DevField& F, const DevWork
     // Band-item changes for the split certificate of phase D (see
     // skip_union_ok): a lost band layer (or an overflowing band index) marks
     // the step; gained layers are listed.
+    const int cp = stamp & 1;  // change-tracking slot of this step
     if (binfo_overflow(old_bi) || binfo_overflow(bi)) {
-      W.ctl->dchange = 1;
+      W.ctl->dchange[cp] = 1;
     } else {
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
@@ -1105,12 +1107,12 @@ __device__ void commit_vertex(const DevMesh& M, const DevField& F, const DevWork
           lo_kept |= lo != 0 && binfo_layer(bi, q) == lo;
           ln_old |= ln != 0 && binfo_layer(old_bi, q) == ln;
         }
-        if (lo != 0 && !lo_kept) W.ctl->dchange = 1;
+        if (lo != 0 && !lo_kept) W.ctl->dchange[cp] = 1;
         if (ln != 0 && !ln_old) {
           W.add_stamp[v] = stamp;
-          const int pos = atomicAdd(&W.ctl->nadded, 1);
-          if (pos < W.added_cap) W.added[pos] = make_int2(v, static_cast<int>(ln));
-          else W.ctl->dchange = 1;
+          const int pos = atomicAdd(&W.ctl->nadded[cp], 1);
+          if (pos < W.added_cap) W.added[static_cast<size_t>(cp) * W.added_cap + pos] = make_int2(v, static_cast<int>(ln));
+          else W.ctl->dchange[cp] = 1;
         }
       }
     }
@@ -1370,9 +1372,10 @@ __device__ __forceinline__ unsigned long long seg_max_u64(unsigned peers, unsign
 // is not needed.  This marks the added items that are not so anchored.
 __device__ void anchor_test(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P, int nadded,
                             int stamp) {
+  const int cp = stamp & 1;
   const int n = min(nadded, W.added_cap);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int2 a = W.added[i];
+    const int2 a = W.added[static_cast<size_t>(cp) * W.added_cap + i];
     const int v = a.x;
     const unsigned l = static_cast<unsigned>(a.y);
     if (!W.active[l]) continue;
@@ -1381,7 +1384,29 @@ __device__ void anchor_test(const DevMesh& M, const DevField& F, const DevWork& 
       const int u = M.n_col[o];
       anchored = W.add_stamp[u] != stamp && band_slot_of(F, W, P, u, l) >= 0;
     }
-    if (!anchored) W.ctl->anchor_fail = 1;
+    if (!anchored) W.ctl->anchor_fail[cp] = 1;
+  }
+}
+
+// Component roots of the band items (ncomp of phase E), for a check whose
+// statistics were gathered under the split certificate that then failed.
+__device__ void phase_roots(const DevField& F, const DevWork& W, const StepParams& P, int lpar, int spar,
+                            unsigned long long ep, int n) {
+  LayerStat* g = W.stat + static_cast<size_t>(spar) * kMaxActive;
+  const int* list = W.ilist[lpar];
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
+    const int v = list[idx];
+    if (!F.interest[v]) continue;
+    const int cv = F.cnt[v];
+    const size_t b = static_cast<size_t>(v) * kSlots;
+    for (int k = 0; k < cv; ++k) {
+      const int l = F.lay[b + k];
+      const double x = F.val[b + k];
+      if (l == 0 || !W.active[l] || !(x > P.band_lo && x < P.sat)) continue;
+      const unsigned item = static_cast<unsigned>(v) * kSlots + k;
+      const unsigned long long pw = W.parent[item];
+      if ((pw >> 32) != ep || static_cast<unsigned>(pw) == item) atomicAdd(&g[W.aidx[l]].ncomp, 1);
+    }
   }
 }
 
@@ -1697,9 +1722,11 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
     if (gtid == 0) {
       ctl->rcount[cur ^ 1] = 0;
       ctl->sum_region += static_cast<unsigned long long>(nR);
-      ctl->dchange = 0;
-      ctl->nadded = 0;
-      ctl->anchor_fail = 0;
+      for (int q = 0; q < 2; ++q) {
+        ctl->dchange[q] = 0;
+        ctl->nadded[q] = 0;
+        ctl->anchor_fail[q] = 0;
+      }
     }
     for (int i = group_rank(P.map_mode & 2 ? 2 : 0); i < nR; i += gsz / kG)
       if (!update_vertex_fast(M, F, W, P, i, W.region[cur][i], false, threadIdx.x & (kG - 1), group_mask()))
@@ -1731,6 +1758,9 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       if (gtid == 0) {
         ctl->spec_error = 0;
         ctl->hash_acc = 0;
+        ctl->dchange[nxt] = 0;  // the slot B(s+1) will fill; step s-1 is done with it
+        ctl->nadded[nxt] = 0;
+        ctl->anchor_fail[nxt] = 0;
       }
     }
     grid_sync_snap(ctl, SC);
@@ -1752,10 +1782,10 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       const int nband = SC.ilcount[lpar];
       const int nR1 = SC.rcount[nxt];  // final since B(s)
       if (gtid == 0) ctl->sum_interest += static_cast<unsigned long long>(nband);
-      // The split certificate (anchor_test) replaces the union-find when it
-      // holds; its slot then runs the speculative A(s+1).
-      bool skip = !P.d_full && P.check_interval == 1 && !first_check && !SC.dchange;
-      bool a_done = false;
+      // Under the split certificate (anchor_test) the union-find is not
+      // needed, and E(s) runs in one phase with the speculative A(s+1).
+      const int spar = cur;
+      const bool skip = !P.d_full && P.check_interval == 1 && !first_check && !SC.dchange[cur];
       auto run_a = [&] {
         if (gtid == 0) {
           ctl->rcount[cur] = 0;
@@ -1771,29 +1801,6 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
           }
         }
       };
-      if (skip) {
-        anchor_test(M, F, W, P, SC.nadded, static_cast<int>(step));
-        if (more) {
-          run_a();
-          a_done = true;
-        }
-      } else {
-        phase_union(M, F, W, P, lpar, ep, group_rank(P.map_mode & 8 ? 1 : 0), gsz / kG, nband);
-      }
-      if (P.do_hash) phase_hash(F, W, M.nv);
-      block_done(W, step - (P.step_end - 64), 1);
-      grid_sync_snap(ctl, SC);
-      if (skip && SC.anchor_fail) {  // an unanchored new band item: run the union-find after all
-        skip = false;
-        phase_union(M, F, W, P, lpar, ep, group_rank(P.map_mode & 8 ? 1 : 0), gsz / kG, nband);
-        grid_sync(ctl);
-      }
-      if (prof) W.prof[pslot + 2] = gtimer();
-      block_start(W, step - (P.step_end - 64), 2);
-      // ---- 3: E(s) + speculative A(s+1) (unless it ran in the D slot)
-      const int spar = cur;
-      block_stats_init(S);
-      phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, QB, nband, !skip);
       // The CTA-level flushes of E (each a __syncthreads) come after A, so
       // the warps running A do not wait for the warps running E.
       auto flush_e = [&] {
@@ -1801,23 +1808,46 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
         bq_flush(Q, &ctl->ilcount[lpar ^ 1], W.ilist[lpar ^ 1]);
         bq_flush(QB, &ctl->nbandpairs, W.bandpairs, W.bandpair_cap, &ctl->bandpair_overflow);
       };
-      if (!more || P.split_a || a_done) flush_e();
-      if (more && !a_done) {
-        if (P.split_a) {
+      if (skip) {
+        // ---- 2+3: certificate, E(s) without roots, speculative A(s+1)
+        anchor_test(M, F, W, P, SC.nadded[cur], static_cast<int>(step));
+        if (P.do_hash) phase_hash(F, W, M.nv);
+        if (prof) W.prof[pslot + 2] = W.prof[pslot + 1];
+        block_stats_init(S);
+        phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, QB, nband, false);
+        if (more) run_a();
+        flush_e();
+        block_done(W, step - (P.step_end - 64), 2);
+        grid_sync_snap(ctl, SC);
+        if (SC.anchor_fail[cur]) {  // an unanchored new band item: the union-find after all
+          phase_union(M, F, W, P, lpar, ep, group_rank(P.map_mode & 8 ? 1 : 0), gsz / kG, nband);
           grid_sync(ctl);
-          if (prof) W.prof[pslot + 3] = gtimer();
+          phase_roots(F, W, P, lpar, spar, ep, nband);
+          grid_sync(ctl);
         }
-        run_a();
-        if (!P.split_a) flush_e();
+      } else {
+        // ---- 2: D(s) union-find
+        phase_union(M, F, W, P, lpar, ep, group_rank(P.map_mode & 8 ? 1 : 0), gsz / kG, nband);
+        if (P.do_hash) phase_hash(F, W, M.nv);
+        block_done(W, step - (P.step_end - 64), 1);
+        grid_sync(ctl);
+        if (prof) W.prof[pslot + 2] = gtimer();
+        block_start(W, step - (P.step_end - 64), 2);
+        // ---- 3: E(s) + speculative A(s+1)
+        block_stats_init(S);
+        phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, QB, nband, true);
+        if (!more || P.split_a) flush_e();
+        if (more) {
+          if (P.split_a) {
+            grid_sync(ctl);
+            if (prof) W.prof[pslot + 3] = gtimer();
+          }
+          run_a();
+          if (!P.split_a) flush_e();
+        }
+        block_done(W, step - (P.step_end - 64), 2);
+        grid_sync_snap(ctl, SC);
       }
-      // Change tracking of B(s+1) starts from zero (read after the barrier).
-      if (gtid == 0) {
-        ctl->dchange = 0;
-        ctl->nadded = 0;
-        ctl->anchor_fail = 0;
-      }
-      block_done(W, step - (P.step_end - 64), 2);
-      grid_sync_snap(ctl, SC);
       if (prof && !P.split_a) W.prof[pslot + 3] = gtimer();
       lpar ^= 1;
       if (P.do_hash && gtid == 0) {
@@ -1848,11 +1878,6 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       if (pend)
         for (int a = gtid; a < P.n_active; a += gsz) flush_stat(M, W, P, a, static_cast<int>(pend_step & 1), pend_step, true);
       pend = false;
-      if (gtid == 0) {
-        ctl->dchange = 0;
-        ctl->nadded = 0;
-        ctl->anchor_fail = 0;
-      }
       if (more) {
         const int nR1 = SC.rcount[nxt];  // snapshot after B(s)
         if (gtid == 0) {

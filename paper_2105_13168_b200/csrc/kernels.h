@@ -115,10 +115,10 @@ struct Ctl {
   int error;                 // DevError of a committed step
   int error_vertex;
   int spec_error;            // error raised by a speculative update (next step)
-  int dchange;               // this step removed a band item (or overflowed a band index / the added list)
-  int nadded;                // band items added this step (W.added)
-  int anchor_fail;           // an added band item has no related band item of the previous step
-  int pad_;
+  int dchange[2];            // by step parity: the step removed a band item (or overflowed a band index / list)
+  int nadded[2];             // by step parity: band items added (W.added)
+  int anchor_fail[2];        // by step parity: an added band item lacks a neighbour of the previous band
+  int pad_[2];
   int spec_error_vertex;
   int stop_bits;
   long long stop_step;       // last step executed by the kernel
@@ -172,7 +172,7 @@ struct DevWork {
   int2 *bandpairs = nullptr;            // (vertex, dense active index) band items of the last check
   int bandpair_cap = 0;
   unsigned long long *parent = nullptr; // nv * kSlots versioned UF parents
-  int2 *added = nullptr;                // band items (vertex, layer) added this step
+  int2 *added = nullptr;                // 2 x added_cap band items (vertex, layer) gained, by step parity
   int added_cap = 0;
   int *add_stamp = nullptr;             // per vertex: last step at which it gained a band item
   unsigned char *active = nullptr;      // kMaxLayers + 1
