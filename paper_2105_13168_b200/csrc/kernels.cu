@@ -1814,8 +1814,10 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
         if (P.do_hash) phase_hash(F, W, M.nv);
         if (prof) W.prof[pslot + 2] = W.prof[pslot + 1];
         block_stats_init(S);
-        phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, QB, nband, false);
+        // A first: its warps (filled from the top of each CTA) start at once,
+        // E's warps (the first two) pass through it without work.
         if (more) run_a();
+        phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, QB, nband, false);
         flush_e();
         block_done(W, step - (P.step_end - 64), 2);
         grid_sync_snap(ctl, SC);
