@@ -1218,9 +1218,9 @@ class PassEngine {
     if (const char* env = std::getenv("DTB_SPLIT_A"); env && env[0] == '1') p.split_a = 1;
     if (const char* env = std::getenv("DTB_NO_UNITE"); env && env[0] == '1') p.split_a_no_unite = 1;
     if (const char* env = std::getenv("DTB_D_FULL"); env && env[0] == '1') p.d_full = 1;
-    // E and D spread round-robin over the CTAs, A filled from each CTA's last
-    // warp so it overlaps E (measured: E+A 14.4 -> 13.4 us per step).
-    p.map_mode = 1 | 2 | 8;
+    // E, B and D spread round-robin over the CTAs, A filled from each CTA's
+    // last warp so it overlaps E (measured: E+A 14.4 -> 13.4 us per step).
+    p.map_mode = 1 | 2 | 4 | 8;
     if (const char* env = std::getenv("DTB_MAP")) p.map_mode = std::atoi(env);
     return p;
   }

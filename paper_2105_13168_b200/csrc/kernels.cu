@@ -1554,6 +1554,8 @@ __device__ __forceinline__ void band_mean(const DevMesh& M, const LayerStat& st,
 
 // snap_to_band (diffusion.hpp:590) over the recorded band items: nearest band
 // vertex to the band mean; key = distance bits (27 low bits dropped) | vertex.
+// Items are spread round-robin over the CTAs from each CTA's last warp, so the
+// snap runs beside the commits of phase B (mapped from the first warps).
 __device__ void phase_snap(const DevMesh& M, const DevWork& W, int spar, BlockStats& S) {
   LayerStat* g = W.stat + static_cast<size_t>(spar) * kMaxActive;
   const int n = min(W.ctl->nbandpairs, W.bandpair_cap);
@@ -1561,7 +1563,8 @@ __device__ void phase_snap(const DevMesh& M, const DevWork& W, int spar, BlockSt
   const int stride = gridDim.x * blockDim.x;
   const int trip = (n + stride - 1) / stride;
   for (int r = 0; r < trip; ++r) {
-    const int i = r * stride + blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = r * stride + (static_cast<int>(blockDim.x) - 1 - static_cast<int>(threadIdx.x)) * gridDim.x +
+                  blockIdx.x;
     int a = -1;
     unsigned long long key = ~0ull;
     if (i < n) {
