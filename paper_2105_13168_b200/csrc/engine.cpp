@@ -1152,6 +1152,12 @@ class PassEngine {
     }
   }
   ~PassEngine() {
+    // The result keeps the field: later queries on it must not use the
+    // stream destroyed here.
+    if (field_) {
+      cudaStreamSynchronize(s_);
+      field_->set_stream(nullptr);
+    }
     if (ev0_) cudaEventDestroy(ev0_);
     if (ev1_) cudaEventDestroy(ev1_);
     if (ev0k_) cudaEventDestroy(ev0k_);

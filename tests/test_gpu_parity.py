@@ -130,3 +130,18 @@ def test_event_heavy_chaotic_torus_matches_reference():
     assert first_bad is None and len(mine) == len(theirs), first_bad
     parity.compare_events(res.events(), ref["events"])
     parity.compare_tracks(res.tracks(), ref["tracks"])
+
+
+def test_result_queries_after_pass_and_between_passes():
+    """A result keeps its field after the pass engine (and its stream) is gone;
+    its device queries must keep working, also after further passes."""
+    mesh = dt.TriangleMesh.generate("genus:2:3")
+    op = dt.assemble_laplacian(mesh)
+    cfg = dt.default_config(max_steps=500)
+    r1 = dt.run_initial_pass(mesh, op, 0, cfg)
+    h1 = r1.field_hash()
+    r2 = dt.run_initial_pass(mesh, op, 5, cfg)
+    assert r1.field_hash() == h1
+    assert r2.field_hash() != 0
+    v, x = r1.layer_values(1)
+    assert len(v) == len(x)

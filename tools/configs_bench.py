@@ -1,0 +1,90 @@
+"""Measures the BASELINE.json configs other than the headline bench line
+(manual; prints one JSON line per config).  Usage on a GPU box:
+
+    python tools/configs_bench.py [--steps 3000] [--only 2,3,4]
+
+configs[2]: marching-tetrahedra gyroid, ~5M vertices, high genus: end-to-end
+            from host arrays (upload, device mesh build, assembly, pass,
+            results).
+configs[3]: Reeb graph construction on a genus-4 surface, ~535k vertices:
+            end-to-end pass + build_reeb.
+configs[4]: batch of 64 synthetic genus-1..32 meshes (shard.batch_specs),
+            one pass each on this GPU; with torchrun each rank runs its
+            round-robin slice (shard.run_sharded) and rank 0 reports.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2105_13168_b200 as dt  # noqa: E402
+from paper_2105_13168_b200 import shard  # noqa: E402
+
+
+def e2e(spec, steps, reps=2):
+    m0 = dt.TriangleMesh.generate(spec)
+    v, f = m0.vertices(), m0.faces()
+    info = m0.info()
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        m = dt.TriangleMesh.from_arrays(v, f)
+        op = dt.assemble_laplacian(m)
+        r = dt.run_initial_pass(m, op, 0, dt.default_config(max_steps=steps))
+        evs = r.events()
+        reeb = r.reeb()
+        t1 = time.perf_counter()
+        tm = r.timing()
+        row = {"e2e_ms": 1e3 * (t1 - t0), "pass_device_ms": 1e3 * tm["t_pass_device"], "status": r.status,
+               "steps": r.steps, "events": len(evs), "reeb_nodes": reeb["nodes"], "reeb_arcs": len(reeb["arcs"]),
+               "reeb_cycle_rank": reeb["cycle_rank"]}
+        if best is None or row["e2e_ms"] < best["e2e_ms"]:
+            best = row
+        del r, op, m
+    return dict(info, spec=spec, **best)
+
+
+def batch(steps, rank=0, world=1, dist=None):
+    specs = shard.batch_specs(64, 32, 3)
+    t0 = time.perf_counter()
+    res = shard.run_sharded(specs, rank, world, lambda s: shard.run_item(s, steps), dist)
+    t1 = time.perf_counter()
+    return {"meshes": len(specs), "n_gpus": world, "wall_s": t1 - t0,
+            "sum_pass_device_s": sum(r["t_pass"] for r in res),
+            "total_vertices": sum(r["V"] for r in res), "genus_range": [1, 32]}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=3000)
+    ap.add_argument("--only", default="2,3,4")
+    a = ap.parse_args()
+    only = {int(x) for x in a.only.split(",")}
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        tdist.init_process_group("nccl")
+        dist = tdist
+    dt.device_info()
+    if 2 in only and rank == 0:
+        print(json.dumps({"config": 2, **e2e("gyroid:8:26:0.3:1.0", a.steps)}), flush=True)
+    if 3 in only and rank == 0:
+        print(json.dumps({"config": 3, **e2e("genus:4:45", a.steps)}), flush=True)
+    if 4 in only:
+        out = batch(a.steps, rank, world, dist)
+        if rank == 0:
+            print(json.dumps({"config": 4, "steps_per_mesh": a.steps, **out}), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
