@@ -608,6 +608,233 @@ __device__ __forceinline__ bool gather_fold(const DevMesh& M, const DevField& F,
   return true;
 }
 
+// Fast path for the bulk of a single front: v and its stiffness neighbours
+// carry at most the base layer and one and the same active layer L (columns
+// of at most two owners, row of at most kG entries).  Then the candidate set
+// is {L} and its neighbour sum equals the total-Laplacian sum: both add
+// s_j * x_j(L) in row order, the latter also adding s_j * 0.0 = +-0.0 for
+// neighbours without L, which leaves a sum of positive-valued terms (never
+// -0.0) unchanged.  Every lane folds the two sums from shuffles and runs the
+// sequential update (the general fast path's arithmetic, term for term);
+// lanes 0..n-1 store the new column.  Returns false, with no side effects,
+// when the case does not apply.
+__device__ bool update_vertex_single(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P,
+                                     int i, int v, bool spec, int lane, unsigned gm) {
+  const int cv = F.cnt[v];
+  const size_t vb = static_cast<size_t>(v) * kSlots;
+  const unsigned own_lw = *reinterpret_cast<const unsigned*>(F.lay + vb);  // slots 0, 1
+  const double2 own_x = *reinterpret_cast<const double2*>(F.val + vb);
+  const int k0 = __ldg(M.s_off + v), k1 = __ldg(M.s_off + v + 1);
+  const double mass = __ldg(M.mass + v);
+  const int k = k0 + lane;
+  const bool valid = k < k1;
+  int u = 0;
+  double s = 0.0;
+  if (valid) {
+    u = __ldg(M.s_col + k);
+    s = __ldg(M.s_val + k);
+  }
+  const size_t ub = static_cast<size_t>(u) * kSlots;
+  const int cu = valid ? static_cast<int>(F.cnt[u]) : 0;
+  const unsigned nlw = valid ? *reinterpret_cast<const unsigned*>(F.lay + ub) : 0u;
+  const double2 nx = valid ? *reinterpret_cast<const double2*>(F.val + ub) : make_double2(0.0, 0.0);
+  if (cv > 2 || k1 - k0 > kG) return false;  // group-uniform
+  // Own column: [base][, L] or [L].
+  const unsigned o0 = own_lw & 0xFFFFu, o1 = own_lw >> 16;
+  const double phib = (cv > 0 && o0 == 0) ? own_x.x : 0.0;
+  unsigned ol = 0;  // own non-base layer (0: none)
+  double ox = 0.0;
+  bool bad = false;
+  if (cv == 1 && o0 != 0) {
+    ol = o0;
+    ox = own_x.x;
+  } else if (cv == 2) {
+    if (o0 != 0) bad = true;  // two non-base owners
+    ol = o1;
+    ox = own_x.y;
+  }
+  // Neighbour column: base value and its non-base layer.
+  double bu = 0.0, xl = 0.0;
+  unsigned nl = 0;
+  if (valid) {
+    const unsigned a0 = nlw & 0xFFFFu, a1 = nlw >> 16;
+    if (cu > 2) {
+      bad = true;
+    } else if (cu == 1) {
+      if (a0 == 0) bu = nx.x;
+      else {
+        nl = a0;
+        xl = nx.x;
+      }
+    } else if (cu == 2) {
+      if (a0 != 0) bad = true;
+      bu = nx.x;
+      nl = a1;
+      xl = nx.y;
+    }
+  }
+  if (__any_sync(gm, bad)) return false;
+  // One common non-base layer L across v and its neighbours.
+  const unsigned lo = __reduce_min_sync(gm, min(nl ? nl : 0xFFFFFFFFu, ol ? ol : 0xFFFFFFFFu));
+  const unsigned hi = __reduce_max_sync(gm, max(nl, ol));
+  const bool has_l = lo != 0xFFFFFFFFu;
+  if (has_l && lo != hi) return false;
+  const unsigned L = has_l ? lo : 0u;
+  if (has_l && !W.active[L]) return false;
+  // Ordered folds of s_j * bu_j and s_j * x_j(L) (au_j) over the row.
+  const double tb = s * bu, tt = s * xl;
+  const bool bpos = valid && bu > 0.0;
+  double lapb = 0.0, lapt = 0.0;
+  const int nvalid = k1 - k0;
+#pragma unroll
+  for (int jj = 0; jj < kG; ++jj) {
+    const double b_ = __shfl_sync(gm, tb, jj, kG);
+    const double t_ = __shfl_sync(gm, tt, jj, kG);
+    if (jj < nvalid) {
+      lapb = lapb + b_;
+      lapt = lapt + t_;
+    }
+  }
+  const bool bnear = phib > 0.0 || __any_sync(gm, bpos);
+  // ---- the sequential update (uniform across the group's lanes)
+  const double lap_b = lapb / mass;
+  bool touched = false, cupd = false, bupd = false;
+  double cn = 0.0, bnext = 0.0;
+  if (has_l) {
+    const double phi = ol == L ? ox : 0.0;
+    if (!(phi == 0.0 && phib <= P.prune)) {
+      const double lap_i = lapt / mass;
+      const double inner = P.w * (phib - phi) + P.half_a2 * (lap_b - lap_i) - P.e * sqrt(max0(phi * phib));
+      const double rate = -P.mu_n * inner;
+      if (!isfinite(rate)) {
+        if (lane == 0) raise_error(W.ctl, kDevBlowup, v, spec);
+        return true;
+      }
+      const double next = clamp01(phi + P.dt * rate);
+      if (next != phi) {
+        touched = true;
+        cupd = true;
+        cn = next;
+      }
+    }
+  }
+  if (bnear) {
+    double total = 0.0, contact = 0.0;
+    if (ol != 0) total = total + ox;  // ol == L, active
+    if (ol != 0) contact = contact + sqrt(max0(phib * ox));
+    const double lap_total = lapt / mass;
+    const double rate = -P.mu_n * (P.w * total + P.half_a2 * lap_total + P.e * contact) +
+                        P.m_mu_n * (P.w * phib + P.half_a2 * lap_b);
+    if (!isfinite(rate)) {
+      if (lane == 0) raise_error(W.ctl, kDevBlowup, v, spec);
+      return true;
+    }
+    const double next = clamp01(phib + P.dt * rate);
+    if (next != phib) {
+      touched = true;
+      bupd = true;
+      bnext = next;
+    }
+  }
+  // set_value into the (at most two-entry) column, sorted by layer.
+  bool changed = false;
+  unsigned El[2] = {0, 0};
+  double Ex[2] = {0.0, 0.0};
+  int n = 0;
+  auto put = [&](unsigned l, double x) {
+    if (n == 0) {
+      El[0] = l;
+      Ex[0] = x;
+    } else {
+      El[1] = l;
+      Ex[1] = x;
+    }
+    ++n;
+  };
+  for (int q = 0; q < 2; ++q) {
+    if (q >= cv) break;
+    const unsigned lq = q == 0 ? o0 : o1;
+    const double xq = q == 0 ? own_x.x : own_x.y;
+    double val = xq;
+    bool upd = false;
+    if (lq == 0) {
+      if (bupd) {
+        val = bnext;
+        upd = true;
+      }
+    } else if (cupd) {  // lq == L
+      val = cn;
+      upd = true;
+    }
+    if (upd) {
+      if (val > 1.0) val = 1.0;
+      if (val < P.prune) val = 0.0;
+      if (val != xq) changed = true;
+    }
+    if (val != 0.0) put(lq, val);
+  }
+  if (bupd && phib == 0.0) {  // base enters the column (sorted first)
+    double val = bnext;
+    if (val > 1.0) val = 1.0;
+    if (val < P.prune) val = 0.0;
+    if (val != 0.0) {
+      if (n == 1) {
+        El[1] = El[0];
+        Ex[1] = Ex[0];
+      }
+      El[0] = 0;
+      Ex[0] = val;
+      ++n;
+      changed = true;
+    }
+  }
+  if (cupd && ol != L) {  // L enters the column (after the base)
+    double val = cn;
+    if (val > 1.0) val = 1.0;
+    if (val < P.prune) val = 0.0;
+    if (val != 0.0) {
+      put(L, val);
+      changed = true;
+    }
+  }
+  // Column normalisation of touched vertices (layer_field.hpp:143).
+  if (touched) {
+    double ssum = 0.0;
+    for (int j = 0; j < n; ++j) ssum = ssum + Ex[j];
+    if (ssum <= 0.0) {
+      if (lane == 0) raise_error(W.ctl, kDevZeroColumn, v, spec);
+      return true;
+    }
+    if (!(fabs(ssum - 1.0) < 1e-15)) {
+      int m = 0;
+      for (int j = 0; j < n; ++j) {
+        double q = Ex[j] / ssum;
+        if (q > 1.0) q = 1.0;
+        if (q < P.prune) q = 0.0;
+        if (q != Ex[j]) changed = true;
+        if (q != 0.0) {
+          El[m] = El[j];
+          Ex[m] = q;
+          ++m;
+        }
+      }
+      n = m;
+    }
+  }
+  const bool old_one = cv > 0 && o0 == 0 && own_x.x == 1.0;
+  const bool new_one = n > 0 && El[0] == 0 && Ex[0] == 1.0;
+  const size_t o = static_cast<size_t>(i) * kSlots;
+  if (lane < n) {
+    W.slay[o + lane] = static_cast<unsigned short>(lane == 0 ? El[0] : El[1]);
+    W.sval[o + lane] = lane == 0 ? Ex[0] : Ex[1];
+  }
+  if (lane == 0) {
+    W.scnt[i] = static_cast<unsigned char>(n);
+    W.sflag[i] = static_cast<unsigned char>((changed ? 1 : 0) | (old_one ? 2 : 0) | (new_one ? 4 : 0));
+  }
+  return true;
+}
+
 __device__ bool update_vertex_fast(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P, int i,
                                    int v, bool spec, int lane, unsigned gm) {
   INSTR_C0(tA);
@@ -1732,7 +1959,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       }
     }
     for (int i = group_rank(P.map_mode & 2 ? 2 : 0); i < nR; i += gsz / kG)
-      if (!update_vertex_fast(M, F, W, P, i, W.region[cur][i], false, threadIdx.x & (kG - 1), group_mask()))
+      if (!update_vertex_single(M, F, W, P, i, W.region[cur][i], false, threadIdx.x & (kG - 1), group_mask()) &&
+              !update_vertex_fast(M, F, W, P, i, W.region[cur][i], false, threadIdx.x & (kG - 1), group_mask()))
         update_vertex(M, F, W, P, i, W.region[cur][i], false, threadIdx.x & (kG - 1), group_mask());
     grid_sync_snap(ctl, SC);
     if (SC.error) stop = kStopError;
@@ -1796,7 +2024,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
         }
         for (int i = group_rank(P.map_mode & 2 ? 2 : 0); i < nR1; i += gsz / kG) {
           INSTR_T0(t0);
-          if (!update_vertex_fast(M, F, W, P, i, W.region[nxt][i], true, threadIdx.x & (kG - 1), group_mask())) {
+          if (!update_vertex_single(M, F, W, P, i, W.region[nxt][i], true, threadIdx.x & (kG - 1), group_mask()) &&
+              !update_vertex_fast(M, F, W, P, i, W.region[nxt][i], true, threadIdx.x & (kG - 1), group_mask())) {
             update_vertex(M, F, W, P, i, W.region[nxt][i], true, threadIdx.x & (kG - 1), group_mask());
             INSTR_REC(4, t0, (threadIdx.x & (kG - 1)) == 0);
           } else {
@@ -1890,7 +2119,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
           ctl->sum_region += static_cast<unsigned long long>(nR1);
         }
         for (int i = group_rank(P.map_mode & 2 ? 2 : 0); i < nR1; i += gsz / kG)
-          if (!update_vertex_fast(M, F, W, P, i, W.region[nxt][i], false, threadIdx.x & (kG - 1), group_mask()))
+          if (!update_vertex_single(M, F, W, P, i, W.region[nxt][i], false, threadIdx.x & (kG - 1), group_mask()) &&
+              !update_vertex_fast(M, F, W, P, i, W.region[nxt][i], false, threadIdx.x & (kG - 1), group_mask()))
             update_vertex(M, F, W, P, i, W.region[nxt][i], false, threadIdx.x & (kG - 1), group_mask());
       }
       grid_sync_snap(ctl, SC);
