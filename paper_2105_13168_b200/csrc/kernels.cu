@@ -1601,7 +1601,9 @@ __device__ void anchor_test(const DevMesh& M, const DevField& F, const DevWork& 
                             int stamp) {
   const int cp = stamp & 1;
   const int n = min(nadded, W.added_cap);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+  // Warp 3 of every CTA: the warps between E's (first) and A's (last).
+  if ((threadIdx.x >> 5) != 3) return;
+  for (int i = (threadIdx.x & 31) * gridDim.x + blockIdx.x; i < n; i += 32 * gridDim.x) {
     const int2 a = W.added[static_cast<size_t>(cp) * W.added_cap + i];
     const int v = a.x;
     const unsigned l = static_cast<unsigned>(a.y);
@@ -1973,8 +1975,12 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
     const bool prof = W.prof && gtid == 0 && pslot + 3 < W.prof_cap;
     if (prof) W.prof[pslot] = gtimer();
     // ---- 1: B(s)   (SC: snapshot taken after the previous barrier)
+    block_start(W, step - (P.step_end - 64), 0);
     {
+      // The commits (first warps) and the trail snap of check s-1 (last
+      // warps) are independent and run side by side; both flush at the end.
       const int nR = SC.rcount[cur];
+      block_stats_init(S);
       for (int i = group_rank(P.map_mode & 4 ? 1 : 0); i < nR; i += gsz / kG)
       {
         INSTR_T0(t0);
@@ -1982,9 +1988,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
                       group_mask(), Q);
         INSTR_REC(0, t0, (threadIdx.x & (kG - 1)) == 0);
       }
-      bq_flush(Q, &ctl->rcount[nxt], W.region[nxt]);
-      block_stats_init(S);
       if (pend && P.record_trails) phase_snap(M, W, static_cast<int>(pend_step & 1), S);
+      bq_flush(Q, &ctl->rcount[nxt], W.region[nxt]);
       block_stats_flush(S, W.stat + static_cast<size_t>(pend_step & 1) * kMaxActive, pend ? P.n_active : 0);
       if (gtid == 0) {
         ctl->spec_error = 0;
@@ -1994,6 +1999,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
         ctl->anchor_fail[nxt] = 0;
       }
     }
+    block_done(W, step - (P.step_end - 64), 0);
     grid_sync_snap(ctl, SC);
     if (prof) W.prof[pslot + 1] = gtimer();
     block_start(W, step - (P.step_end - 64), 1);
@@ -2042,6 +2048,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       };
       if (skip) {
         // ---- 2+3: certificate, E(s) without roots, speculative A(s+1)
+        block_start(W, step - (P.step_end - 64), 2);
         anchor_test(M, F, W, P, SC.nadded[cur], static_cast<int>(step));
         if (P.do_hash) phase_hash(F, W, M.nv);
         if (prof) W.prof[pslot + 2] = W.prof[pslot + 1];
