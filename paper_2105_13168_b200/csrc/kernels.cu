@@ -2007,7 +2007,11 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       ++ep;
       // ---- 2: D(s) + flush of the previous check's trail records
       if (pend)
-        for (int a = gtid; a < P.n_active; a += gsz) flush_stat(M, W, P, a, static_cast<int>(pend_step & 1), pend_step, true);
+        // Trail records of check s-1 on warp 4 of every CTA (idle in this
+        // phase), not on CTA 0's first warp, which runs E.
+        if ((threadIdx.x >> 5) == 4)
+          for (int a = (threadIdx.x & 31) * gridDim.x + blockIdx.x; a < P.n_active; a += 32 * gridDim.x)
+            flush_stat(M, W, P, a, static_cast<int>(pend_step & 1), pend_step, true);
       pend = false;
       if (gtid == 0) {
         ctl->ilcount[lpar ^ 1] = 0;
@@ -2117,7 +2121,11 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       // ---- 3': trail flush of the previous check (its stats parity is
       // reused two steps later) + A(s+1)
       if (pend)
-        for (int a = gtid; a < P.n_active; a += gsz) flush_stat(M, W, P, a, static_cast<int>(pend_step & 1), pend_step, true);
+        // Trail records of check s-1 on warp 4 of every CTA (idle in this
+        // phase), not on CTA 0's first warp, which runs E.
+        if ((threadIdx.x >> 5) == 4)
+          for (int a = (threadIdx.x & 31) * gridDim.x + blockIdx.x; a < P.n_active; a += 32 * gridDim.x)
+            flush_stat(M, W, P, a, static_cast<int>(pend_step & 1), pend_step, true);
       pend = false;
       if (more) {
         const int nR1 = SC.rcount[nxt];  // snapshot after B(s)
