@@ -1254,6 +1254,29 @@ __device__ void bq_flush(BlockQueueT<T>& q, int* gcount, T* glist, int cap = 0x7
   __syncthreads();
 }
 
+// Two block queues flushed together: their global ranges are reserved by two
+// threads at once, so the CTA waits for one atomic round trip, not two.
+template <class T1, class T2>
+__device__ void bq_flush2(BlockQueueT<T1>& q1, int* gcount1, T1* glist1, BlockQueueT<T2>& q2, int* gcount2, T2* glist2,
+                          int cap2, int* overflow2) {
+  __syncthreads();
+  const int n1 = min(q1.n, kQCap), n2 = min(q2.n, kQCap);
+  if (threadIdx.x == 0) q1.base = n1 ? atomicAdd(gcount1, n1) : 0;
+  if (threadIdx.x == 32) q2.base = n2 ? atomicAdd(gcount2, n2) : 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n1; i += blockDim.x) glist1[q1.base + i] = q1.buf[i];
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+    if (q2.base + i < cap2) glist2[q2.base + i] = q2.buf[i];
+    else if (overflow2) *overflow2 = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    q1.n = 0;
+    q2.n = 0;
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ void queue_region(const DevWork& W, int u, int stamp, int nxt, BlockQueue& Q) {
   if (atomicExch(W.stamp + u, stamp) != stamp) bq_push(Q, &W.ctl->rcount[nxt], W.region[nxt], u);
 }
@@ -2047,8 +2070,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       // the warps running A do not wait for the warps running E.
       auto flush_e = [&] {
         block_stats_flush(S, W.stat + static_cast<size_t>(spar) * kMaxActive, P.n_active, ctl);
-        bq_flush(Q, &ctl->ilcount[lpar ^ 1], W.ilist[lpar ^ 1]);
-        bq_flush(QB, &ctl->nbandpairs, W.bandpairs, W.bandpair_cap, &ctl->bandpair_overflow);
+        bq_flush2(Q, &ctl->ilcount[lpar ^ 1], W.ilist[lpar ^ 1], QB, &ctl->nbandpairs, W.bandpairs, W.bandpair_cap,
+                  &ctl->bandpair_overflow);
       };
       if (skip) {
         // ---- 2+3: certificate, E(s) without roots, speculative A(s+1)
