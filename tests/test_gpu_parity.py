@@ -145,3 +145,18 @@ def test_result_queries_after_pass_and_between_passes():
     assert r2.field_hash() != 0
     v, x = r1.layer_values(1)
     assert len(v) == len(x)
+
+
+@pytest.mark.parametrize("spec,steps", [("torus:96:32:3:1.0", 2500), ("genus:2:3", 1500)])
+def test_split_certificate_matches_full_union_find(spec, steps, monkeypatch):
+    """The split certificate (skipping the front union-find on steps that
+    cannot split a front) gives the same trajectory and events as running the
+    union-find at every check (DTB_D_FULL=1)."""
+    mesh = dt.TriangleMesh.generate(spec)
+    op = dt.assemble_laplacian(mesh)
+    cfg = dt.default_config(max_steps=steps, record_hashes=1)
+    fast = dt.run_initial_pass(mesh, op, 0, cfg)
+    monkeypatch.setenv("DTB_D_FULL", "1")
+    full = dt.run_initial_pass(mesh, op, 0, cfg)
+    assert [int(h) for h in fast.hashes()] == [int(h) for h in full.hashes()]
+    assert [(e.kind, e.step, e.layers) for e in fast.events()] == [(e.kind, e.step, e.layers) for e in full.events()]
