@@ -1716,8 +1716,12 @@ __device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& 
     const long long px = live ? fxv : 0, py = live ? fyv : 0, pz = live ? fzv : 0;
     if (live) INSTR_CP(9, tE);
     bool cand = false;
-    const int kmax = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(cv));
-    for (int k = 0; k < kmax; ++k) {
+    // The base owner (layer 0, always slot 0) contributes nothing below, so
+    // lanes walk their non-base slots only: one round for a single front.
+    const int kb = (cv > 0 && L4[0] == 0) ? 1 : 0;
+    const int kmax = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(cv - kb));
+    for (int k2 = 0; k2 < kmax; ++k2) {
+      const int k = k2 + kb;
       int a = -1;
       bool band = false, unsat = false, root = false;
       if (k < cv) {
