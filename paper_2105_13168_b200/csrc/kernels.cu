@@ -1593,6 +1593,42 @@ __device__ void block_stats_flush(BlockStats& S, LayerStat* g, int n_active, Ctl
   }
 }
 
+// E's flush when E runs on warps of its own (the first nE threads): a named
+// barrier among those warps replaces __syncthreads, so the CTA's A warps
+// never wait for it.  Same effect as block_stats_flush + bq_flush2.
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ void flush_e_named(BlockStats& S, LayerStat* g, int n_active, Ctl* ctl, BlockQueue& Q, int* gc1, int* gl1,
+                              PairQueue& QB, int* gc2, int2* gl2, int cap2, int* ovf2, int nE) {
+  named_sync(1, nE);
+  if (threadIdx.x == 0 && S.bmax) atomicMax(&ctl->base_max_bits, S.bmax);
+  for (int a = threadIdx.x; a < n_active && a < kSmemLayers; a += nE) {
+    if (S.cnt[a][0]) atomicAdd(&g[a].ncomp, S.cnt[a][0]);
+    if (S.cnt[a][1]) atomicAdd(&g[a].nband, S.cnt[a][1]);
+    if (S.cnt[a][2]) atomicAdd(&g[a].nunsat, S.cnt[a][2]);
+    for (int c = 0; c < 3; ++c)
+      if (S.sum[a][c])
+        atomicAdd(reinterpret_cast<unsigned long long*>(c == 0 ? &g[a].sx : (c == 1 ? &g[a].sy : &g[a].sz)),
+                  static_cast<unsigned long long>(S.sum[a][c]));
+    if (S.snap[a] != ~0ull) atomicMin(&g[a].snap, S.snap[a]);
+  }
+  const int n1 = min(Q.n, kQCap), n2 = min(QB.n, kQCap);
+  if (threadIdx.x == 0) Q.base = n1 ? atomicAdd(gc1, n1) : 0;
+  if (threadIdx.x == (nE > 32 ? 32 : 1)) QB.base = n2 ? atomicAdd(gc2, n2) : 0;
+  named_sync(1, nE);
+  for (int i = threadIdx.x; i < n1; i += nE) gl1[Q.base + i] = Q.buf[i];
+  for (int i = threadIdx.x; i < n2; i += nE) {
+    if (QB.base + i < cap2) gl2[QB.base + i] = QB.buf[i];
+    else if (ovf2) *ovf2 = 1;
+  }
+  named_sync(1, nE);
+  if (threadIdx.x == 0) {  // read again only after the grid barrier that ends the phase
+    Q.n = 0;
+    QB.n = 0;
+  }
+}
+
 // Segmented warp reductions: lanes holding the same key (dense active layer
 // index) combine their contributions with 32-bit __reduce_*_sync, so each
 // warp issues one shared-memory atomic per layer (64-bit shared atomics are
@@ -2054,11 +2090,13 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       // needed, and E(s) runs in one phase with the speculative A(s+1).
       const int spar = cur;
       const bool skip = !P.d_full && P.check_interval == 1 && !first_check && !SC.dchange[cur];
+      // Frontier s+2 starts empty; the counter update is by thread 0 of the
+      // grid whichever warp role it has in this phase.
+      if (more && gtid == 0) {
+        ctl->rcount[cur] = 0;
+        ctl->sum_region += static_cast<unsigned long long>(nR1);
+      }
       auto run_a = [&] {
-        if (gtid == 0) {
-          ctl->rcount[cur] = 0;
-          ctl->sum_region += static_cast<unsigned long long>(nR1);
-        }
         for (int i = group_rank(P.map_mode & 2 ? 2 : 0); i < nR1; i += gsz / kG) {
           INSTR_T0(t0);
           if (!update_vertex_single(M, F, W, P, i, W.region[nxt][i], true, threadIdx.x & (kG - 1), group_mask()) &&
@@ -2084,11 +2122,31 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
         if (P.do_hash) phase_hash(F, W, M.nv);
         if (prof) W.prof[pslot + 2] = W.prof[pslot + 1];
         block_stats_init(S);
-        // A first: its warps (filled from the top of each CTA) start at once,
-        // E's warps (the first two) pass through it without work.
-        if (more) run_a();
-        phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, QB, nband, false);
-        flush_e();
+        // E occupies the first warps (spread map), A the last ones.  When they
+        // are disjoint, E flushes behind a named barrier of its own warps and
+        // A never waits for it; otherwise A runs first and E flushes at the
+        // end with __syncthreads.
+        const int e_per_cta = (nband + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x);
+        const int a_per_cta = (nR1 + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x);
+        const int e_warps = (e_per_cta + 31) / 32, a_warps = (a_per_cta + 3) / 4;
+        const bool e_alone = (P.map_mode & 3) == 3 && e_per_cta <= static_cast<int>(blockDim.x) &&
+                             a_per_cta <= static_cast<int>(blockDim.x) / kG &&
+                             e_warps + a_warps <= static_cast<int>(blockDim.x) / 32 && e_warps > 0;
+        if (e_alone) {
+          const int warp = threadIdx.x >> 5;
+          if (warp < e_warps) {
+            phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, QB, nband, false);
+            flush_e_named(S, W.stat + static_cast<size_t>(spar) * kMaxActive, P.n_active, ctl, Q,
+                          &ctl->ilcount[lpar ^ 1], W.ilist[lpar ^ 1], QB, &ctl->nbandpairs, W.bandpairs,
+                          W.bandpair_cap, &ctl->bandpair_overflow, e_warps * 32);
+          } else if (more) {
+            run_a();
+          }
+        } else {
+          if (more) run_a();
+          phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, QB, nband, false);
+          flush_e();
+        }
         block_done(W, step - (P.step_end - 64), 2);
         grid_sync_snap(ctl, SC);
         if (SC.anchor_fail[cur]) {  // an unanchored new band item: the union-find after all
