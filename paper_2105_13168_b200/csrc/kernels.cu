@@ -212,6 +212,16 @@ constexpr int kReg = 4;  // neighbour-column slots kept in registers (packed as 
 
 __device__ __forceinline__ unsigned group_mask() { return 0xFFu << (threadIdx.x & 24); }
 
+// Dynamic shared memory: one slab per 8-lane group, used either for the fold
+// staging of the fast update or for the work arrays of the general update
+// (which would otherwise live in local memory, i.e. in L2).
+constexpr int kSlabBytes = 1600;
+constexpr int kDynSmem = (kBlock / kG) * kSlabBytes;
+extern __shared__ double s_dyn[];
+__device__ __forceinline__ char* group_slab() {
+  return reinterpret_cast<char*>(s_dyn) + static_cast<size_t>(threadIdx.x / kG) * kSlabBytes;
+}
+
 // Work-to-CTA maps.  Rank r of a group (or thread) is spread round-robin over
 // the CTAs so every SM gets an equal share of a short list; the "high" map
 // fills each CTA from its last warp so that it does not collide with work
@@ -239,17 +249,28 @@ __device__ __forceinline__ void cand_add(unsigned short* cl, double* ca, int& nc
 
 __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P,
                               int i, int v, bool spec, int lane, unsigned gm) {
-  unsigned short ol[kSlots];
-  double ox[kSlots];
+  // Work arrays in the group's shared-memory slab.  Every lane of the group
+  // runs this code with the same values, so each lane reads back what it
+  // (and its siblings, identically) wrote.
+  double* const ox = reinterpret_cast<double*>(group_slab());
+  double* const ca = ox + kSlots;
+  double* const nx = ca + kCand;
+  double* const sx = nx + kWork;
+  unsigned short* const ol = reinterpret_cast<unsigned short*>(sx + kWork);
+  unsigned short* const cl = ol + kSlots;
+  unsigned short* const nl = cl + kCand;
+  unsigned short* const sl = nl + kWork;
+  static_assert((kSlots + kCand + 2 * kWork) * (8 + 2) <= kSlabBytes, "the general update's arrays fit the slab");
+  __syncwarp(gm);  // the slab may hold the fold staging of this group's previous vertex
   const int cv = F.cnt[v];
-  for (int j = 0; j < cv; ++j) {
-    ol[j] = F.lay[static_cast<size_t>(v) * kSlots + j];
-    ox[j] = F.val[static_cast<size_t>(v) * kSlots + j];
-  }
-  const double phib = (cv > 0 && ol[0] == 0) ? ox[0] : 0.0;
+  const size_t vb = static_cast<size_t>(v) * kSlots;
+  if (lane == 0)
+    for (int j = 0; j < cv; ++j) {
+      ol[j] = F.lay[vb + j];
+      ox[j] = F.val[vb + j];
+    }
+  const double phib = (cv > 0 && F.lay[vb] == 0) ? F.val[vb] : 0.0;
 
-  unsigned short cl[kCand];
-  double ca[kCand];
   int nc = 0;
   double lapb = 0.0, lapt = 0.0;
   bool bnear = phib > 0.0;
@@ -304,18 +325,22 @@ __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork
       for (int q = 0; q < kReg; ++q) {
         const int l_ = __shfl_sync(gm, static_cast<int>(L[q]), jj, kG);
         const double x_ = __shfl_sync(gm, X[q], jj, kG);
-        if (q < cu_ && l_ != 0 && W.active[l_]) cand_add(cl, ca, nc, overflow, l_, s_ * x_);
+        if (lane == 0 && q < cu_ && l_ != 0 && W.active[l_]) cand_add(cl, ca, nc, overflow, l_, s_ * x_);
       }
       if (cu_ > kReg) {
         const int u_ = __shfl_sync(gm, u, jj, kG);
         const size_t b = static_cast<size_t>(u_) * kSlots;
         for (int q = kReg; q < cu_; ++q) {
           const int l_ = F.lay[b + q];
-          if (l_ != 0 && W.active[l_]) cand_add(cl, ca, nc, overflow, l_, s_ * F.val[b + q]);
+          if (lane == 0 && l_ != 0 && W.active[l_]) cand_add(cl, ca, nc, overflow, l_, s_ * F.val[b + q]);
         }
       }
     }
   }
+  // From here on lane 0 alone: the candidate list and the working column live
+  // in the group's slab, so only one lane may write them.  (Its siblings meet
+  // it again at the group's next shuffle or __syncwarp.)
+  if (lane != 0) return;
   // Layers held at v itself are near support even if the stiffness row
   // lacks its diagonal (never on valid meshes, kept for exactness).
   for (int j = 0; j < cv; ++j) {
@@ -340,8 +365,6 @@ __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork
 
   const double mass = __ldg(M.mass + v);
   const double lap_b = lapb / mass;
-  unsigned short nl[kWork];
-  double nx[kWork];
   int nn = cv;
   for (int j = 0; j < cv; ++j) {
     nl[j] = ol[j];
@@ -400,8 +423,6 @@ __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork
       return;
     }
     if (!(fabs(s - 1.0) < 1e-15)) {
-      unsigned short sl[kWork];
-      double sx[kWork];
       const int sn = nn;
       for (int j = 0; j < sn; ++j) {
         sl[j] = nl[j];
@@ -417,14 +438,12 @@ __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork
   const bool old_one = cv > 0 && ol[0] == 0 && ox[0] == 1.0;
   const bool new_one = nn > 0 && nl[0] == 0 && nx[0] == 1.0;
   const size_t o = static_cast<size_t>(i) * kSlots;
-  for (int j = lane; j < nn; j += kG) {
+  for (int j = 0; j < nn; ++j) {
     W.slay[o + j] = nl[j];
     W.sval[o + j] = nx[j];
   }
-  if (lane == 0) {
-    W.scnt[i] = static_cast<unsigned char>(nn);
-    W.sflag[i] = static_cast<unsigned char>((changed ? 1 : 0) | (old_one ? 2 : 0) | (new_one ? 4 : 0));
-  }
+  W.scnt[i] = static_cast<unsigned char>(nn);
+  W.sflag[i] = static_cast<unsigned char>((changed ? 1 : 0) | (old_one ? 2 : 0) | (new_one ? 4 : 0));
 }
 
 // ---------------------------------------------------------------------------
@@ -484,9 +503,7 @@ __device__ __forceinline__ void reg_insert(int (&El)[kN], double (&Ex)[kN], int&
 // Staging for the ordered neighbour folds of update_vertex_fold: lane j of a
 // group parks its contributions here and lanes 0..5 each fold one column.
 constexpr int kFoldCols = kF + 2;  // kF candidate layers, base laplacian, total laplacian
-constexpr int kFoldSmem = kBlock * kFoldCols * static_cast<int>(sizeof(double));  // dynamic shared memory
-extern __shared__ double s_dyn[];
-__device__ __forceinline__ double (*fold_buf())[kFoldCols] { return reinterpret_cast<double(*)[kFoldCols]>(s_dyn); }
+static_assert(kG * kFoldCols * 8 <= kSlabBytes, "the fold staging of a group fits its slab");
 
 // Gather of the fast path for rows of at most kG stiffness entries whose
 // neighbour columns fit kReg slots (the bulk of a front).  The candidate
@@ -567,7 +584,7 @@ __device__ __forceinline__ bool gather_fold(const DevMesh& M, const DevField& F,
   }
   INSTR_CP(13, tG);
   // Contributions, staged per lane.
-  double(*s_fold)[kFoldCols] = fold_buf();
+  double* s_fold = reinterpret_cast<double*>(group_slab());  // [lane][kFoldCols]
   const int base = threadIdx.x & ~(kG - 1);
   const int gshift = threadIdx.x & 24;
   unsigned pm[kF];
@@ -581,11 +598,11 @@ __device__ __forceinline__ bool gather_fold(const DevMesh& M, const DevField& F,
         t = s * X[q];
         present = true;
       }
-    s_fold[threadIdx.x][c] = t;
+    s_fold[lane * kFoldCols + c] = t;
     pm[c] = (__ballot_sync(gm, present) >> gshift) & 0xFFu;
   }
-  s_fold[threadIdx.x][kF] = s * bu;
-  s_fold[threadIdx.x][kF + 1] = s * au;
+  s_fold[lane * kFoldCols + kF] = s * bu;
+  s_fold[lane * kFoldCols + kF + 1] = s * au;
   const unsigned vm = (__ballot_sync(gm, valid) >> gshift) & 0xFFu;
   bnear = bnear || ((__ballot_sync(gm, valid && bu > 0.0) >> gshift) & 0xFFu) != 0;
   __syncwarp(gm);
@@ -597,7 +614,7 @@ __device__ __forceinline__ bool gather_fold(const DevMesh& M, const DevField& F,
       if (lane == c) use = pm[c];
 #pragma unroll
     for (int jj = 0; jj < kG; ++jj)
-      if ((use >> jj) & 1) acc = acc + s_fold[base + jj][lane];
+      if ((use >> jj) & 1) acc = acc + s_fold[jj * kFoldCols + lane];
   }
   __syncwarp(gm);  // s_fold is reused by the group's next vertex
   INSTR_CP(14, tG);
@@ -2270,7 +2287,7 @@ cudaError_t engine_attributes() {
     const void* fns[] = {reinterpret_cast<const void*>(&k_engine<0>), reinterpret_cast<const void*>(&k_engine<1>),
                          reinterpret_cast<const void*>(&k_engine<2>), reinterpret_cast<const void*>(&k_engine<3>)};
     for (const void* fn : fns) {
-      const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kFoldSmem);
+      const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem);
       if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
@@ -2288,7 +2305,7 @@ int coop_launch(const void* fn, int blocks, const DevMesh& m, const DevField& f,
   const cudaError_t ea = engine_attributes();
   if (ea != cudaSuccess) return static_cast<int>(ea);
   note_launch();
-  return static_cast<int>(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kBlock), args, kFoldSmem,
+  return static_cast<int>(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kBlock), args, kDynSmem,
                                                       static_cast<cudaStream_t>(stream)));
 }
 
@@ -2306,10 +2323,10 @@ int dev_max_coresident_blocks(int* out) {
   if (e != cudaSuccess) return static_cast<int>(e);
   e = engine_attributes();
   if (e != cudaSuccess) return static_cast<int>(e);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_engine<0>, kBlock, kFoldSmem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_engine<0>, kBlock, kDynSmem);
   if (e != cudaSuccess) return static_cast<int>(e);
   int per1 = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k_engine<1>, kBlock, kFoldSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, k_engine<1>, kBlock, kDynSmem);
   if (per1 < per) per = per1;
   *out = sms * (per < 1 ? 1 : per);
   return 0;
@@ -2353,7 +2370,7 @@ int launch_check(const DevMesh& m, const DevField& f, const DevWork& w, const St
 int launch_snap(const DevMesh& m, const DevField& f, const DevWork& w, const StepParams& p, void* stream) {
   if (const cudaError_t ea = engine_attributes(); ea != cudaSuccess) return static_cast<int>(ea);
   note_launch();
-  k_engine<2><<<148 * 4, kBlock, kFoldSmem, static_cast<cudaStream_t>(stream)>>>(m, f, w, p);
+  k_engine<2><<<148 * 4, kBlock, kDynSmem, static_cast<cudaStream_t>(stream)>>>(m, f, w, p);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -2362,7 +2379,7 @@ int launch_flush(const DevMesh& m, const DevField& f, const DevWork& w, const St
   if (blocks == 0) return 0;
   if (const cudaError_t ea = engine_attributes(); ea != cudaSuccess) return static_cast<int>(ea);
   note_launch();
-  k_engine<3><<<blocks, kBlock, kFoldSmem, static_cast<cudaStream_t>(stream)>>>(m, f, w, p);
+  k_engine<3><<<blocks, kBlock, kDynSmem, static_cast<cudaStream_t>(stream)>>>(m, f, w, p);
   return static_cast<int>(cudaGetLastError());
 }
 
