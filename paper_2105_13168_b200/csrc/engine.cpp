@@ -369,6 +369,7 @@ DeviceLaplacian::DeviceLaplacian(std::shared_ptr<DeviceMesh> dm, cudaStream_t s)
   if (rc == -1) fail(kDegeneracyError, "non-finite cotangent weight");
   ck(rc, "laplacian assembly");
   nnz_ = to_host(dnnz, 1, s)[0];
+  build_ell(s);
   std::vector<double> g = to_host(grow, nv, s);
   gersh_ = 0;
   for (double r : g) gersh_ = std::max(gersh_, r);
@@ -389,6 +390,7 @@ DeviceLaplacian::DeviceLaplacian(std::shared_ptr<DeviceMesh> dm, const std::vect
   val.upload(v.data(), v.size(), s);
   mass.alloc(nv);
   mass.upload(ms.data(), nv, s);
+  build_ell(s);
   cuda_check(cudaStreamSynchronize(s), "operator upload");
 }
 
@@ -416,7 +418,18 @@ DevMesh DeviceLaplacian::view() const {
   v.s_col = col.p;
   v.s_val = val.p;
   v.mass = mass.p;
+  v.e_len = e_len.p;
+  v.e_col = e_col.p;
+  v.e_val = e_val.p;
   return v;
+}
+
+void DeviceLaplacian::build_ell(cudaStream_t s) {
+  const size_t nv = dm_->nv();
+  e_len.alloc(nv);
+  e_col.alloc(nv * kEll);
+  e_val.alloc(nv * kEll);
+  ck(launch_ell(static_cast<int>(nv), off.p, col.p, val.p, e_len.p, e_col.p, e_val.p, s), "padded rows");
 }
 
 double stable_time_step(const DeviceLaplacian& op, const Coefficients& c) {

@@ -131,9 +131,13 @@ class DeviceLaplacian {
   void apply(const double* x_host, double* y_host, cudaStream_t s) const;
   std::shared_ptr<DeviceMesh> mesh() const { return dm_; }
   DevMesh view() const;
+  void build_ell(cudaStream_t s);
 
   DevBuf<int> off, col;
   DevBuf<double> val, mass;
+  DevBuf<unsigned char> e_len;  // padded rows (DevMesh::e_len)
+  DevBuf<int> e_col;
+  DevBuf<double> e_val;
 
  private:
   std::shared_ptr<DeviceMesh> dm_;

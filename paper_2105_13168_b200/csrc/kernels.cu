@@ -641,16 +641,15 @@ __device__ bool update_vertex_single(const DevMesh& M, const DevField& F, const 
   const size_t vb = static_cast<size_t>(v) * kSlots;
   const unsigned own_lw = *reinterpret_cast<const unsigned*>(F.lay + vb);  // slots 0, 1
   const double2 own_x = *reinterpret_cast<const double2*>(F.val + vb);
-  const int k0 = __ldg(M.s_off + v), k1 = __ldg(M.s_off + v + 1);
   const double mass = __ldg(M.mass + v);
-  const int k = k0 + lane;
-  const bool valid = k < k1;
-  int u = 0;
-  double s = 0.0;
-  if (valid) {
-    u = __ldg(M.s_col + k);
-    s = __ldg(M.s_val + k);
-  }
+  // The padded row: lane j's entry is one load away from v.
+  const int rlen = __ldg(M.e_len + v);
+  const int u_e = __ldg(M.e_col + static_cast<size_t>(v) * kEll + lane);
+  const double s_e = __ldg(M.e_val + static_cast<size_t>(v) * kEll + lane);
+  const bool valid = lane < rlen;
+  const int u = valid ? u_e : 0;
+  const double s = valid ? s_e : 0.0;
+  const int k0 = 0, k1 = rlen;
   const size_t ub = static_cast<size_t>(u) * kSlots;
   const int cu = valid ? static_cast<int>(F.cnt[u]) : 0;
   const unsigned nlw = valid ? *reinterpret_cast<const unsigned*>(F.lay + ub) : 0u;
@@ -1313,13 +1312,14 @@ __device__ void commit_vertex(const DevMesh& M, const DevField& F, const DevWork
   const int nn = W.scnt[i];
   const unsigned short sl = W.slay[o + lane];
   const double sx = W.sval[o + lane];
-  const int k0 = __ldg(M.s_off + v), k1 = __ldg(M.s_off + v + 1);
+  const int rlen = __ldg(M.e_len + v);  // the one-ring from the padded row: no s_off round trip
+  const int ue = lane >= 1 ? __ldg(M.e_col + static_cast<size_t>(v) * kEll + lane - 1) : v;
   const unsigned char listed = W.in_list[v];
   const uint4 old_bi = F.binfo[v];  // band layers before this commit (change tracking)
   if (!(flag & 1)) return;
   INSTR_CP(4, tB);
   const int t0 = lane;  // first row entry of this lane: t = 0 is v itself
-  const int u0 = t0 == 0 ? v : (t0 <= k1 - k0 ? __ldg(M.s_col + k0 + t0 - 1) : -1);
+  const int u0 = t0 == 0 ? v : (t0 <= rlen ? ue : -1);
   bool inter = false;
   if (lane < nn) {
     F.lay[d + lane] = sl;
@@ -1395,7 +1395,9 @@ __device__ void commit_vertex(const DevMesh& M, const DevField& F, const DevWork
   }
   INSTR_CP(5, tB);
   if (u0 >= 0) queue_region(W, u0, stamp, nxt, Q);
-  for (int t = lane + kG; t <= k1 - k0; t += kG) queue_region(W, __ldg(M.s_col + k0 + t - 1), stamp, nxt, Q);
+  for (int t = lane + kG; t <= rlen; t += kG)  // entries past the group: padded row, then the CSR
+    queue_region(W, t - 1 < kEll ? __ldg(M.e_col + static_cast<size_t>(v) * kEll + t - 1) : __ldg(M.s_col + __ldg(M.s_off + v) + t - 1),
+                 stamp, nxt, Q);
   INSTR_CP(7, tB);
 }
 

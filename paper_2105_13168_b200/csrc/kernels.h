@@ -74,6 +74,7 @@ constexpr int kMaxActive = 4096;   // simultaneously active non-base layers
 constexpr int kPairCap = 1 << 16;  // collision pair hash table slots
 constexpr int kTrailCap = 1 << 20; // device trail ring capacity (records)
 constexpr int kBlock = 512;        // threads per CTA for all engine kernels
+constexpr int kEll = 8;            // padded stiffness row width (= 8-lane group)
 
 // Error codes raised by device code (mirrored in mesh.hpp ErrorCode).
 enum DevError : int {
@@ -103,6 +104,11 @@ struct DevMesh {
   const unsigned *edges = nullptr;                                // 2 * ne (lo, hi)
   const int *s_off = nullptr, *s_col = nullptr;                   // stiffness CSR
   const double *s_val = nullptr, *mass = nullptr;
+  // The same rows padded to kEll entries per vertex (columns -1 past the end;
+  // e_len > kEll: use the CSR), so a row is one load away from the vertex id.
+  const unsigned char* e_len = nullptr;
+  const int* e_col = nullptr;
+  const double* e_val = nullptr;
   const int *c_off = nullptr, *c_col = nullptr;                   // front connectivity
   const int *n_off = nullptr, *n_col = nullptr;                   // mesh neighbours
 };
@@ -268,6 +274,8 @@ void* dev_alloc(size_t bytes);
 void dev_free(void* p, size_t bytes);
 int launch_front_count(const FrontBuild& b, int* c_off, int* nnz, void* stream);
 int launch_front_fill(const FrontBuild& b, const int* c_off, int* c_col, void* stream);
+int launch_ell(int nv, const int* off, const int* col, const double* val, unsigned char* e_len, int* e_col,
+               double* e_val, void* stream);
 int launch_spmv(int nv, const int* off, const int* col, const double* val, const double* mass,
                 const double* x, double* y, void* stream);
 

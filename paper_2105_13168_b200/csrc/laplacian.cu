@@ -166,6 +166,28 @@ int launch_assemble(const LapBuild& b, void* stream) {
   return hbad ? -1 : 0;
 }
 
+namespace {
+__global__ void k_ell(int nv, const int* off, const int* col, const double* val, unsigned char* e_len, int* e_col,
+                      double* e_val) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  const int k0 = off[v], n = off[v + 1] - k0;
+  e_len[v] = static_cast<unsigned char>(n > 255 ? 255 : n);
+  for (int j = 0; j < kEll; ++j) {
+    const bool ok = j < n;
+    e_col[static_cast<size_t>(v) * kEll + j] = ok ? col[k0 + j] : -1;
+    e_val[static_cast<size_t>(v) * kEll + j] = ok ? val[k0 + j] : 0.0;
+  }
+}
+}  // namespace
+
+int launch_ell(int nv, const int* off, const int* col, const double* val, unsigned char* e_len, int* e_col,
+               double* e_val, void* stream) {
+  k_ell<<<(nv + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(nv, off, col, val, e_len, e_col, e_val);
+  note_launch();
+  return static_cast<int>(cudaGetLastError());
+}
+
 int launch_spmv(int nv, const int* off, const int* col, const double* val, const double* mass, const double* x,
                 double* y, void* stream) {
   const int threads = 256;
