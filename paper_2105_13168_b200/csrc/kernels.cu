@@ -689,14 +689,16 @@ __device__ bool update_vertex_single(const DevMesh& M, const DevField& F, const 
       xl = nx.y;
     }
   }
-  if (__any_sync(gm, bad)) return false;
+  // Activity of the non-base layers, looked up as soon as each is known
+  // (not after the group agrees on L, which would add a dependent round).
+  const bool act_ok = (ol == 0 || W.active[ol]) && (nl == 0 || W.active[nl]);
+  if (__any_sync(gm, bad || !act_ok)) return false;
   // One common non-base layer L across v and its neighbours.
   const unsigned lo = __reduce_min_sync(gm, min(nl ? nl : 0xFFFFFFFFu, ol ? ol : 0xFFFFFFFFu));
   const unsigned hi = __reduce_max_sync(gm, max(nl, ol));
   const bool has_l = lo != 0xFFFFFFFFu;
   if (has_l && lo != hi) return false;
   const unsigned L = has_l ? lo : 0u;
-  if (has_l && !W.active[L]) return false;
   // Ordered folds of s_j * bu_j and s_j * x_j(L) (au_j) over the row.
   const double tb = s * bu, tt = s * xl;
   const bool bpos = valid && bu > 0.0;
