@@ -605,6 +605,7 @@ void DeviceField::setup() {
   cnt.alloc(nv);
   interest.alloc(nv);
   scnt.alloc(nv);
+  sbinfo.alloc(nv);
   sflag.alloc(nv);
   lay.alloc(nv * kSlots);
   slay.alloc(nv * kSlots);
@@ -643,6 +644,7 @@ void DeviceField::setup() {
   work_.region[1] = region1.p;
   work_.stamp = stamp.p;
   work_.scnt = scnt.p;
+  work_.sbinfo = sbinfo.p;
   work_.slay = slay.p;
   work_.sval = sval.p;
   work_.sflag = sflag.p;

@@ -263,6 +263,7 @@ class DeviceField {
 
   // storage
   DevBuf<unsigned char> cnt, interest, scnt, sflag, active, in_list;
+  DevBuf<uint4> sbinfo;  // band index of each scratch column (computed by the update)
   DevBuf<unsigned short> lay, slay;
   DevBuf<double> val, sval, lastpos;
   DevBuf<int> region0, region1, stamp, ilist0, ilist1, aidx, alist;

@@ -247,6 +247,45 @@ __device__ __forceinline__ void cand_add(unsigned short* cl, double* ca, int& nc
   ca[c] = ca[c] + t;
 }
 
+// The committed column's band index and interest flag, computed where the
+// column is produced (so phase B only copies them): make_binfo's definition
+// over the new entries, interest = some value strictly inside (0, 1).
+// NMAX > 0: register arrays of that capacity (fully unrolled, constant
+// indices); NMAX == 0: pointers into shared memory.
+template <int NMAX, class LT, class XT>
+__device__ __forceinline__ void scratch_header(const DevWork& W, int i, int n, const LT& lay, const XT& val, bool changed,
+                                               bool old_one, bool new_one) {
+  unsigned L[4] = {0, 0, 0, 0}, S[4] = {0, 0, 0, 0};
+  int nb = 0;
+  bool over = false, inter = false;
+#pragma unroll
+  for (int j = 0; j < (NMAX > 0 ? NMAX : kWork); ++j) {
+    if (j >= n) break;
+    const unsigned l = static_cast<unsigned>(lay[j]);
+    const double x = val[j];
+    inter |= x > 0.0 && x < 1.0;
+    if (l != 0 && x > W.band_lo && x < W.sat) {
+      if (nb < 4) {
+        L[nb] = l;
+        S[nb] = static_cast<unsigned>(j);
+        ++nb;
+      } else {
+        over = true;
+      }
+    }
+  }
+  uint4 bi = make_uint4(0, 0, 0, 0);
+  if (inter) {
+    bi.x = L[0] | (L[1] << 16);
+    bi.y = L[2] | (L[3] << 16);
+    bi.z = S[0] | (S[1] << 16);
+    bi.w = S[2] | ((over ? kBandOverflow : S[3]) << 16);
+  }
+  W.sbinfo[i] = bi;
+  W.scnt[i] = static_cast<unsigned char>(n);
+  W.sflag[i] = static_cast<unsigned char>((changed ? 1 : 0) | (old_one ? 2 : 0) | (new_one ? 4 : 0) | (inter ? 8 : 0));
+}
+
 __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P,
                               int i, int v, bool spec, int lane, unsigned gm) {
   // Work arrays in the group's shared-memory slab.  Every lane of the group
@@ -442,8 +481,7 @@ __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork
     W.slay[o + j] = nl[j];
     W.sval[o + j] = nx[j];
   }
-  W.scnt[i] = static_cast<unsigned char>(nn);
-  W.sflag[i] = static_cast<unsigned char>((changed ? 1 : 0) | (old_one ? 2 : 0) | (new_one ? 4 : 0));
+  scratch_header<0>(W, i, nn, nl, nx, changed, old_one, new_one);
 }
 
 // ---------------------------------------------------------------------------
@@ -847,8 +885,21 @@ __device__ bool update_vertex_single(const DevMesh& M, const DevField& F, const 
     W.sval[o + lane] = lane == 0 ? Ex[0] : Ex[1];
   }
   if (lane == 0) {
+    // Header of a column of at most [base, L]: one band entry at most.
+    const bool in0 = n > 0 && Ex[0] > 0.0 && Ex[0] < 1.0, in1 = n > 1 && Ex[1] > 0.0 && Ex[1] < 1.0;
+    const bool inter = in0 || in1;
+    const int bj = (n > 0 && El[0] != 0 && Ex[0] > W.band_lo && Ex[0] < W.sat)
+                       ? 0
+                       : ((n > 1 && El[1] != 0 && Ex[1] > W.band_lo && Ex[1] < W.sat) ? 1 : -1);
+    uint4 bi = make_uint4(0, 0, 0, 0);
+    if (inter && bj >= 0) {
+      bi.x = bj == 0 ? El[0] : El[1];
+      bi.z = static_cast<unsigned>(bj);
+    }
+    W.sbinfo[i] = bi;
     W.scnt[i] = static_cast<unsigned char>(n);
-    W.sflag[i] = static_cast<unsigned char>((changed ? 1 : 0) | (old_one ? 2 : 0) | (new_one ? 4 : 0));
+    W.sflag[i] =
+        static_cast<unsigned char>((changed ? 1 : 0) | (old_one ? 2 : 0) | (new_one ? 4 : 0) | (inter ? 8 : 0));
   }
   return true;
 }
@@ -1210,10 +1261,7 @@ __device__ bool update_vertex_fast(const DevMesh& M, const DevField& F, const De
       W.slay[o + j] = static_cast<unsigned short>(El[j]);
       W.sval[o + j] = Ex[j];
     }
-  if (lane == 0) {
-    W.scnt[i] = static_cast<unsigned char>(n);
-    W.sflag[i] = static_cast<unsigned char>((changed ? 1 : 0) | (old_one ? 2 : 0) | (new_one ? 4 : 0));
-  }
+  if (lane == 0) scratch_header<kN>(W, i, n, El, Ex, changed, old_one, new_one);
   return true;
 }
 
@@ -1318,46 +1366,22 @@ __device__ void commit_vertex(const DevMesh& M, const DevField& F, const DevWork
   const int ue = lane >= 1 ? __ldg(M.e_col + static_cast<size_t>(v) * kEll + lane - 1) : v;
   const unsigned char listed = W.in_list[v];
   const uint4 old_bi = F.binfo[v];  // band layers before this commit (change tracking)
+  const uint4 bi = W.sbinfo[i];     // the new column's band index (computed by the update)
   if (!(flag & 1)) return;
   INSTR_CP(4, tB);
   const int t0 = lane;  // first row entry of this lane: t = 0 is v itself
   const int u0 = t0 == 0 ? v : (t0 <= rlen ? ue : -1);
-  bool inter = false;
+  // Claim the one-ring for frontier s+1 now; the exchange's round trip
+  // overlaps the column writes below.
+  const bool first = u0 >= 0 && atomicExch(W.stamp + u0, stamp) != stamp;
+  const bool inter = (flag & 8) != 0;
   if (lane < nn) {
     F.lay[d + lane] = sl;
     F.val[d + lane] = sx;
-    inter = sx > 0.0 && sx < 1.0;
   }
   for (int j = lane + kG; j < nn; j += kG) {  // columns longer than kG (slow-path results)
-    const double x = W.sval[o + j];
     F.lay[d + j] = W.slay[o + j];
-    F.val[d + j] = x;
-    inter |= (x > 0.0 && x < 1.0);
-  }
-  inter = __ballot_sync(gm, inter) != 0;
-  // Band index from the lanes' slots (make_binfo's definition) when the
-  // column fits the group; longer columns rescan scratch.
-  uint4 bi = make_uint4(0, 0, 0, 0);
-  if (inter) {
-    if (nn <= kG) {
-      const bool bd = lane < nn && sl != 0 && sx > W.band_lo && sx < W.sat;
-      const unsigned bm = (__ballot_sync(gm, bd) >> (threadIdx.x & 24)) & 0xFFu;
-      unsigned L[4], S[4], rest = bm;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int src = rest ? __ffs(rest) - 1 : 0;
-        const unsigned l = __shfl_sync(gm, static_cast<unsigned>(sl), src, kG);
-        L[t] = rest ? l : 0;
-        S[t] = rest ? static_cast<unsigned>(src) : 0;
-        rest &= rest - 1;
-      }
-      bi.x = L[0] | (L[1] << 16);
-      bi.y = L[2] | (L[3] << 16);
-      bi.z = S[0] | (S[1] << 16);
-      bi.w = S[2] | ((rest ? kBandOverflow : S[3]) << 16);
-    } else if (lane == 0) {
-      bi = make_binfo(W.slay + o, W.sval + o, nn, W.band_lo, W.sat);
-    }
+    F.val[d + j] = W.sval[o + j];
   }
   if (lane == 0) {
     // Band-item changes for the split certificate of phase D (see
@@ -1396,7 +1420,7 @@ __device__ void commit_vertex(const DevMesh& M, const DevField& F, const DevWork
     if (delta) atomicAdd(&W.ctl->base_one, delta);
   }
   INSTR_CP(5, tB);
-  if (u0 >= 0) queue_region(W, u0, stamp, nxt, Q);
+  if (first) bq_push(Q, &W.ctl->rcount[nxt], W.region[nxt], u0);
   for (int t = lane + kG; t <= rlen; t += kG)  // entries past the group: padded row, then the CSR
     queue_region(W, t - 1 < kEll ? __ldg(M.e_col + static_cast<size_t>(v) * kEll + t - 1) : __ldg(M.s_col + __ldg(M.s_off + v) + t - 1),
                  stamp, nxt, Q);

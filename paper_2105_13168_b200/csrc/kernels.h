@@ -172,7 +172,8 @@ struct DevWork {
   unsigned char *scnt = nullptr;        // scratch columns per region slot
   unsigned short *slay = nullptr;
   double *sval = nullptr;
-  unsigned char *sflag = nullptr;
+  unsigned char *sflag = nullptr;         // bit 0 changed, 1 old base==1, 2 new base==1, 3 interest
+  uint4 *sbinfo = nullptr;               // band index of each scratch column
   int *ilist[2] = {nullptr, nullptr};   // band lists (double buffer); dead entries skipped
   unsigned char *in_list = nullptr;     // vertex is in the current band list
   int2 *bandpairs = nullptr;            // (vertex, dense active index) band items of the last check
