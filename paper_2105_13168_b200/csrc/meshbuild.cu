@@ -105,6 +105,14 @@ __global__ void k_face_init(unsigned* p, int nf) {
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f < nf) p[f] = static_cast<unsigned>(f);
 }
+// Randomised linking (hash keys) keeps the trees shallow; linking by index
+// builds long chains on meshes whose faces are numbered along strips.
+__device__ __forceinline__ unsigned fkey(unsigned x) {
+  x *= 0x9E3779B1u;
+  x ^= x >> 15;
+  x *= 0x85EBCA77u;
+  return x ^ (x >> 13);
+}
 __global__ void k_face_union(const unsigned* partner, int ns, unsigned* p) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= ns) return;
@@ -114,12 +122,13 @@ __global__ void k_face_union(const unsigned* partner, int ns, unsigned* p) {
     a = froot(p, a);
     b = froot(p, b);
     if (a == b) return;
-    if (a < b) {
+    const unsigned ka = fkey(a), kb = fkey(b);
+    if (ka < kb || (ka == kb && a < b)) {  // hook the smaller key under the larger
       const unsigned t = a;
       a = b;
       b = t;
     }
-    if (atomicCAS(p + a, a, b) == a) return;
+    if (atomicCAS(p + b, b, a) == b) return;
   }
 }
 __global__ void k_face_roots(const unsigned* p, int nf, int* nroots) {
