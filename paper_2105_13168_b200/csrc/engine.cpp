@@ -364,15 +364,15 @@ DeviceLaplacian::DeviceLaplacian(std::shared_ptr<DeviceMesh> dm, cudaStream_t s)
   b.s_val = val.p;
   b.mass = mass.p;
   b.gersh_row = grow.p;
+  DevBuf<double> gmax(1);
+  b.gersh_max = gmax.p;
   b.nnz = dnnz.p;
   const int rc = launch_assemble(b, s);
   if (rc == -1) fail(kDegeneracyError, "non-finite cotangent weight");
   ck(rc, "laplacian assembly");
   nnz_ = to_host(dnnz, 1, s)[0];
   build_ell(s);
-  std::vector<double> g = to_host(grow, nv, s);
-  gersh_ = 0;
-  for (double r : g) gersh_ = std::max(gersh_, r);
+  gersh_ = std::max(0.0, to_host(gmax, 1, s)[0]);
 }
 
 DeviceLaplacian::DeviceLaplacian(std::shared_ptr<DeviceMesh> dm, const std::vector<int>& o, const std::vector<int>& c,

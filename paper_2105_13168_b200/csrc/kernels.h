@@ -240,7 +240,8 @@ struct LapBuild {
   int *s_col;                  // out: capacity nv + 2 * ne
   double *s_val;               // out
   double *mass;                // out
-  double *gersh_row;           // out: per-row bound (max reduced on host)
+  double *gersh_row;           // out: per-row bound
+  double *gersh_max;           // out: max over the rows (device scalar)
   int *nnz;                    // out
 };
 int launch_assemble(const LapBuild& b, void* stream);

@@ -154,9 +154,17 @@ int launch_assemble(const LapBuild& b, void* stream) {
   cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, b.s_off, b.nv + 1, s);
   k_row_fill<<<blocks, threads, 0, s>>>(b);
   cudaMemcpyAsync(b.nnz, b.s_off + b.nv, sizeof(int), cudaMemcpyDeviceToDevice, s);
+  // Gershgorin bound: max over the rows (exact in any order).
+  size_t red_bytes = 0;
+  cub::DeviceReduce::Max(nullptr, red_bytes, b.gersh_row, b.gersh_max, b.nv, s);
+  void* red = nullptr;
+  cudaMallocAsync(&red, red_bytes, s);
+  cub::DeviceReduce::Max(red, red_bytes, b.gersh_row, b.gersh_max, b.nv, s);
+  note_launch(1);
   int hbad = 0;
   cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
   cudaFreeAsync(tmp, s);
+  cudaFreeAsync(red, s);
   cudaFreeAsync(counts, s);
   cudaFreeAsync(bad, s);
   e = cudaStreamSynchronize(s);
