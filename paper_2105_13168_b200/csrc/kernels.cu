@@ -142,7 +142,8 @@ struct CtlSnap {
   int dchange[2];
   int nadded[2];
   int anchor_fail[2];
-  int pad_[2];
+  int nbandpairs;
+  int pad_;
 };
 static_assert(sizeof(CtlSnap) == 64, "CtlSnap mirrors the first 64 bytes of Ctl");
 __device__ __forceinline__ void ctl_snap(const Ctl* ctl, CtlSnap& sc) {
@@ -1644,8 +1645,7 @@ __device__ void block_stats_flush(BlockStats& S, LayerStat* g, int n_active, Ctl
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
-__device__ void flush_e_named(BlockStats& S, LayerStat* g, int n_active, Ctl* ctl, BlockQueue& Q, int* gc1, int* gl1,
-                              PairQueue& QB, int* gc2, int2* gl2, int cap2, int* ovf2, int nE) {
+__device__ void flush_e_named(BlockStats& S, LayerStat* g, int n_active, Ctl* ctl, int nE) {
   named_sync(1, nE);
   if (threadIdx.x == 0 && S.bmax) atomicMax(&ctl->base_max_bits, S.bmax);
   for (int a = threadIdx.x; a < n_active && a < kSmemLayers; a += nE) {
@@ -1657,20 +1657,6 @@ __device__ void flush_e_named(BlockStats& S, LayerStat* g, int n_active, Ctl* ct
         atomicAdd(reinterpret_cast<unsigned long long*>(c == 0 ? &g[a].sx : (c == 1 ? &g[a].sy : &g[a].sz)),
                   static_cast<unsigned long long>(S.sum[a][c]));
     if (S.snap[a] != ~0ull) atomicMin(&g[a].snap, S.snap[a]);
-  }
-  const int n1 = min(Q.n, kQCap), n2 = min(QB.n, kQCap);
-  if (threadIdx.x == 0) Q.base = n1 ? atomicAdd(gc1, n1) : 0;
-  if (threadIdx.x == (nE > 32 ? 32 : 1)) QB.base = n2 ? atomicAdd(gc2, n2) : 0;
-  named_sync(1, nE);
-  for (int i = threadIdx.x; i < n1; i += nE) gl1[Q.base + i] = Q.buf[i];
-  for (int i = threadIdx.x; i < n2; i += nE) {
-    if (QB.base + i < cap2) gl2[QB.base + i] = QB.buf[i];
-    else if (ovf2) *ovf2 = 1;
-  }
-  named_sync(1, nE);
-  if (threadIdx.x == 0) {  // read again only after the grid barrier that ends the phase
-    Q.n = 0;
-    QB.n = 0;
   }
 }
 
@@ -1780,8 +1766,18 @@ __device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& 
     const bool live = v >= 0 && inter_v;
     if (live) INSTR_CP(8, tE);
     if (compact) {
-      if (live) bq_push(Q, &W.ctl->ilcount[lpar ^ 1], W.ilist[lpar ^ 1], v);
-      else if (v >= 0) W.in_list[v] = 0;
+      // Survivors go straight to the next band list, one atomic per warp
+      // (the list's order does not matter), so no flush is left for the end
+      // of the phase.
+      const unsigned lm = __ballot_sync(0xffffffffu, live);
+      if (lm) {
+        const int leader = __ffs(lm) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(&W.ctl->ilcount[lpar ^ 1], __popc(lm));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (live) W.ilist[lpar ^ 1][base + __popc(lm & ((1u << lane) - 1u))] = v;
+      }
+      if (!live && v >= 0) W.in_list[v] = 0;
     }
     const int cv = live ? cnt_v : 0;
     const double base = (cv > 0 && L4[0] == 0) ? X4[0] : 0.0;
@@ -1832,8 +1828,21 @@ __device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& 
             // is stale (never linked this epoch) or points to itself.
             const unsigned item = static_cast<unsigned>(v) * kSlots + k;
             root = count_roots && ((pw >> 32) != ep || static_cast<unsigned>(pw) == item);
-            if (P.record_trails)
-              bq_push(QB, &W.ctl->nbandpairs, W.bandpairs, make_int2(v, a), W.bandpair_cap, &W.ctl->bandpair_overflow);
+
+          }
+        }
+      }
+      if (P.record_trails) {  // band items for the trail snap, one atomic per warp
+        const unsigned bm = __ballot_sync(0xffffffffu, band);
+        if (bm) {
+          const int leader = __ffs(bm) - 1;
+          int base = 0;
+          if (lane == leader) base = atomicAdd(&W.ctl->nbandpairs, __popc(bm));
+          base = __shfl_sync(0xffffffffu, base, leader);
+          const int pos = base + __popc(bm & ((1u << lane) - 1u));
+          if (band) {
+            if (pos < W.bandpair_cap) W.bandpairs[pos] = make_int2(v, a);
+            else W.ctl->bandpair_overflow = 1;
           }
         }
       }
@@ -1893,9 +1902,9 @@ __device__ __forceinline__ void band_mean(const DevMesh& M, const LayerStat& st,
 // vertex to the band mean; key = distance bits (27 low bits dropped) | vertex.
 // Items are spread round-robin over the CTAs from each CTA's last warp, so the
 // snap runs beside the commits of phase B (mapped from the first warps).
-__device__ void phase_snap(const DevMesh& M, const DevWork& W, int spar, BlockStats& S) {
+__device__ void phase_snap(const DevMesh& M, const DevWork& W, int spar, BlockStats& S, int nbandpairs) {
   LayerStat* g = W.stat + static_cast<size_t>(spar) * kMaxActive;
-  const int n = min(W.ctl->nbandpairs, W.bandpair_cap);
+  const int n = min(nbandpairs, W.bandpair_cap);
   const int lane = threadIdx.x & 31;
   const int stride = gridDim.x * blockDim.x;
   const int trip = (n + stride - 1) / stride;
@@ -2035,7 +2044,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
   if (kMode == 2) {
     const int spar = static_cast<int>(P.step_begin & 1);
     block_stats_init(S);
-    phase_snap(M, W, spar, S);
+    phase_snap(M, W, spar, S, W.ctl->nbandpairs);
     block_stats_flush(S, W.stat + static_cast<size_t>(spar) * kMaxActive, P.n_active);
     return;
   }
@@ -2096,7 +2105,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
                       group_mask(), Q);
         INSTR_REC(0, t0, (threadIdx.x & (kG - 1)) == 0);
       }
-      if (pend && P.record_trails) phase_snap(M, W, static_cast<int>(pend_step & 1), S);
+      if (pend && P.record_trails) phase_snap(M, W, static_cast<int>(pend_step & 1), S, SC.nbandpairs);
       bq_flush(Q, &ctl->rcount[nxt], W.region[nxt]);
       block_stats_flush(S, W.stat + static_cast<size_t>(pend_step & 1) * kMaxActive, pend ? P.n_active : 0);
       if (gtid == 0) {
@@ -2105,6 +2114,14 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
         ctl->dchange[nxt] = 0;  // the slot B(s+1) will fill; step s-1 is done with it
         ctl->nadded[nxt] = 0;
         ctl->anchor_fail[nxt] = 0;
+        // Outputs of E(s), appended while E runs: reset here, a barrier ahead.
+        // (This phase's trail snap reads the band pairs of check s-1 through
+        // the snapshot's count.)
+        ctl->ilcount[lpar ^ 1] = 0;
+        ctl->npairs = 0;
+        ctl->pair_overflow = 0;
+        ctl->base_max_bits = 0;
+        ctl->nbandpairs = 0;
       }
     }
     block_done(W, step - (P.step_end - 64), 0);
@@ -2121,13 +2138,6 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
           for (int a = (threadIdx.x & 31) * gridDim.x + blockIdx.x; a < P.n_active; a += 32 * gridDim.x)
             flush_stat(M, W, P, a, static_cast<int>(pend_step & 1), pend_step, true);
       pend = false;
-      if (gtid == 0) {
-        ctl->ilcount[lpar ^ 1] = 0;
-        ctl->npairs = 0;
-        ctl->pair_overflow = 0;
-        ctl->base_max_bits = 0;
-        ctl->nbandpairs = 0;
-      }
       const int nband = SC.ilcount[lpar];
       const int nR1 = SC.rcount[nxt];  // final since B(s)
       if (gtid == 0) ctl->sum_interest += static_cast<unsigned long long>(nband);
@@ -2155,11 +2165,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       };
       // The CTA-level flushes of E (each a __syncthreads) come after A, so
       // the warps running A do not wait for the warps running E.
-      auto flush_e = [&] {
-        block_stats_flush(S, W.stat + static_cast<size_t>(spar) * kMaxActive, P.n_active, ctl);
-        bq_flush2(Q, &ctl->ilcount[lpar ^ 1], W.ilist[lpar ^ 1], QB, &ctl->nbandpairs, W.bandpairs, W.bandpair_cap,
-                  &ctl->bandpair_overflow);
-      };
+      auto flush_e = [&] { block_stats_flush(S, W.stat + static_cast<size_t>(spar) * kMaxActive, P.n_active, ctl); };
       if (skip) {
         // ---- 2+3: certificate, E(s) without roots, speculative A(s+1)
         block_start(W, step - (P.step_end - 64), 2);
@@ -2181,9 +2187,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
           const int warp = threadIdx.x >> 5;
           if (warp < e_warps) {
             phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, QB, nband, false);
-            flush_e_named(S, W.stat + static_cast<size_t>(spar) * kMaxActive, P.n_active, ctl, Q,
-                          &ctl->ilcount[lpar ^ 1], W.ilist[lpar ^ 1], QB, &ctl->nbandpairs, W.bandpairs,
-                          W.bandpair_cap, &ctl->bandpair_overflow, e_warps * 32);
+            flush_e_named(S, W.stat + static_cast<size_t>(spar) * kMaxActive, P.n_active, ctl, e_warps * 32);
           } else if (more) {
             run_a();
           }
@@ -2279,7 +2283,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
   if (stop == 0 && pend) {
     // Budget exhausted right after a quiet check: finish its trail records.
     block_stats_init(S);
-    if (P.record_trails) phase_snap(M, W, static_cast<int>(pend_step & 1), S);
+    if (P.record_trails) phase_snap(M, W, static_cast<int>(pend_step & 1), S, W.ctl->nbandpairs);
     block_stats_flush(S, W.stat + static_cast<size_t>(pend_step & 1) * kMaxActive, P.n_active);
     grid_sync(ctl);
     for (int a = gtid; a < P.n_active; a += gsz) flush_stat(M, W, P, a, static_cast<int>(pend_step & 1), pend_step, true);

@@ -124,13 +124,13 @@ struct Ctl {
   int dchange[2];            // by step parity: the step removed a band item (or overflowed a band index / list)
   int nadded[2];             // by step parity: band items added (W.added)
   int anchor_fail[2];        // by step parity: an added band item lacks a neighbour of the previous band
-  int pad_[2];
+  int nbandpairs;            // (vertex, layer) band items recorded by the last check
+  int pad_;
   int spec_error_vertex;
   int stop_bits;
   long long stop_step;       // last step executed by the kernel
   long long epoch;           // union-find / pair-set version
   int base_one;              // number of vertices whose base value is exactly 1.0
-  int nbandpairs;            // (vertex, layer) band items recorded by the last check
   unsigned long long base_max_bits;  // max base value in (0,1) (as ordered bits)
   int npairs;                // collision pairs recorded this check
   int pair_overflow;
