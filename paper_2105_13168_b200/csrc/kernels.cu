@@ -1611,7 +1611,8 @@ struct BlockStats {
   int cnt[kSmemLayers][3];  // ncomp, nband, nunsat
   long long sum[kSmemLayers][3];
   unsigned long long snap[kSmemLayers];
-  unsigned long long bmax;  // max base value in (0, 1), as ordered bits
+  unsigned long long bmax;               // max base value in (0, 1), as ordered bits
+  unsigned long long wbmax[kBlock / 32];  // per-warp maxima (each warp's leader owns its slot: no atomics)
 };
 
 __device__ void block_stats_init(BlockStats& S) {
@@ -1621,12 +1622,21 @@ __device__ void block_stats_init(BlockStats& S) {
     S.snap[i] = ~0ull;
   }
   if (threadIdx.x == 0) S.bmax = 0;
+  if (threadIdx.x < kBlock / 32) S.wbmax[threadIdx.x] = 0;
   __syncthreads();
+}
+__device__ __forceinline__ unsigned long long block_bmax(const BlockStats& S) {
+  unsigned long long m = S.bmax;
+  for (int w = 0; w < kBlock / 32; ++w) m = S.wbmax[w] > m ? S.wbmax[w] : m;
+  return m;
 }
 
 __device__ void block_stats_flush(BlockStats& S, LayerStat* g, int n_active, Ctl* ctl = nullptr) {
   __syncthreads();
-  if (ctl && threadIdx.x == 0 && S.bmax) atomicMax(&ctl->base_max_bits, S.bmax);
+  if (ctl && threadIdx.x == 0) {
+    const unsigned long long m = block_bmax(S);
+    if (m) atomicMax(&ctl->base_max_bits, m);
+  }
   for (int a = threadIdx.x; a < n_active && a < kSmemLayers; a += blockDim.x) {
     if (S.cnt[a][0]) atomicAdd(&g[a].ncomp, S.cnt[a][0]);
     if (S.cnt[a][1]) atomicAdd(&g[a].nband, S.cnt[a][1]);
@@ -1647,7 +1657,10 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 }
 __device__ void flush_e_named(BlockStats& S, LayerStat* g, int n_active, Ctl* ctl, int nE) {
   named_sync(1, nE);
-  if (threadIdx.x == 0 && S.bmax) atomicMax(&ctl->base_max_bits, S.bmax);
+  if (threadIdx.x == 0) {
+    const unsigned long long m = block_bmax(S);
+    if (m) atomicMax(&ctl->base_max_bits, m);
+  }
   for (int a = threadIdx.x; a < n_active && a < kSmemLayers; a += nE) {
     if (S.cnt[a][0]) atomicAdd(&g[a].ncomp, S.cnt[a][0]);
     if (S.cnt[a][1]) atomicAdd(&g[a].nband, S.cnt[a][1]);
@@ -1787,12 +1800,16 @@ __device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& 
       if (m) {
         const unsigned long long bm =
             seg_max_u64(0xffffffffu, has ? static_cast<unsigned long long>(__double_as_longlong(base)) : 0ull);
-        if (lane == __ffs(m) - 1) atomicMax(&S.bmax, bm);
+        if (lane == __ffs(m) - 1) {
+          unsigned long long& slot = S.wbmax[threadIdx.x >> 5];
+          slot = bm > slot ? bm : slot;
+        }
       }
     }
     const long long px = live ? fxv : 0, py = live ? fyv : 0, pz = live ? fzv : 0;
     if (live) INSTR_CP(9, tE);
     bool cand = false;
+    int nkappa = 0;  // active layers at or above the collision threshold
     // The base owner (layer 0, always slot 0) contributes nothing below, so
     // lanes walk their non-base slots only: one round for a single front.
     const int kb = (cv > 0 && L4[0] == 0) ? 1 : 0;
@@ -1822,6 +1839,7 @@ __device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& 
           a = W.aidx[l];
           unsat = x > 0.0 && x < 1.0;
           if (unsat && x >= P.kappa) cand = true;
+          if (x >= P.kappa) ++nkappa;
           band = x > P.band_lo && x < P.sat;
           if (band) {
             // Unions are complete, so an item is a root iff its parent entry
@@ -1876,7 +1894,7 @@ __device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& 
       }
     }
     if (live) INSTR_CP(10, tE);
-    if (cand && !(base > P.coll_base_limit)) {
+    if (cand && nkappa >= 2 && !(base > P.coll_base_limit)) {  // a pair needs two such layers
       int first = -1;
       for (int k = 0; k < cv; ++k) {
         const int l = F.lay[b + k];
