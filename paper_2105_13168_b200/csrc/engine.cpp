@@ -597,6 +597,10 @@ std::shared_ptr<DeviceField> DeviceMesh::acquire_field(cudaStream_t s) {
     }
   });
 }
+namespace {
+int engine_blocks(int nv);
+}  // namespace
+
 
 void DeviceField::setup() {
   const size_t nv = dm_->nv();
@@ -617,7 +621,19 @@ void DeviceField::setup() {
   ilist0.alloc(nv);
   ilist1.alloc(nv);
   in_list.alloc(nv);
-  bandpairs.alloc(2 * nv + 4096);
+  {
+    // Trail-snap band items: one segment per engine CTA (twice the CTA's
+    // share of the vertices) plus a shared overflow list.
+    const size_t nseg = static_cast<size_t>(engine_blocks(static_cast<int>(nv)));
+    size_t seg = 2 * ((nv + nseg - 1) / nseg) + 64;
+    if (const char* env = std::getenv("DTB_BP_SEG")) seg = static_cast<size_t>(std::max(1, std::atoi(env)));  // tests
+    bandpairs.alloc(nseg * seg);
+    bpcount.alloc(nseg);
+    bp_ovf.alloc(2 * nv + 4096);
+    bpcount.zero(s_);
+    work_.bp_nseg = static_cast<int>(nseg);
+    work_.bp_seg = static_cast<int>(seg);
+  }
   parent.alloc(nv * kSlots);
   added.alloc(2 * (nv / 8 + 4096));  // two step-parity halves
   add_stamp.alloc(nv);
@@ -652,7 +668,9 @@ void DeviceField::setup() {
   work_.ilist[1] = ilist1.p;
   work_.in_list = in_list.p;
   work_.bandpairs = bandpairs.p;
-  work_.bandpair_cap = static_cast<int>(bandpairs.n);
+  work_.bpcount = bpcount.p;
+  work_.bp_ovf = bp_ovf.p;
+  work_.bandpair_cap = static_cast<int>(bp_ovf.n);
   binfo.alloc(nv);
   view_.binfo = binfo.p;
   // Event-time scratch (layer pulls, isoline crossings, edits): allocated once

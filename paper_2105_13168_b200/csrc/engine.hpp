@@ -267,7 +267,8 @@ class DeviceField {
   DevBuf<unsigned short> lay, slay;
   DevBuf<double> val, sval, lastpos;
   DevBuf<int> region0, region1, stamp, ilist0, ilist1, aidx, alist;
-  DevBuf<int2> bandpairs;
+  DevBuf<int2> bandpairs, bp_ovf;
+  DevBuf<int> bpcount;
   DevBuf<int> ai0, ai1, acnt;       // event-time scratch (see setup())
   DevBuf<double> ad0, ad1, ad2;
   DevBuf<uint4> binfo;

@@ -1291,7 +1291,6 @@ struct BlockQueueT {
   T buf[kQCap];
 };
 using BlockQueue = BlockQueueT<int>;
-using PairQueue = BlockQueueT<int2>;
 
 template <class T>
 __device__ __forceinline__ void bq_push(BlockQueueT<T>& q, int* gcount, T* glist, T item, int cap = 0x7fffffff,
@@ -1318,29 +1317,6 @@ __device__ void bq_flush(BlockQueueT<T>& q, int* gcount, T* glist, int cap = 0x7
   }
   __syncthreads();
   if (threadIdx.x == 0) q.n = 0;
-  __syncthreads();
-}
-
-// Two block queues flushed together: their global ranges are reserved by two
-// threads at once, so the CTA waits for one atomic round trip, not two.
-template <class T1, class T2>
-__device__ void bq_flush2(BlockQueueT<T1>& q1, int* gcount1, T1* glist1, BlockQueueT<T2>& q2, int* gcount2, T2* glist2,
-                          int cap2, int* overflow2) {
-  __syncthreads();
-  const int n1 = min(q1.n, kQCap), n2 = min(q2.n, kQCap);
-  if (threadIdx.x == 0) q1.base = n1 ? atomicAdd(gcount1, n1) : 0;
-  if (threadIdx.x == 32) q2.base = n2 ? atomicAdd(gcount2, n2) : 0;
-  __syncthreads();
-  for (int i = threadIdx.x; i < n1; i += blockDim.x) glist1[q1.base + i] = q1.buf[i];
-  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-    if (q2.base + i < cap2) glist2[q2.base + i] = q2.buf[i];
-    else if (overflow2) *overflow2 = 1;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    q1.n = 0;
-    q2.n = 0;
-  }
   __syncthreads();
 }
 
@@ -1613,6 +1589,7 @@ struct BlockStats {
   unsigned long long snap[kSmemLayers];
   unsigned long long bmax;               // max base value in (0, 1), as ordered bits
   unsigned long long wbmax[kBlock / 32];  // per-warp maxima (each warp's leader owns its slot: no atomics)
+  int nbp;                                // band items appended to this CTA's segment
 };
 
 __device__ void block_stats_init(BlockStats& S) {
@@ -1621,7 +1598,10 @@ __device__ void block_stats_init(BlockStats& S) {
     S.sum[i][0] = S.sum[i][1] = S.sum[i][2] = 0;
     S.snap[i] = ~0ull;
   }
-  if (threadIdx.x == 0) S.bmax = 0;
+  if (threadIdx.x == 0) {
+    S.bmax = 0;
+    S.nbp = 0;
+  }
   if (threadIdx.x < kBlock / 32) S.wbmax[threadIdx.x] = 0;
   __syncthreads();
 }
@@ -1631,11 +1611,21 @@ __device__ __forceinline__ unsigned long long block_bmax(const BlockStats& S) {
   return m;
 }
 
-__device__ void block_stats_flush(BlockStats& S, LayerStat* g, int n_active, Ctl* ctl = nullptr) {
+// Length of this CTA's band-item segment (E's flush); CTA 0 clears the
+// segments of CTAs beyond the grid.
+__device__ __forceinline__ void record_segment(const BlockStats& S, const DevWork& W) {
+  if (blockIdx.x < W.bp_nseg) W.bpcount[blockIdx.x] = min(S.nbp, W.bp_seg);
+  if (blockIdx.x == 0)
+    for (int c = gridDim.x; c < W.bp_nseg; ++c) W.bpcount[c] = 0;
+}
+
+__device__ void block_stats_flush(BlockStats& S, LayerStat* g, int n_active, Ctl* ctl = nullptr,
+                                  const DevWork* W = nullptr) {
   __syncthreads();
   if (ctl && threadIdx.x == 0) {
     const unsigned long long m = block_bmax(S);
     if (m) atomicMax(&ctl->base_max_bits, m);
+    if (W) record_segment(S, *W);
   }
   for (int a = threadIdx.x; a < n_active && a < kSmemLayers; a += blockDim.x) {
     if (S.cnt[a][0]) atomicAdd(&g[a].ncomp, S.cnt[a][0]);
@@ -1651,15 +1641,16 @@ __device__ void block_stats_flush(BlockStats& S, LayerStat* g, int n_active, Ctl
 
 // E's flush when E runs on warps of its own (the first nE threads): a named
 // barrier among those warps replaces __syncthreads, so the CTA's A warps
-// never wait for it.  Same effect as block_stats_flush + bq_flush2.
+// never wait for it.  Same effect as block_stats_flush.
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
-__device__ void flush_e_named(BlockStats& S, LayerStat* g, int n_active, Ctl* ctl, int nE) {
+__device__ void flush_e_named(BlockStats& S, LayerStat* g, int n_active, Ctl* ctl, const DevWork& W, int nE) {
   named_sync(1, nE);
   if (threadIdx.x == 0) {
     const unsigned long long m = block_bmax(S);
     if (m) atomicMax(&ctl->base_max_bits, m);
+    record_segment(S, W);
   }
   for (int a = threadIdx.x; a < n_active && a < kSmemLayers; a += nE) {
     if (S.cnt[a][0]) atomicAdd(&g[a].ncomp, S.cnt[a][0]);
@@ -1749,7 +1740,7 @@ __device__ void phase_roots(const DevField& F, const DevWork& W, const StepParam
 // vertex's slots in lock step so contributions can be combined per warp.
 __device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P, int lpar,
                             int spar, unsigned long long ep, bool compact, BlockStats& S, BlockQueue& Q,
-                            PairQueue& QB, int n, bool count_roots = true) {
+                            int n, bool count_roots = true) {
   LayerStat* g = W.stat + static_cast<size_t>(spar) * kMaxActive;
   const int* list = W.ilist[lpar];
   const int lane = threadIdx.x & 31;
@@ -1850,17 +1841,34 @@ __device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& 
           }
         }
       }
-      if (P.record_trails) {  // band items for the trail snap, one atomic per warp
+      if (P.record_trails) {
+        // Band items for the trail snap: appended to this CTA's segment with
+        // one shared-memory atomic per warp; the part of a batch that does
+        // not fit goes to the overflow list (one global atomic).
         const unsigned bm = __ballot_sync(0xffffffffu, band);
         if (bm) {
           const int leader = __ffs(bm) - 1;
           int base = 0;
-          if (lane == leader) base = atomicAdd(&W.ctl->nbandpairs, __popc(bm));
+          if (lane == leader) base = atomicAdd(&S.nbp, __popc(bm));
           base = __shfl_sync(0xffffffffu, base, leader);
           const int pos = base + __popc(bm & ((1u << lane) - 1u));
+          const int seg = blockIdx.x < W.bp_nseg ? W.bp_seg : 0;
+          int obase = 0;
+          unsigned om = 0;
+          if (base + __popc(bm) > seg) {
+            om = __ballot_sync(0xffffffffu, band && pos >= seg);
+            const int ol = __ffs(om) - 1;
+            if (lane == ol) obase = atomicAdd(&W.ctl->nbandpairs, __popc(om));
+            obase = __shfl_sync(0xffffffffu, obase, ol);
+          }
           if (band) {
-            if (pos < W.bandpair_cap) W.bandpairs[pos] = make_int2(v, a);
-            else W.ctl->bandpair_overflow = 1;
+            if (pos < seg) {
+              W.bandpairs[static_cast<size_t>(blockIdx.x) * W.bp_seg + pos] = make_int2(v, a);
+            } else {
+              const int o = obase + __popc(om & ((1u << lane) - 1u));
+              if (o < W.bandpair_cap) W.bp_ovf[o] = make_int2(v, a);
+              else W.ctl->bandpair_overflow = 1;
+            }
           }
         }
       }
@@ -1920,19 +1928,19 @@ __device__ __forceinline__ void band_mean(const DevMesh& M, const LayerStat& st,
 // vertex to the band mean; key = distance bits (27 low bits dropped) | vertex.
 // Items are spread round-robin over the CTAs from each CTA's last warp, so the
 // snap runs beside the commits of phase B (mapped from the first warps).
-__device__ void phase_snap(const DevMesh& M, const DevWork& W, int spar, BlockStats& S, int nbandpairs) {
-  LayerStat* g = W.stat + static_cast<size_t>(spar) * kMaxActive;
-  const int n = min(nbandpairs, W.bandpair_cap);
+// Trail snap of one list of band items: lane `rank` of `stride` walks it
+// (every lane runs the same number of rounds so the warp-level minimum is
+// well defined).
+__device__ void snap_list(const DevMesh& M, LayerStat* g, BlockStats& S, const int2* items, int n, int rank,
+                          int stride) {
   const int lane = threadIdx.x & 31;
-  const int stride = gridDim.x * blockDim.x;
   const int trip = (n + stride - 1) / stride;
   for (int r = 0; r < trip; ++r) {
-    const int i = r * stride + (static_cast<int>(blockDim.x) - 1 - static_cast<int>(threadIdx.x)) * gridDim.x +
-                  blockIdx.x;
+    const int i = r * stride + rank;
     int a = -1;
     unsigned long long key = ~0ull;
     if (i < n) {
-      const int2 bp = W.bandpairs[i];
+      const int2 bp = items[i];
       const int v = bp.x;
       a = bp.y;
       double mx, my, mz;
@@ -1948,6 +1956,19 @@ __device__ void phase_snap(const DevMesh& M, const DevWork& W, int spar, BlockSt
       else atomicMin(&g[a].snap, kmin);
     }
   }
+}
+
+// Trail snap over the band items of the last check: each CTA takes the
+// segments c = blockIdx.x (mod grid) -- in the engine its own -- and a
+// grid-strided share of the overflow list.  Threads are used from the last
+// warp down (the first warps run the commits beside it in phase B).
+__device__ void phase_snap(const DevMesh& M, const DevWork& W, int spar, BlockStats& S, int n_ovf) {
+  LayerStat* g = W.stat + static_cast<size_t>(spar) * kMaxActive;
+  const int rev = static_cast<int>(blockDim.x) - 1 - static_cast<int>(threadIdx.x);
+  for (int c = blockIdx.x; c < W.bp_nseg; c += gridDim.x)
+    snap_list(M, g, S, W.bandpairs + static_cast<size_t>(c) * W.bp_seg, min(W.bpcount[c], W.bp_seg), rev,
+              blockDim.x);
+  snap_list(M, g, S, W.bp_ovf, min(n_ovf, W.bandpair_cap), rev * gridDim.x + blockIdx.x, gridDim.x * blockDim.x);
 }
 
 __device__ void reset_stat(LayerStat* st) {
@@ -2019,12 +2040,10 @@ template <int kMode>
 __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, DevWork W, StepParams P) {
   __shared__ BlockStats S;
   __shared__ BlockQueue Q;
-  __shared__ PairQueue QB;
   __shared__ CtlSnap SC;
   Ctl* ctl = W.ctl;
   if (threadIdx.x == 0) {
     Q.n = 0;
-    QB.n = 0;
   }
 #ifdef DTB_INSTR
   for (int i = threadIdx.x; i < 6 * 16; i += blockDim.x) s_hist[i / 16][i % 16] = 0;
@@ -2052,9 +2071,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
     phase_union(M, F, W, P, lpar, ep, group_rank(P.map_mode & 8 ? 1 : 0), gsz / kG, SC.ilcount[lpar]);
     grid_sync_snap(ctl, SC);
     block_stats_init(S);
-    phase_stats(M, F, W, P, lpar, spar, ep, false, S, Q, QB, SC.ilcount[lpar]);
-    block_stats_flush(S, g, P.n_active, ctl);
-    bq_flush(QB, &ctl->nbandpairs, W.bandpairs, W.bandpair_cap, &ctl->bandpair_overflow);
+    phase_stats(M, F, W, P, lpar, spar, ep, false, S, Q, SC.ilcount[lpar]);
+    block_stats_flush(S, g, P.n_active, ctl, &W);
     grid_sync(ctl);
     if (gtid == 0) ctl->epoch = static_cast<long long>(ep);
     return;
@@ -2183,7 +2201,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       };
       // The CTA-level flushes of E (each a __syncthreads) come after A, so
       // the warps running A do not wait for the warps running E.
-      auto flush_e = [&] { block_stats_flush(S, W.stat + static_cast<size_t>(spar) * kMaxActive, P.n_active, ctl); };
+      auto flush_e = [&] { block_stats_flush(S, W.stat + static_cast<size_t>(spar) * kMaxActive, P.n_active, ctl, &W); };
       if (skip) {
         // ---- 2+3: certificate, E(s) without roots, speculative A(s+1)
         block_start(W, step - (P.step_end - 64), 2);
@@ -2204,14 +2222,14 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
         if (e_alone) {
           const int warp = threadIdx.x >> 5;
           if (warp < e_warps) {
-            phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, QB, nband, false);
-            flush_e_named(S, W.stat + static_cast<size_t>(spar) * kMaxActive, P.n_active, ctl, e_warps * 32);
+            phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, nband, false);
+            flush_e_named(S, W.stat + static_cast<size_t>(spar) * kMaxActive, P.n_active, ctl, W, e_warps * 32);
           } else if (more) {
             run_a();
           }
         } else {
           if (more) run_a();
-          phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, QB, nband, false);
+          phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, nband, false);
           flush_e();
         }
         block_done(W, step - (P.step_end - 64), 2);
@@ -2232,7 +2250,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
         block_start(W, step - (P.step_end - 64), 2);
         // ---- 3: E(s) + speculative A(s+1)
         block_stats_init(S);
-        phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, QB, nband, true);
+        phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, nband, true);
         if (!more || P.split_a) flush_e();
         if (more) {
           if (P.split_a) {

@@ -124,7 +124,7 @@ struct Ctl {
   int dchange[2];            // by step parity: the step removed a band item (or overflowed a band index / list)
   int nadded[2];             // by step parity: band items added (W.added)
   int anchor_fail[2];        // by step parity: an added band item lacks a neighbour of the previous band
-  int nbandpairs;            // (vertex, layer) band items recorded by the last check
+  int nbandpairs;            // band items of the last check in the overflow list
   int pad_;
   int spec_error_vertex;
   int stop_bits;
@@ -176,8 +176,15 @@ struct DevWork {
   uint4 *sbinfo = nullptr;               // band index of each scratch column
   int *ilist[2] = {nullptr, nullptr};   // band lists (double buffer); dead entries skipped
   unsigned char *in_list = nullptr;     // vertex is in the current band list
-  int2 *bandpairs = nullptr;            // (vertex, dense active index) band items of the last check
-  int bandpair_cap = 0;
+  // (vertex, dense active index) band items of the last check: one segment
+  // of bp_seg entries per CTA (appended with a shared-memory counter, length
+  // in bpcount[cta]), entries beyond a full segment in the shared overflow
+  // list bp_ovf (length Ctl::nbandpairs).
+  int2 *bandpairs = nullptr;
+  int *bpcount = nullptr;
+  int bp_nseg = 0, bp_seg = 0;
+  int2 *bp_ovf = nullptr;
+  int bandpair_cap = 0;                 // capacity of bp_ovf
   unsigned long long *parent = nullptr; // nv * kSlots versioned UF parents
   int2 *added = nullptr;                // 2 x added_cap band items (vertex, layer) gained, by step parity
   int added_cap = 0;

@@ -160,3 +160,22 @@ def test_split_certificate_matches_full_union_find(spec, steps, monkeypatch):
     full = dt.run_initial_pass(mesh, op, 0, cfg)
     assert [int(h) for h in fast.hashes()] == [int(h) for h in full.hashes()]
     assert [(e.kind, e.step, e.layers) for e in fast.events()] == [(e.kind, e.step, e.layers) for e in full.events()]
+
+
+@pytest.mark.parametrize("spec,steps", [("torus_irr:40:20:2:0.6:0.2:0.05:7", 800), ("genus:2:3", 600)])
+def test_trail_snap_overflow_list_matches_segments(spec, steps, monkeypatch):
+    """Band items for the trail snap go to per-CTA segments; a full segment
+    spills into the shared overflow list.  Tiny segments (DTB_BP_SEG=3) force
+    nearly every item through the overflow path: trails must not change."""
+    mesh = dt.TriangleMesh.generate(spec)
+    op = dt.assemble_laplacian(mesh)
+    cfg = dt.default_config(max_steps=steps, record_hashes=1)
+    a = dt.run_initial_pass(mesh, op, 0, cfg)
+    monkeypatch.setenv("DTB_BP_SEG", "3")
+    b = dt.run_initial_pass(mesh, op, 0, cfg)
+    assert [int(h) for h in a.hashes()] == [int(h) for h in b.hashes()]
+    ta, tb = a.tracks(), b.tracks()
+    assert len(ta) == len(tb) and sum(len(t["trail"]) for t in ta) > 0
+    for x, y in zip(ta, tb):
+        assert x["layer"] == y["layer"]
+        np.testing.assert_array_equal(np.asarray(x["trail"]), np.asarray(y["trail"]))
