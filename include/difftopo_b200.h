@@ -56,7 +56,7 @@ typedef struct {
   double covered_threshold;
   double seed_radius;         /* <= 0: 1.5 * interface length scale */
   int32_t record_hashes;      /* per-check 64-bit field digests (parity tooling) */
-  int32_t reserved;
+  int32_t grid_ctas;          /* CTAs of the persistent step kernel; 0 = one per SM (B200: 148) */
 } dtb_config;
 
 /* CoefficientScheme (layer_field.hpp:30). */
@@ -111,6 +111,17 @@ int dtb_stable_time_step(const dtb_laplacian* op, const dtb_coefficients* c, dou
 /* ---- initial pass (diffusion.hpp:861 run_initial_pass) ------------------ */
 int dtb_run_initial_pass(const dtb_mesh* m, const dtb_laplacian* op, uint32_t seed_vertex, const dtb_config* cfg,
                          const dtb_coefficients* c, dtb_result** out);
+/* Batch of independent initial passes on this GPU (BASELINE configs[4]):
+ * item i runs run_initial_pass(meshes[i], ops[i], seeds[i] (0 if seeds is
+ * NULL)) exactly as dtb_run_initial_pass would, up to `concurrency` passes at
+ * once (<= 0: 8), each a persistent kernel on its own stream over
+ * cfg->grid_ctas CTAs (0: SMs / concurrency).  out[i] receives the result
+ * (NULL on failure) and rc[i] (optional) its code; the return value is the
+ * first failing item's code.  Replaces a caller's loop over
+ * Engine::run_initial_pass (diffusion.hpp:530) for independent meshes. */
+int dtb_run_initial_pass_batch(const dtb_mesh* const* meshes, const dtb_laplacian* const* ops,
+                               const uint32_t* seeds, int32_t n, const dtb_config* cfg, const dtb_coefficients* c,
+                               int32_t concurrency, dtb_result** out, int32_t* rc);
 void dtb_result_free(dtb_result* r);
 /* status = DTB_OK or the error that ended the run (e.g. DTB_EMAXSTEPS); the
  * event log and tracks recorded up to that point stay available. */

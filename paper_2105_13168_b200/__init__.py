@@ -43,7 +43,7 @@ class Config(C.Structure):
         ("dt", C.c_double), ("band_low_threshold", C.c_double), ("saturation", C.c_double),
         ("collision_threshold", C.c_double), ("check_interval", C.c_int32), ("record_trails", C.c_int32),
         ("max_steps", C.c_int64), ("covered_threshold", C.c_double), ("seed_radius", C.c_double),
-        ("record_hashes", C.c_int32), ("reserved", C.c_int32),
+        ("record_hashes", C.c_int32), ("grid_ctas", C.c_int32),
     ]
 
 
@@ -94,6 +94,8 @@ def load_library(path: str = LIB_PATH):
         "dtb_laplacian_apply": (C.c_int, [P, pD, pD]),
         "dtb_stable_time_step": (C.c_int, [P, C.POINTER(Coefficients), pD]),
         "dtb_run_initial_pass": (C.c_int, [P, P, U32, C.POINTER(Config), C.POINTER(Coefficients), pP]),
+        "dtb_run_initial_pass_batch": (C.c_int, [pP, pP, pU32, C.c_int32, C.POINTER(Config),
+                                                 C.POINTER(Coefficients), C.c_int32, pP, pI32]),
         "dtb_result_free": (None, [P]),
         "dtb_result_summary": (C.c_int, [P, pI32, pI64, pD, pI64, pI64, pI64, pI64]),
         "dtb_result_message": (C.c_char_p, [P]),
@@ -514,6 +516,33 @@ def run_initial_pass(mesh: TriangleMesh, op: LaplacianOperator, seed_vertex: int
     h = C.c_void_p()
     _check(lib.dtb_run_initial_pass(mesh._h, op._h, seed_vertex, C.byref(cfg), C.byref(co), C.byref(h)))
     return InitialPassResult(h)
+
+
+def run_initial_pass_batch(meshes: Sequence[TriangleMesh], ops: Sequence[LaplacianOperator],
+                           seeds: Optional[Sequence[int]] = None, cfg: Optional[Config] = None,
+                           coefficients: Optional[Coefficients] = None,
+                           concurrency: int = 0) -> List[InitialPassResult]:
+    """Independent initial passes of a batch of meshes on this GPU, several at
+    once (dtb_run_initial_pass_batch); item i equals
+    run_initial_pass(meshes[i], ops[i], seeds[i], cfg)."""
+    lib = load_library()
+    n = len(meshes)
+    if len(ops) != n or (seeds is not None and len(seeds) != n):
+        raise ValueError("meshes, ops and seeds must have the same length")
+    cfg = cfg or default_config()
+    co = coefficients or default_coefficients()
+    mh = (C.c_void_p * max(1, n))(*[m._h for m in meshes])
+    oh = (C.c_void_p * max(1, n))(*[o._h for o in ops])
+    sd = np.ascontiguousarray(seeds if seeds is not None else np.zeros(n), np.uint32)
+    out = (C.c_void_p * max(1, n))()
+    rc = np.zeros(max(1, n), np.int32)
+    code = lib.dtb_run_initial_pass_batch(mh, oh, _ptr(sd, C.c_uint32), n, C.byref(cfg), C.byref(co), concurrency,
+                                          out, _ptr(rc, C.c_int32))
+    err = DiffTopoError(code, lib.dtb_last_error().decode()) if code else None  # before other calls reset it
+    results = [InitialPassResult(C.c_void_p(out[i])) if out[i] else None for i in range(n)]
+    if err is not None:
+        raise err
+    return results
 
 
 class LayerField:

@@ -3,10 +3,13 @@
 #include "../../include/difftopo_b200.h"
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "engine.hpp"
 
@@ -67,6 +70,8 @@ struct dtb_result {
 namespace {
 
 thread_local std::string g_err;
+// Default number of passes a batch runs at once (each on SMs / lanes CTAs).
+constexpr int kBatchLanes = 8;
 
 template <class F>
 int guard(F&& f) {
@@ -99,6 +104,7 @@ Config to_cfg(const dtb_config* c) {
   cfg.covered_threshold = c->covered_threshold;
   cfg.seed_radius = c->seed_radius;
   cfg.record_hashes = c->record_hashes != 0;
+  cfg.grid_ctas = c->grid_ctas;
   return cfg;
 }
 Coefficients to_coef(const dtb_coefficients* c) {
@@ -150,7 +156,7 @@ void dtb_config_default(dtb_config* c) {
   c->covered_threshold = d.covered_threshold;
   c->seed_radius = d.seed_radius;
   c->record_hashes = 0;
-  c->reserved = 0;
+  c->grid_ctas = 0;
 }
 
 void dtb_coefficients_default(dtb_coefficients* c) {
@@ -421,6 +427,70 @@ int dtb_run_initial_pass(const dtb_mesh* m, const dtb_laplacian* op, uint32_t se
     auto r = std::make_unique<dtb_result>();
     r->r = run_initial_pass(m->dev ? m->dev : (m->device(), m->dev), *op->op, seed, to_cfg(cfg), to_coef(c));
     *out = r.release();
+  });
+}
+
+int dtb_run_initial_pass_batch(const dtb_mesh* const* meshes, const dtb_laplacian* const* ops,
+                               const uint32_t* seeds, int32_t n, const dtb_config* cfg, const dtb_coefficients* c,
+                               int32_t concurrency, dtb_result** out, int32_t* rc) {
+  return guard([&] {
+    need(meshes, "meshes");
+    need(ops, "ops");
+    need(out, "out");
+    if (n < 0) fail(kInvalidParameter, "negative batch size");
+    for (int32_t i = 0; i < n; ++i) {
+      out[i] = nullptr;
+      if (rc) rc[i] = DTB_OK;
+      need(meshes[i], "mesh");
+      need(ops[i], "op");
+    }
+    if (n == 0) return;
+    int dev = 0, sms = 0;
+    cuda_check(cudaGetDevice(&dev), "device");
+    cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms");
+    const int lanes = std::max(1, std::min<int>(concurrency > 0 ? concurrency : kBatchLanes, n));
+    Config base = to_cfg(cfg);
+    // Each pass is a persistent cooperative kernel on its own stream; the
+    // concurrent passes split the SMs between them.
+    if (base.grid_ctas == 0) base.grid_ctas = std::max(1, sms / lanes);
+    const Coefficients co = to_coef(c);
+    // Device copies of host-built meshes are made here, one at a time.
+    size_t max_nv = 0, max_ne = 0;
+    for (int32_t i = 0; i < n; ++i) {
+      meshes[i]->device();
+      max_nv = std::max<size_t>(max_nv, meshes[i]->nv());
+      max_ne = std::max<size_t>(max_ne, meshes[i]->ne());
+    }
+    // Every result keeps its workspace, so a batch that fits (about 1 KB per
+    // vertex) reserves one per item; a larger one only one per lane.
+    const size_t want = static_cast<size_t>(n) * max_nv * 1024 <= (size_t{16} << 30) ? static_cast<size_t>(n)
+                                                                                       : static_cast<size_t>(lanes);
+    DeviceMesh::reserve_fields(want, max_nv, max_ne);
+    std::atomic<int32_t> next{0};
+    std::vector<int32_t> codes(static_cast<size_t>(n), DTB_OK);
+    std::vector<std::string> msgs(static_cast<size_t>(n));
+    auto worker = [&] {
+      if (cudaSetDevice(dev) != cudaSuccess) return;
+      for (int32_t i; (i = next.fetch_add(1)) < n;) {
+        const int code = guard([&] {
+          auto r = std::make_unique<dtb_result>();
+          r->r = run_initial_pass(meshes[i]->dev, *ops[i]->op, seeds ? seeds[i] : 0, base, co);
+          out[i] = r.release();
+        });
+        codes[static_cast<size_t>(i)] = code;
+        if (code != DTB_OK) msgs[static_cast<size_t>(i)] = g_err;
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int k = 1; k < lanes; ++k) pool.emplace_back(worker);
+    worker();
+    for (auto& t : pool) t.join();
+    for (int32_t i = 0; i < n; ++i) {
+      if (rc) rc[i] = codes[static_cast<size_t>(i)];
+      if (codes[static_cast<size_t>(i)] != DTB_OK)
+        throw Error(codes[static_cast<size_t>(i)],
+                    "batch item " + std::to_string(i) + ": " + msgs[static_cast<size_t>(i)]);
+    }
   });
 }
 

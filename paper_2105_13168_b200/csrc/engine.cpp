@@ -446,6 +446,7 @@ void Config::validate() const {
     fail(kInvalidParameter, "collision threshold must lie in (0, 0.5]");
   if (check_interval < 1) fail(kInvalidParameter, "check interval must be >= 1");
   if (max_steps < 1) fail(kInvalidParameter, "max steps must be >= 1");
+  if (grid_ctas < 0) fail(kInvalidParameter, "grid CTAs must be >= 0");
 }
 
 // Geodesic ball by Dijkstra over mesh edges (diffusion.hpp:134).
@@ -555,7 +556,9 @@ std::vector<SurfaceLoop> extract_isoline(const Mesh& mesh, const std::vector<dou
 DeviceField::DeviceField(std::shared_ptr<DeviceMesh> dm, cudaStream_t s) : dm_(dm.get()), keep_(std::move(dm)), s_(s) {
   setup();
 }
-DeviceField::DeviceField(DeviceMesh* dm, cudaStream_t s) : dm_(dm), s_(s) { setup(); }
+DeviceField::DeviceField(DeviceMesh* dm, cudaStream_t s, size_t nv_cap, size_t ne_cap) : dm_(dm), s_(s) {
+  setup(nv_cap, ne_cap);
+}
 
 DeviceMesh::~DeviceMesh() = default;
 
@@ -566,17 +569,18 @@ namespace {
 // batch of meshes -- do not re-allocate.
 std::mutex g_pool_mu;
 std::vector<DeviceField*> g_pool;
-constexpr size_t kPoolKeep = 4;
+constexpr size_t kPoolKeep = 16;
 }  // namespace
 
 std::shared_ptr<DeviceField> DeviceMesh::acquire_field(cudaStream_t s) {
   DeviceField* f = nullptr;
-  const size_t need = nv();
+  const size_t need = nv(), need_e = ne();
   {
     std::lock_guard<std::mutex> lk(g_pool_mu);
     size_t best = g_pool.size();
     for (size_t i = 0; i < g_pool.size(); ++i)
-      if (g_pool[i]->capacity() >= need && (best == g_pool.size() || g_pool[i]->capacity() < g_pool[best]->capacity()))
+      if (g_pool[i]->capacity() >= need && g_pool[i]->edge_capacity() >= need_e &&
+          (best == g_pool.size() || g_pool[i]->capacity() < g_pool[best]->capacity()))
         best = i;
     if (best < g_pool.size()) {
       f = g_pool[best];
@@ -597,15 +601,38 @@ std::shared_ptr<DeviceField> DeviceMesh::acquire_field(cudaStream_t s) {
     }
   });
 }
+
+void DeviceMesh::reserve_fields(size_t count, size_t nv, size_t ne) {
+  size_t have = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    for (DeviceField* f : g_pool) have += f->capacity() >= nv && f->edge_capacity() >= ne;
+  }
+  std::vector<DeviceField*> made;
+  for (size_t k = have; k < count; ++k) made.push_back(new DeviceField(static_cast<DeviceMesh*>(nullptr), nullptr, nv, ne));
+  cuda_check(cudaStreamSynchronize(nullptr), "reserve fields");
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  // Trim the smallest workspaces first.
+  for (DeviceField* f : made) g_pool.push_back(f);
+  std::stable_sort(g_pool.begin(), g_pool.end(),
+                   [](const DeviceField* a, const DeviceField* b) { return a->capacity() < b->capacity(); });
+  while (g_pool.size() > std::max(kPoolKeep, count)) {
+    delete g_pool.front();
+    g_pool.erase(g_pool.begin());
+  }
+}
+
 namespace {
-int engine_blocks(int nv);
+int engine_blocks(int nv, int requested = 0);
 }  // namespace
 
 
-void DeviceField::setup() {
-  const size_t nv = dm_->nv();
+void DeviceField::setup(size_t nv_cap, size_t ne_cap) {
+  const size_t nv = std::max<size_t>(nv_cap, dm_ ? dm_->nv() : 0);
+  const size_t ne = std::max<size_t>(ne_cap, dm_ ? dm_->ne() : 0);
   if (nv * kSlots >= 0xFFFFFFFFull) fail(kCapacityExceeded, "more than 134M vertices (32-bit union-find items)");
   cap_ = nv;
+  cap_e_ = ne;
   cnt.alloc(nv);
   interest.alloc(nv);
   scnt.alloc(nv);
@@ -644,7 +671,11 @@ void DeviceField::setup() {
   pair_keys.alloc(kPairCap);
   pairs.alloc(kPairCap);
   lastpos.alloc(4 * static_cast<size_t>(kMaxLayers + 1));
-  trail.alloc(kTrailCap);
+  // Trail ring: 8 records per vertex, between 2^16 and kTrailCap (a launch
+  // stops before it can wrap, see advance_until_event).
+  size_t tcap = size_t{1} << 16;
+  while (tcap < 8 * nv && tcap < static_cast<size_t>(kTrailCap)) tcap <<= 1;
+  trail.alloc(tcap);
   ctl.alloc(1);
   parent.zero(s_);
   pair_keys.zero(s_);
@@ -675,7 +706,7 @@ void DeviceField::setup() {
   view_.binfo = binfo.p;
   // Event-time scratch (layer pulls, isoline crossings, edits): allocated once
   // so host event handling never calls cudaMalloc/cudaFree.
-  const size_t ncap = std::max<size_t>(nv, dm_->ne()) + 1;
+  const size_t ncap = std::max<size_t>(nv, ne) + 1;
   ai0.alloc(ncap);
   ai1.alloc(ncap);
   ad0.alloc(ncap);
@@ -694,6 +725,7 @@ void DeviceField::setup() {
   work_.pairs = pairs.p;
   work_.lastpos = lastpos.p;
   work_.trail = trail.p;
+  work_.trail_mask = static_cast<int>(trail.n - 1);
   work_.ctl = ctl.p;
 }
 
@@ -1015,7 +1047,7 @@ StepParams make_params(const DeviceField& field, const Config& cfg, const Coeffi
 // Grid of the persistent kernel: at most one CTA per SM (the grid barrier's
 // cost grows with the CTA count, and a step's frontier/band work rarely needs
 // more than 148 x 256 threads), fewer for small meshes.
-int engine_blocks(int nv) {
+int engine_blocks(int nv, int requested) {
   // One 512-thread CTA per SM regardless of mesh size: a step's work is a
   // handful of dependent loads per frontier/band item, so more groups means
   // fewer items per group; the grid barrier costs ~1.2 us at 148 CTAs.
@@ -1027,6 +1059,7 @@ int engine_blocks(int nv) {
     cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms");
   }
   (void)nv;
+  if (requested > 0) return std::min(requested, maxco);
   if (const char* env = std::getenv("DTB_BLOCKS")) {
     const int b = std::atoi(env);
     if (b > 0) return std::min(b, maxco);
@@ -1067,7 +1100,7 @@ void run_check_kernel(DeviceField& field, const Config& cfg, const Coefficients&
   p.step_begin = s;
   static int maxco = 0;
   if (!maxco) ck(dev_max_coresident_blocks(&maxco), "occupancy");
-  const int blocks = std::min(maxco, engine_blocks(static_cast<int>(field.mesh().nv())));
+  const int blocks = std::min(maxco, engine_blocks(static_cast<int>(field.mesh().nv()), cfg.grid_ctas));
   ck(launch_check(field.mesh().view(), field.view(), field.work(), p, blocks, field.stream()), "check kernel");
   cuda_check(cudaStreamSynchronize(field.stream()), "check sync");
 }
@@ -1116,7 +1149,7 @@ void step(DeviceField& field, const DeviceLaplacian& op, const Config& cfg, cons
   p.step_begin = 1;
   p.step_end = 2;
   p.do_check = 0;
-  ck(launch_run(m, field.view(), w, p, engine_blocks(m.nv), s), "step kernel");
+  ck(launch_run(m, field.view(), w, p, engine_blocks(m.nv, cfg.grid_ctas), s), "step kernel");
   cuda_check(cudaStreamSynchronize(s), "step sync");
   const Ctl after = field.read_ctl();
   if (after.error == kDevBlowup) fail(kNumericalBlowup, "non-finite rate; reduce dt");
@@ -1178,7 +1211,7 @@ class PassEngine {
     track(1).created_event = 0;
     std::vector<int> sv(seeds.begin(), seeds.end());
     field_->mark_region(op_.view(), sv, 0, 1);
-    blocks_ = engine_blocks(static_cast<int>(dm_->nv()));
+    blocks_ = engine_blocks(static_cast<int>(dm_->nv()), cfg_.grid_ctas);
     if (const char* env = std::getenv("DTB_PHASE_PROF"); env && env[0] == '1') {
       prof_.alloc(4 * static_cast<size_t>(std::min<long>(cfg_.max_steps, 100000)) + 8 + 2 * 64 * 3 * 160 + 64);
       prof_.zero(s_);
@@ -1283,7 +1316,7 @@ class PassEngine {
   long advance_until_event(long done) {
     const auto t0 = std::chrono::steady_clock::now();
     StepParams p = params();
-    const long per_launch = std::max<long>(1, (kTrailCap / std::max(1, p.n_active)) - 2);
+    const long per_launch = std::max<long>(1, (static_cast<long>(field_->trail.n) / std::max(1, p.n_active)) - 2);
     long begin = done + 1;
     while (true) {
       const long end = std::min<long>(cfg_.max_steps + 1, begin + std::min<long>(per_launch, 1L << 20));
@@ -1321,7 +1354,7 @@ class PassEngine {
 
   void drain_trails(Ctl& c) {
     if (c.ntrail == 0) return;
-    if (c.ntrail > kTrailCap) fail(kCapacityExceeded, "trail ring overflow");
+    if (c.ntrail > static_cast<long>(field_->trail.n)) fail(kCapacityExceeded, "trail ring overflow");
     std::vector<TrailRec> recs = to_host(field_->trail, static_cast<size_t>(c.ntrail), s_);
     std::sort(recs.begin(), recs.end(), [](const TrailRec& a, const TrailRec& b) {
       return a.step != b.step ? a.step < b.step : a.layer < b.layer;

@@ -85,6 +85,11 @@ class DeviceMesh : public std::enable_shared_from_this<DeviceMesh> {
   ~DeviceMesh();
   // A field workspace for this mesh from the process-wide pool.
   std::shared_ptr<DeviceField> acquire_field(cudaStream_t s);
+  // Puts `count` workspaces for meshes of up to nv vertices / ne edges into
+  // the process-wide pool (a batch allocates before its passes start, so no
+  // pass frees device memory -- an implicit device synchronisation -- while
+  // others run).
+  static void reserve_fields(size_t count, size_t nv, size_t ne);
   Index nv() const { return nv_; }
   Index nf() const { return nf_; }
   Index ne() const { return ne_; }
@@ -163,6 +168,7 @@ struct Config {  // diffusion.hpp DiffusionConfig
   double seed_radius = 0.0;
   bool record_trails = true;
   bool record_hashes = false;  // per-check field digests (parity tooling)
+  int grid_ctas = 0;           // CTAs of the persistent step kernel (0: one per SM); batches split the SMs
   std::function<void(long)> on_check;  // host hook; forces a host round trip per check
   void validate() const;
 };
@@ -222,7 +228,7 @@ struct LayerMeta {
 class DeviceField {
  public:
   DeviceField(std::shared_ptr<DeviceMesh> dm, cudaStream_t s);
-  DeviceField(DeviceMesh* dm, cudaStream_t s);  // pooled (no ownership)
+  DeviceField(DeviceMesh* dm, cudaStream_t s, size_t nv_cap = 0, size_t ne_cap = 0);  // pooled (no ownership)
   // init_field (layer_field.hpp:318): base + one seed layer.
   void init(const std::vector<Index>& seeds);
 
@@ -249,6 +255,7 @@ class DeviceField {
   cudaStream_t stream() const { return s_; }
   void set_stream(cudaStream_t s) { s_ = s; }
   size_t capacity() const { return cap_; }
+  size_t edge_capacity() const { return cap_e_; }
   void retarget(DeviceMesh* dm) { dm_ = dm; }
   void set_band(double lo, double sat) {
     work_.band_lo = lo;
@@ -282,10 +289,11 @@ class DeviceField {
 
  private:
   friend class DeviceMesh;
-  void setup();
+  void setup(size_t nv_cap = 0, size_t ne_cap = 0);
   DeviceMesh* dm_;
   std::shared_ptr<DeviceMesh> keep_;  // keeps the mesh alive while the field is handed out
   size_t cap_ = 0;                    // vertex capacity of the device buffers
+  size_t cap_e_ = 0;                  // edge capacity (event-time scratch)
   cudaStream_t s_;
   std::vector<LayerMeta> meta_;
   DevField view_;

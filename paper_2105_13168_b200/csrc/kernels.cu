@@ -2004,7 +2004,7 @@ __device__ void flush_stat(const DevMesh& M, const DevWork& W, const StepParams&
       r.vx = M.px[r.vertex];
       r.vy = M.py[r.vertex];
       r.vz = M.pz[r.vertex];
-      W.trail[pos & (kTrailCap - 1)] = r;
+      W.trail[pos & W.trail_mask] = r;
     }
   }
   reset_stat(st);

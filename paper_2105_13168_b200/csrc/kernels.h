@@ -196,7 +196,8 @@ struct DevWork {
   unsigned long long *pair_keys = nullptr;  // kPairCap versioned keys
   unsigned *pairs = nullptr;            // recorded pairs (first << 16 | second)
   double *lastpos = nullptr;            // 4 * (kMaxLayers + 1): x, y, z, valid
-  TrailRec *trail = nullptr;            // kTrailCap
+  TrailRec *trail = nullptr;            // trail_mask + 1 records (a power of two <= kTrailCap)
+  int trail_mask = 0;
   unsigned long long *hashes = nullptr; // per-step field digests (optional)
   long long hash_base = 0;              // step of hashes[0]
   int hash_cap = 0;

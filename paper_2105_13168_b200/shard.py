@@ -8,7 +8,7 @@ data-path collective; only the per-item summaries are gathered at the end
 (`torch.distributed.gather_object`, NCCL or gloo)."""
 from __future__ import annotations
 
-from typing import Callable, List, Sequence
+from typing import Callable, List, Optional, Sequence
 
 
 def shard(items: Sequence, rank: int, world: int) -> List:
@@ -37,11 +37,45 @@ def run_item(spec: str, max_steps: int, seed: int = 0) -> dict:
             "field_hash": res.field_hash()}
 
 
+def run_batch(specs: Sequence[str], max_steps: int, seed: int = 0, concurrency: int = 0,
+              arrays: Optional[dict] = None) -> List[dict]:
+    """This rank's items as one native batch (dtb_run_initial_pass_batch):
+    meshes and operators are built first, then the passes run several at a
+    time on disjoint SM shares; each summary equals run_item's.  `arrays`
+    (spec -> (vertices, faces)) supplies host arrays instead of generating."""
+    from . import TriangleMesh, assemble_laplacian, default_config, run_initial_pass_batch
+
+    meshes = [TriangleMesh.from_arrays(*arrays[s]) if arrays else TriangleMesh.generate(s) for s in specs]
+    ops = [assemble_laplacian(m) for m in meshes]
+    res = run_initial_pass_batch(meshes, ops, [seed] * len(specs), default_config(max_steps=max_steps),
+                                 concurrency=concurrency)
+    out = []
+    for spec, mesh, r in zip(specs, meshes, res):
+        info = mesh.info()
+        out.append({"spec": spec, "V": info["V"], "genus": info["genus"], "status": r.status, "steps": r.steps,
+                    "events": r.n_events, "handle_estimates": r.handle_estimate_count,
+                    "t_pass": r.timing()["t_pass_device"], "field_hash": r.field_hash()})
+    return out
+
+
+def run_sharded_batch(items: Sequence, rank: int, world: int, max_steps: int, dist=None,
+                      concurrency: int = 0, arrays: Optional[dict] = None) -> List[dict]:
+    """run_sharded with this rank's slice run as one concurrent batch."""
+    mine = shard(items, rank, world)
+    res = run_batch(mine, max_steps, concurrency=concurrency, arrays=arrays)
+    out = [dict(r, index=rank + world * k) for k, r in enumerate(res)]
+    return _gather(out, rank, world, dist)
+
+
 def run_sharded(items: Sequence, rank: int, world: int, worker: Callable[[object], dict], dist=None) -> List[dict]:
     """Runs `worker` on this rank's slice; rank 0 returns every item's result
     in the original order (other ranks return their own slice)."""
     mine = shard(items, rank, world)
     out = [dict(worker(it), index=rank + world * k) for k, it in enumerate(mine)]
+    return _gather(out, rank, world, dist)
+
+
+def _gather(out: List[dict], rank: int, world: int, dist) -> List[dict]:
     if dist is None or world == 1:
         return out
     gathered = [None] * world if rank == 0 else None
