@@ -328,12 +328,8 @@ inline InitialPassResult read_result(dtb_result* r, Index seed) {
 }
 }  // namespace detail
 
-// run_initial_pass (diffusion.hpp:861).  Like the reference it throws the
-// error that ended the run (e.g. MaxStepsExceeded); run_initial_pass_partial
-// returns the partial log instead.
-inline InitialPassResult run_initial_pass_partial(const TriangleMesh& mesh, const LaplacianOperator& op,
-                                                  Index seed_vertex, const DiffusionConfig& cfg = {},
-                                                  const CoefficientScheme& scheme = {}) {
+namespace detail {
+inline dtb_config to_c(const DiffusionConfig& cfg) {
   dtb_config c;
   dtb_config_default(&c);
   c.dt = cfg.dt;
@@ -345,6 +341,17 @@ inline InitialPassResult run_initial_pass_partial(const TriangleMesh& mesh, cons
   c.max_steps = cfg.max_steps;
   c.covered_threshold = cfg.covered_threshold;
   c.seed_radius = cfg.seed_radius;
+  return c;
+}
+}  // namespace detail
+
+// run_initial_pass (diffusion.hpp:861).  Like the reference it throws the
+// error that ended the run (e.g. MaxStepsExceeded); run_initial_pass_partial
+// returns the partial log instead.
+inline InitialPassResult run_initial_pass_partial(const TriangleMesh& mesh, const LaplacianOperator& op,
+                                                  Index seed_vertex, const DiffusionConfig& cfg = {},
+                                                  const CoefficientScheme& scheme = {}) {
+  const dtb_config c = detail::to_c(cfg);
   dtb_coefficients co{scheme.gradient_energy, scheme.penalty, scheme.contact, scheme.mobility};
   dtb_result* r = nullptr;
   check(dtb_run_initial_pass(mesh.handle(), op.handle(), seed_vertex, &c, &co, &r));
@@ -356,6 +363,39 @@ inline InitialPassResult run_initial_pass(const TriangleMesh& mesh, const Laplac
   InitialPassResult r = run_initial_pass_partial(mesh, op, seed_vertex, cfg, scheme);
   if (r.status != DTB_OK) throw_code(r.status, r.message);
   return r;
+}
+
+// Independent passes over a batch of meshes, several at once on this GPU
+// (dtb_run_initial_pass_batch); item i equals
+// run_initial_pass_partial(*meshes[i], *ops[i], seeds[i], cfg, scheme).
+// Throws the first failing item's error.
+inline std::vector<InitialPassResult> run_initial_pass_batch(const std::vector<const TriangleMesh*>& meshes,
+                                                             const std::vector<const LaplacianOperator*>& ops,
+                                                             const std::vector<Index>& seeds,
+                                                             const DiffusionConfig& cfg = {},
+                                                             const CoefficientScheme& scheme = {},
+                                                             int concurrency = 0) {
+  const size_t n = meshes.size();
+  if (ops.size() != n || seeds.size() != n) throw std::invalid_argument("batch sizes differ");
+  const dtb_config c = detail::to_c(cfg);
+  dtb_coefficients co{scheme.gradient_energy, scheme.penalty, scheme.contact, scheme.mobility};
+  std::vector<const dtb_mesh*> mh(n);
+  std::vector<const dtb_laplacian*> oh(n);
+  std::vector<uint32_t> sd(n);
+  for (size_t i = 0; i < n; ++i) {
+    mh[i] = meshes[i]->handle();
+    oh[i] = ops[i]->handle();
+    sd[i] = static_cast<uint32_t>(seeds[i]);
+  }
+  std::vector<dtb_result*> rs(n, nullptr);
+  const int code = dtb_run_initial_pass_batch(mh.data(), oh.data(), sd.data(), static_cast<int32_t>(n), &c, &co,
+                                              concurrency, rs.data(), nullptr);
+  const std::string msg = code != DTB_OK ? dtb_last_error() : "";
+  std::vector<InitialPassResult> out;
+  for (size_t i = 0; i < n; ++i)
+    if (rs[i]) out.push_back(detail::read_result(rs[i], seeds[i]));
+  if (code != DTB_OK) throw_code(code, msg);
+  return out;
 }
 
 // Reeb graph (SPEC reeb.build_reeb): nodes = events, arcs = layer lifetimes.

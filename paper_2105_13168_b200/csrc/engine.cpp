@@ -1173,7 +1173,9 @@ class PassEngine {
     cuda_check(cudaEventCreate(&ev0k_), "event");
     cuda_check(cudaEventCreate(&ev1k_), "event");
     cuda_check(cudaEventRecord(ev0_, s_), "event record");
+    StageTimer tm(s_);
     field_ = dm_->acquire_field(s_);
+    tm.mark("pass workspace");
     field_->set_band(cfg_.band_low_threshold, cfg_.saturation);
     res_.field = field_;
     res_.seed_vertex = seed;
@@ -1195,7 +1197,9 @@ class PassEngine {
       }
     }
     if (!seeded) seeds = seed_region(mesh(), seed, radius);
+    tm.mark("pass seed");
     field_->init(seeds);
+    tm.mark("pass init");
     dt_ = cfg_.dt > 0 ? cfg_.dt : stable_time_step(op_, co_);
     res_.dt_used = dt_;
     if (cfg_.record_hashes) {
@@ -1211,6 +1215,7 @@ class PassEngine {
     track(1).created_event = 0;
     std::vector<int> sv(seeds.begin(), seeds.end());
     field_->mark_region(op_.view(), sv, 0, 1);
+    tm.mark("pass frontier");
     blocks_ = engine_blocks(static_cast<int>(dm_->nv()), cfg_.grid_ctas);
     if (const char* env = std::getenv("DTB_PHASE_PROF"); env && env[0] == '1') {
       prof_.alloc(4 * static_cast<size_t>(std::min<long>(cfg_.max_steps, 100000)) + 8 + 2 * 64 * 3 * 160 + 64);
@@ -1253,6 +1258,7 @@ class PassEngine {
       res_.message = e.what();
     }
     res_.steps = step;
+    StageTimer tm(s_);
     if (prof_.p) {
       report_phases();
       instr_report();
@@ -1263,6 +1269,7 @@ class PassEngine {
       res_.sum_interest = c.sum_interest;
     }
     finish_tracks();
+    tm.mark("pass tracks");
     cuda_check(cudaEventRecord(ev1_, s_), "event record");
     cuda_check(cudaEventSynchronize(ev1_), "event sync");
     float ms = 0;

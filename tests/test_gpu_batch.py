@@ -60,3 +60,23 @@ def test_batch_failing_item_is_isolated():
         dt.run_initial_pass_batch(meshes, ops, [0, 10 ** 6, 5], cfg, concurrency=2)
     assert "batch item 1" in str(e.value)
     assert dt.run_initial_pass_batch([], [], None, cfg) == []
+
+
+def test_cpp_facade_batch(tmp_path):
+    import json
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "batch_passes"
+    subprocess.run(["g++", "-O2", "-std=c++17", f"-I{root}/include", f"{root}/examples/batch_passes.cpp",
+                    f"-L{root}/paper_2105_13168_b200/lib", "-ldifftopo_b200",
+                    f"-Wl,-rpath,{root}/paper_2105_13168_b200/lib", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe), "4", "300"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    rows = [json.loads(line) for line in out.stdout.splitlines()]
+    cfg = dt.default_config(max_steps=300)
+    for i, row in enumerate(rows):
+        m = dt.TriangleMesh.generate(f"genus:{1 + i}:3")
+        r = dt.run_initial_pass(m, dt.assemble_laplacian(m), 0, cfg)
+        assert (row["steps"], row["events"]) == (r.steps, r.n_events), i
+    assert len(rows) == 4
