@@ -301,15 +301,27 @@ __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork
   unsigned short* const nl = cl + kCand;
   unsigned short* const sl = nl + kWork;
   static_assert((kSlots + kCand + 2 * kWork) * (8 + 2) <= kSlabBytes, "the general update's arrays fit the slab");
+  INSTR_C0(tU);
   __syncwarp(gm);  // the slab may hold the fold staging of this group's previous vertex
   const int cv = F.cnt[v];
   const size_t vb = static_cast<size_t>(v) * kSlots;
-  if (lane == 0)
-    for (int j = 0; j < cv; ++j) {
-      ol[j] = F.lay[vb + j];
+  // The column is staged lane-parallel (slot j on lane j % kG), and the
+  // activity of its layers is gathered into own_act (bit j: slot j holds an
+  // active non-base layer) so lane 0's sequential part makes no global loads.
+  unsigned own_act = 0;
+  for (int jb = 0; jb < cv; jb += kG) {
+    const int j = jb + lane;
+    bool act = false;
+    if (j < cv) {
+      const int l = F.lay[vb + j];
+      ol[j] = static_cast<unsigned short>(l);
       ox[j] = F.val[vb + j];
+      act = l != 0 && W.active[l];
     }
-  const double phib = (cv > 0 && F.lay[vb] == 0) ? F.val[vb] : 0.0;
+    own_act |= ((__ballot_sync(gm, act) >> (threadIdx.x & 24)) & 0xFFu) << jb;
+  }
+  __syncwarp(gm);
+  const double phib = (cv > 0 && ol[0] == 0) ? ox[0] : 0.0;
 
   int nc = 0;
   double lapb = 0.0, lapt = 0.0;
@@ -328,6 +340,7 @@ __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork
       L[q] = 0;
       X[q] = 0.0;
     }
+    unsigned amask = 0;  // bit q: neighbour slot q < min(cu, kReg) holds an active layer
     if (valid) {
       u = __ldg(M.s_col + k);
       s = __ldg(M.s_val + k);
@@ -342,8 +355,12 @@ __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork
 #pragma unroll
       for (int q = 0; q < kReg; ++q)
         if (q < cu) {
-          if (L[q] == 0) bu = X[q];
-          else if (W.active[L[q]]) au = au + X[q];
+          if (L[q] == 0) {
+            bu = X[q];
+          } else if (W.active[L[q]]) {
+            au = au + X[q];
+            amask |= 1u << q;
+          }
         }
       for (int q = kReg; q < cu; ++q) {
         const int l = F.lay[b + q];
@@ -358,6 +375,7 @@ __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork
       const int cu_ = __shfl_sync(gm, cu, jj, kG);
       const double bu_ = __shfl_sync(gm, bu, jj, kG);
       const double au_ = __shfl_sync(gm, au, jj, kG);
+      const unsigned am_ = __shfl_sync(gm, amask, jj, kG);
       lapb = lapb + s_ * bu_;
       lapt = lapt + s_ * au_;
       if (bu_ > 0.0) bnear = true;
@@ -365,18 +383,34 @@ __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork
       for (int q = 0; q < kReg; ++q) {
         const int l_ = __shfl_sync(gm, static_cast<int>(L[q]), jj, kG);
         const double x_ = __shfl_sync(gm, X[q], jj, kG);
-        if (lane == 0 && q < cu_ && l_ != 0 && W.active[l_]) cand_add(cl, ca, nc, overflow, l_, s_ * x_);
+        if (lane == 0 && ((am_ >> q) & 1)) cand_add(cl, ca, nc, overflow, l_, s_ * x_);
       }
       if (cu_ > kReg) {
+        // Slots past kReg: loaded lane-parallel, added by lane 0 in slot order.
         const int u_ = __shfl_sync(gm, u, jj, kG);
         const size_t b = static_cast<size_t>(u_) * kSlots;
-        for (int q = kReg; q < cu_; ++q) {
-          const int l_ = F.lay[b + q];
-          if (lane == 0 && l_ != 0 && W.active[l_]) cand_add(cl, ca, nc, overflow, l_, s_ * F.val[b + q]);
+        for (int qb = kReg; qb < cu_; qb += kG) {
+          const int q = qb + lane;
+          int l = 0;
+          double x = 0.0;
+          bool act = false;
+          if (q < cu_) {
+            l = F.lay[b + q];
+            x = F.val[b + q];
+            act = l != 0 && W.active[l];
+          }
+          const unsigned am = (__ballot_sync(gm, act) >> (threadIdx.x & 24)) & 0xFFu;
+          const int m = min(kG, cu_ - qb);
+          for (int t = 0; t < m; ++t) {
+            const int l_ = __shfl_sync(gm, l, t, kG);
+            const double x_ = __shfl_sync(gm, x, t, kG);
+            if (lane == 0 && ((am >> t) & 1)) cand_add(cl, ca, nc, overflow, l_, s_ * x_);
+          }
         }
       }
     }
   }
+  INSTR_CP(6, tU);
   // From here on lane 0 alone: the candidate list and the working column live
   // in the group's slab, so only one lane may write them.  (Its siblings meet
   // it again at the group's next shuffle or __syncwarp.)
@@ -385,7 +419,7 @@ __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork
   // lacks its diagonal (never on valid meshes, kept for exactness).
   for (int j = 0; j < cv; ++j) {
     const int l = ol[j];
-    if (l == 0 || !W.active[l]) continue;
+    if (!((own_act >> j) & 1)) continue;
     int c = 0;
     while (c < nc && cl[c] != l) ++c;
     if (c == nc) {
@@ -433,14 +467,10 @@ __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork
   }
   if (bnear) {
     double total = 0.0, contact = 0.0;
-    for (int j = 0; j < cv; ++j) {
-      const int l = ol[j];
-      if (l != 0 && W.active[l]) total = total + ox[j];
-    }
-    for (int j = 0; j < cv; ++j) {
-      const int l = ol[j];
-      if (l != 0 && W.active[l]) contact = contact + sqrt(max0(phib * ox[j]));
-    }
+    for (int j = 0; j < cv; ++j)
+      if ((own_act >> j) & 1) total = total + ox[j];
+    for (int j = 0; j < cv; ++j)
+      if ((own_act >> j) & 1) contact = contact + sqrt(max0(phib * ox[j]));
     const double lap_total = lapt / mass;
     const double rate = -P.mu_n * (P.w * total + P.half_a2 * lap_total + P.e * contact) +
                         P.m_mu_n * (P.w * phib + P.half_a2 * lap_b);
@@ -483,6 +513,7 @@ __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork
     W.sval[o + j] = nx[j];
   }
   scratch_header<0>(W, i, nn, nl, nx, changed, old_one, new_one);
+  INSTR_CP(15, tU);
 }
 
 // ---------------------------------------------------------------------------
