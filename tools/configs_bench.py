@@ -25,11 +25,11 @@ import paper_2105_13168_b200 as dt  # noqa: E402
 from paper_2105_13168_b200 import shard  # noqa: E402
 
 
-def e2e(spec, steps, reps=2):
+def e2e(spec, steps, reps=3):
     m0 = dt.TriangleMesh.generate(spec)
     v, f = m0.vertices(), m0.faces()
     info = m0.info()
-    best = None
+    best, cold = None, None
     for _ in range(reps):
         t0 = time.perf_counter()
         m = dt.TriangleMesh.from_arrays(v, f)
@@ -42,10 +42,11 @@ def e2e(spec, steps, reps=2):
         row = {"e2e_ms": 1e3 * (t1 - t0), "pass_device_ms": 1e3 * tm["t_pass_device"], "status": r.status,
                "steps": r.steps, "events": len(evs), "reeb_nodes": reeb["nodes"], "reeb_arcs": len(reeb["arcs"]),
                "reeb_cycle_rank": reeb["cycle_rank"]}
+        cold = cold or row["e2e_ms"]  # first rep: workspace allocated inside the timed region
         if best is None or row["e2e_ms"] < best["e2e_ms"]:
             best = row
-        del r, op, m
-    return dict(info, spec=spec, **best)
+        del r, op, m, evs, reeb  # results keep their workspace; release it for the next rep
+    return dict(info, spec=spec, e2e_cold_ms=cold, **best)
 
 
 def batch(steps, rank=0, world=1, dist=None, concurrency=0):
