@@ -3,6 +3,9 @@
 // executed only at steps where the device reported a topology event.
 #include "engine.hpp"
 
+#include <dlfcn.h>
+#include <execinfo.h>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -125,7 +128,9 @@ double value_in(const std::vector<std::pair<Index, double>>& sorted_vals, Index 
   return (it != sorted_vals.end() && it->first == v) ? it->second : 0.0;
 }
 
-V3 mean_of(const Mesh& m, const std::vector<Index>& verts) {
+template <class MV>
+V3 mean_of(const MV& m, const std::vector<Index>& verts) {
+  m.need_vertices(verts);
   V3 c{};
   for (Index v : verts) c = c + m.p(v);
   return verts.empty() ? c : c / static_cast<double>(verts.size());
@@ -295,7 +300,17 @@ std::shared_ptr<const Mesh> DeviceMesh::host_ptr() const {
   if (mesh_) return mesh_;
   // Device-built mesh: download its arrays once (own stream, pinned staging
   // is not worth it for a one-off copy).
-  if (const char* e = std::getenv("DTB_TIMING"); e && e[0] == '1') std::fprintf(stderr, "[dtb] host mesh download\n");
+  if (const char* e = std::getenv("DTB_TIMING"); e && e[0] == '1') {
+    std::fprintf(stderr, "[dtb] host mesh download\n");
+    void* frames[16];
+    const int nf = backtrace(frames, 16);
+    for (int k = 0; k < nf; ++k) {
+      Dl_info info{};
+      if (dladdr(frames[k], &info) && info.dli_fbase)
+        std::fprintf(stderr, "[dtb]   at %s+0x%lx\n", info.dli_fname,
+                     static_cast<unsigned long>(static_cast<char*>(frames[k]) - static_cast<char*>(info.dli_fbase)));
+    }
+  }
   cudaStream_t s = nullptr;
   cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
   std::vector<V3> pos(nv_);
@@ -493,11 +508,198 @@ V3 SurfaceLoop::centroid() const {
   return c / total;
 }
 
+// Mesh views for host event handling.  HostView reads a host mesh; LocalMesh
+// reads a device-resident mesh through gathers of just the vertices, faces
+// and edges an event touches (their records are identical to the host
+// mesh's), so a device-built mesh is never downloaded whole (~700 MB at 5M
+// vertices).  need_*() batch the gathers; any record asked for without a
+// prior need_*() is fetched on its own.
+struct Row {
+  const Index* b;
+  const Index* e;
+  const Index* begin() const { return b; }
+  const Index* end() const { return e; }
+};
+
+class HostView {
+ public:
+  explicit HostView(const Mesh& m) : m_(m) {}
+  void need_vertices(const std::vector<Index>&) const {}
+  void need_faces(const std::vector<Index>&) const {}
+  void need_edges(const std::vector<Index>&) const {}
+  const V3& p(Index v) const { return m_.p(v); }
+  Row v2v(Index v) const { return {m_.v2v().data() + m_.v2v_off()[v], m_.v2v().data() + m_.v2v_off()[v + 1]}; }
+  Row v2f(Index v) const { return {m_.v2f().data() + m_.v2f_off()[v], m_.v2f().data() + m_.v2f_off()[v + 1]}; }
+  const std::array<Index, 3>& face(Index f) const { return m_.face(f); }
+  const std::array<Index, 3>& face_edges(Index f) const { return m_.face_edges(f); }
+  const std::array<Index, 2>& edge_vertices(Index e) const { return m_.edge_vertices(e); }
+  const std::array<Index, 2>& edge_faces(Index e) const { return m_.edge_faces(e); }
+  Index opposite_face(Index e, Index f) const { return m_.opposite_face(e, f); }
+
+ private:
+  const Mesh& m_;
+};
+
+class LocalMesh {
+ public:
+  LocalMesh(const DeviceMesh& dm, cudaStream_t s) : dm_(dm), s_(s) {
+    rows_.px = dm.px.p;
+    rows_.py = dm.py.p;
+    rows_.pz = dm.pz.p;
+    rows_.v2v_off = dm.n_off.p;
+    rows_.v2v = dm.n_col.p;
+    rows_.v2f_off = dm.f_off.p;
+    rows_.v2f = dm.f_col.p;
+    rows_.faces = dm.faces.p;
+    rows_.face_edges = dm.fe.p;
+    rows_.edges = dm.edges.p;
+    rows_.edge_faces = dm.ef.p;
+  }
+  void need_vertices(const std::vector<Index>& vs) const {
+    std::vector<unsigned> miss = missing(vs, vert_);
+    const int n = static_cast<int>(miss.size());
+    if (!n) return;
+    DevBuf<unsigned> list(miss.size());
+    DevBuf<int> bounds(4 * miss.size()), dst(miss.size());
+    DevBuf<double> pos(3 * miss.size());
+    list.upload(miss.data(), miss.size(), s_);
+    ck(launch_gather_vhead(rows_, list.p, n, bounds.p, pos.p, s_), "gather vertices");
+    std::vector<int> hb(4 * miss.size());
+    std::vector<double> hp(3 * miss.size());
+    bounds.download(hb.data(), hb.size(), s_);
+    pos.download(hp.data(), hp.size(), s_);
+    cuda_check(cudaStreamSynchronize(s_), "gather vertices");
+    std::vector<int> off(miss.size());
+    size_t tot = 0;
+    for (int i = 0; i < n; ++i) {
+      off[i] = static_cast<int>(tot);
+      tot += static_cast<size_t>(hb[4 * i + 1] - hb[4 * i]) + static_cast<size_t>(hb[4 * i + 3] - hb[4 * i + 2]);
+    }
+    std::vector<unsigned> hr(tot);
+    if (tot) {
+      DevBuf<unsigned> rows(tot);
+      dst.upload(off.data(), off.size(), s_);
+      ck(launch_gather_vrows(rows_, bounds.p, dst.p, n, rows.p, s_), "gather rows");
+      rows.download(hr.data(), tot, s_);
+      cuda_check(cudaStreamSynchronize(s_), "gather rows");
+    }
+    for (int i = 0; i < n; ++i) {
+      VertRec r;
+      r.p = V3{hp[3 * i], hp[3 * i + 1], hp[3 * i + 2]};
+      const size_t a = off[i], nv2v = hb[4 * i + 1] - hb[4 * i], nv2f = hb[4 * i + 3] - hb[4 * i + 2];
+      r.v2v.assign(hr.begin() + a, hr.begin() + a + nv2v);
+      r.v2f.assign(hr.begin() + a + nv2v, hr.begin() + a + nv2v + nv2f);
+      vert_.emplace(miss[i], std::move(r));
+    }
+  }
+  void need_faces(const std::vector<Index>& fs) const {
+    std::vector<unsigned> miss = missing(fs, face_);
+    if (miss.empty()) return;
+    std::vector<unsigned> h = gather(miss, 6, launch_gather_faces);
+    for (size_t i = 0; i < miss.size(); ++i)
+      face_.emplace(miss[i], FaceRec{{h[6 * i], h[6 * i + 1], h[6 * i + 2]}, {h[6 * i + 3], h[6 * i + 4], h[6 * i + 5]}});
+  }
+  void need_edges(const std::vector<Index>& es) const {
+    std::vector<unsigned> miss = missing(es, edge_);
+    if (miss.empty()) return;
+    std::vector<unsigned> h = gather(miss, 4, launch_gather_edges);
+    for (size_t i = 0; i < miss.size(); ++i)
+      edge_.emplace(miss[i], EdgeRec{{h[4 * i], h[4 * i + 1]}, {h[4 * i + 2], h[4 * i + 3]}});
+  }
+  const V3& p(Index v) const { return vert(v).p; }
+  Row v2v(Index v) const {
+    const auto& r = vert(v);
+    return {r.v2v.data(), r.v2v.data() + r.v2v.size()};
+  }
+  Row v2f(Index v) const {
+    const auto& r = vert(v);
+    return {r.v2f.data(), r.v2f.data() + r.v2f.size()};
+  }
+  const std::array<Index, 3>& face(Index f) const { return face_rec(f).v; }
+  const std::array<Index, 3>& face_edges(Index f) const { return face_rec(f).e; }
+  const std::array<Index, 2>& edge_vertices(Index e) const { return edge_rec(e).v; }
+  const std::array<Index, 2>& edge_faces(Index e) const { return edge_rec(e).f; }
+  Index opposite_face(Index e, Index f) const {
+    const auto& r = edge_rec(e);
+    return r.f[0] == f ? r.f[1] : r.f[0];
+  }
+
+ private:
+  struct VertRec {
+    V3 p;
+    std::vector<Index> v2v, v2f;
+  };
+  struct FaceRec {
+    std::array<Index, 3> v, e;
+  };
+  struct EdgeRec {
+    std::array<Index, 2> v, f;
+  };
+  template <class M>
+  static std::vector<unsigned> missing(const std::vector<Index>& ids, const M& have) {
+    std::vector<unsigned> out;
+    for (Index x : ids)
+      if (!have.count(x)) out.push_back(static_cast<unsigned>(x));
+    std::sort(out.begin(), out.end());
+    out.erase(std::unique(out.begin(), out.end()), out.end());
+    return out;
+  }
+  template <class L>
+  std::vector<unsigned> gather(const std::vector<unsigned>& ids, int width, L launch) const {
+    DevBuf<unsigned> list(ids.size()), out(width * ids.size());
+    list.upload(ids.data(), ids.size(), s_);
+    ck(launch(rows_, list.p, static_cast<int>(ids.size()), out.p, s_), "gather");
+    std::vector<unsigned> h(width * ids.size());
+    out.download(h.data(), h.size(), s_);
+    cuda_check(cudaStreamSynchronize(s_), "gather");
+    return h;
+  }
+  const VertRec& vert(Index v) const {
+    auto it = vert_.find(v);
+    if (it == vert_.end()) {
+      need_vertices({v});
+      it = vert_.find(v);
+    }
+    return it->second;
+  }
+  const FaceRec& face_rec(Index f) const {
+    auto it = face_.find(f);
+    if (it == face_.end()) {
+      need_faces({f});
+      it = face_.find(f);
+    }
+    return it->second;
+  }
+  const EdgeRec& edge_rec(Index e) const {
+    auto it = edge_.find(e);
+    if (it == edge_.end()) {
+      need_edges({e});
+      it = edge_.find(e);
+    }
+    return it->second;
+  }
+  const DeviceMesh& dm_;
+  cudaStream_t s_;
+  MeshRows rows_{};
+  mutable std::unordered_map<Index, VertRec> vert_;
+  mutable std::unordered_map<Index, FaceRec> face_;
+  mutable std::unordered_map<Index, EdgeRec> edge_;
+};
+
 // Chains edge crossings into closed loops (isoline.hpp:55-103): seeds in
 // ascending edge order, each walk leaves through the face's other crossed
 // edge, the closing point repeats the first.
-static std::vector<SurfaceLoop> chain_crossings(const Mesh& mesh, const std::vector<int>& e_sorted,
+template <class MV>
+static std::vector<SurfaceLoop> chain_crossings(const MV& mesh, const std::vector<int>& e_sorted,
                                                 const std::unordered_map<Index, double>& t_of) {
+  {
+    const std::vector<Index> es(e_sorted.begin(), e_sorted.end());
+    mesh.need_edges(es);
+    std::vector<Index> ends;
+    for (Index e : es)
+      for (Index v : mesh.edge_vertices(e)) ends.push_back(v);
+    mesh.need_vertices(ends);
+  }
   std::unordered_map<Index, std::array<Index, 2>> face_edges;
   for (int ei : e_sorted) {
     const Index e = static_cast<Index>(ei);
@@ -547,7 +749,7 @@ std::vector<SurfaceLoop> extract_isoline(const Mesh& mesh, const std::vector<dou
     es.push_back(static_cast<int>(e));
     t_of[e] = sa / (sa - sb);
   }
-  return chain_crossings(mesh, es, t_of);
+  return chain_crossings(HostView(mesh), es, t_of);
 }
 
 // ---------------------------------------------------------------------------
@@ -959,18 +1161,31 @@ long InitialPassResult::handle_estimate_count() const {
 // ---------------------------------------------------------------------------
 // extract_front / detect_collisions / step (one-shot API)
 
-std::vector<FrontComponent> extract_front(const DeviceField& field, Index layer, const Config& cfg) {
-  const Mesh& mesh = field.mesh().host();
+namespace {
+template <class MV>
+std::vector<FrontComponent> extract_front_with(const MV& mesh, const DeviceField& field, Index layer,
+                                               const Config& cfg) {
   const auto vals = field.layer_values(layer);
   std::vector<Index> band;
   for (const auto& [v, x] : vals)
     if (x < 1.0 && x > cfg.band_low_threshold && x < cfg.saturation) band.push_back(v);
   if (band.empty()) return {};
+  mesh.need_vertices(band);
   std::vector<Index> tris;
   for (Index v : band)
-    for (Index q = mesh.v2f_off()[v]; q < mesh.v2f_off()[v + 1]; ++q) tris.push_back(mesh.v2f()[q]);
+    for (Index f : mesh.v2f(v)) tris.push_back(f);
   std::sort(tris.begin(), tris.end());
   tris.erase(std::unique(tris.begin(), tris.end()), tris.end());
+  mesh.need_faces(tris);
+  {
+    std::vector<Index> es, corners;
+    for (Index f : tris) {
+      for (Index e : mesh.face_edges(f)) es.push_back(e);
+      for (Index v : mesh.face(f)) corners.push_back(v);
+    }
+    mesh.need_edges(es);
+    mesh.need_vertices(corners);
+  }
   auto slot = [&](Index f) -> long {
     auto it = std::lower_bound(tris.begin(), tris.end(), f);
     return (it != tris.end() && *it == f) ? static_cast<long>(it - tris.begin()) : -1;
@@ -1015,6 +1230,13 @@ std::vector<FrontComponent> extract_front(const DeviceField& field, Index layer,
     c.band_length = len;
   }
   return comps;
+}
+}  // namespace
+
+std::vector<FrontComponent> extract_front(const DeviceField& field, Index layer, const Config& cfg) {
+  const DeviceMesh& dm = field.mesh();
+  if (dm.has_host()) return extract_front_with(HostView(dm.host()), field, layer, cfg);
+  return extract_front_with(LocalMesh(dm, field.stream()), field, layer, cfg);
 }
 
 namespace {
@@ -1412,15 +1634,18 @@ class PassEngine {
     for (Index c = 0; c < fronts.size(); ++c)
       for (Index v : fronts[c].boundary_vertices)
         if (label.emplace(v, c).second) queue.push_back(v);
-    for (size_t head = 0; head < queue.size(); ++head) {
-      const Index v = queue[head];
-      const Index c = label.at(v);
-      for (Index o = mesh().v2v_off()[v]; o < mesh().v2v_off()[v + 1]; ++o) {
-        const Index u = mesh().v2v()[o];
-        if (!is_unsat(u)) continue;
-        if (label.emplace(u, c).second) queue.push_back(u);
+    with_view([&](const auto& mv) {
+      mv.need_vertices(unsat);  // the search only enters unsaturated vertices
+      for (size_t head = 0; head < queue.size(); ++head) {
+        const Index v = queue[head];
+        const Index c = label.at(v);
+        for (Index u : mv.v2v(v)) {
+          if (!is_unsat(u)) continue;
+          if (label.emplace(u, c).second) queue.push_back(u);
+        }
       }
-    }
+      return 0;
+    });
     std::vector<std::vector<Index>> comps(fronts.size());
     for (Index v : unsat) {
       auto it = label.find(v);
@@ -1438,7 +1663,7 @@ class PassEngine {
     ev.step = s;
     ev.layers = {layer};
     ev.produced = children;
-    ev.position = mean_of(mesh(), parent_band);
+    ev.position = with_view([&](const auto& mv) { return mean_of(mv, parent_band); });
     const Index idx = static_cast<Index>(res_.events.size());
     res_.events.push_back(std::move(ev));
     track(layer).consumed_event = idx;
@@ -1464,7 +1689,7 @@ class PassEngine {
       b1[static_cast<Index>(e[i])] = bb[i];
     }
     std::sort(e.begin(), e.end());
-    std::vector<SurfaceLoop> loops = chain_crossings(mesh(), e, t_of);
+    std::vector<SurfaceLoop> loops = with_view([&](const auto& mv) { return chain_crossings(mv, e, t_of); });
     double best = -1;
     for (auto& loop : loops) {
       double base_mass = 0;
@@ -1511,7 +1736,7 @@ class PassEngine {
     ev.kind = EventKind::Merge;
     ev.step = s;
     ev.layers = group;
-    ev.position = mean_of(mesh(), union_band);
+    ev.position = with_view([&](const auto& mv) { return mean_of(mv, union_band); });
     ev.covered_snapshot = field_->covered_set(cfg_.covered_threshold);
     const Index idx = static_cast<Index>(res_.events.size());
     if (!loops.empty()) {
@@ -1551,7 +1776,7 @@ class PassEngine {
     if (!get_lastpos(layer, p)) {
       std::vector<Index> support;
       for (const auto& [v, x] : field_->layer_values(layer)) support.push_back(v);
-      p = mean_of(mesh(), support);
+      p = with_view([&](const auto& mv) { return mean_of(mv, support); });
     }
     ev.position = p;
     const Index idx = static_cast<Index>(res_.events.size());
@@ -1571,7 +1796,7 @@ class PassEngine {
       const std::vector<Index> act = field_->active_nonbase();
       for (size_t a = 0; a < act.size(); ++a) {
         if (st[a].ncomp < 2) continue;
-        auto fronts = extract_front(*field_, act[a], cfg_);
+        auto fronts = with_view([&](const auto& mv) { return extract_front_with(mv, *field_, act[a], cfg_); });
         if (fronts.size() < 2)
           fail(kInconsistentLog, "device reported a split the host front extraction does not see");
         changed |= handle_split(act[a], fronts, s);
@@ -1698,6 +1923,15 @@ class PassEngine {
 
   std::shared_ptr<DeviceMesh> dm_;
   const Mesh& mesh() const { return dm_->host(); }  // downloaded on first use for device-built meshes
+  // Event handlers read the mesh through a view: the host mesh when there is
+  // one, else local gathers from the device (never the whole-mesh download).
+  template <class F>
+  auto with_view(F&& f) const -> decltype(f(std::declval<const HostView&>())) {
+    if (dm_->has_host()) return f(HostView(dm_->host()));
+    if (!local_) local_ = std::make_unique<LocalMesh>(*dm_, s_);
+    return f(*local_);
+  }
+  mutable std::unique_ptr<LocalMesh> local_;
   const DeviceLaplacian& op_;
   Config cfg_;
   Coefficients co_;

@@ -260,6 +260,19 @@ struct FrontBuild {
   const unsigned *faces, *face_edges, *edge_faces, *edges;  // 3F, 3F, 2E, 2E
   const int *v2v_off, *v2v, *v2f_off, *v2f;
 };
+// Records of listed vertices (positions, v2v and v2f rows), faces (corners,
+// edges) and edges (ends, faces) for host event handling (meshdev.cu).
+struct MeshRows {
+  const double *px, *py, *pz;
+  const int *v2v_off, *v2v, *v2f_off, *v2f;
+  const unsigned *faces, *face_edges, *edges, *edge_faces;  // 3F, 3F, 2E, 2E
+};
+// bounds: 4 per vertex (v2v begin/end, v2f begin/end); pos: 3 per vertex.
+int launch_gather_vhead(const MeshRows& m, const unsigned* list, int n, int* bounds, double* pos, void* stream);
+// rows: vertex i's v2v row then its v2f row, from packed offset dst[i].
+int launch_gather_vrows(const MeshRows& m, const int* bounds, const int* dst, int n, unsigned* rows, void* stream);
+int launch_gather_faces(const MeshRows& m, const unsigned* list, int n, unsigned* out, void* stream);  // 6 per face
+int launch_gather_edges(const MeshRows& m, const unsigned* list, int n, unsigned* out, void* stream);  // 4 per edge
 int launch_positions(const double* xyz, int nv, double scale, double* px, double* py, double* pz, long long* fx,
                      long long* fy, long long* fz, void* stream);
 void instr_report();

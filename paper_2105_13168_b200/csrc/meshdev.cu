@@ -233,4 +233,75 @@ int launch_front_fill(const FrontBuild& b, const int* c_off, int* c_col, void* s
   return static_cast<int>(cudaGetLastError());
 }
 
+// ---------------------------------------------------------------------------
+// Local gathers for host event handling (engine.cpp LocalMesh): the records
+// of listed vertices, faces and edges, so an event never downloads the whole
+// mesh.  Rows are copied in two passes: bounds + positions, then the rows at
+// host-computed packed offsets.
+__global__ void k_gather_vhead(MeshRows m, const unsigned* list, int n, int* bounds, double* pos) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned v = list[i];
+  bounds[4 * i + 0] = m.v2v_off[v];
+  bounds[4 * i + 1] = m.v2v_off[v + 1];
+  bounds[4 * i + 2] = m.v2f_off[v];
+  bounds[4 * i + 3] = m.v2f_off[v + 1];
+  pos[3 * i + 0] = m.px[v];
+  pos[3 * i + 1] = m.py[v];
+  pos[3 * i + 2] = m.pz[v];
+}
+
+__global__ void k_gather_vrows(MeshRows m, const int* bounds, const int* dst, int n, unsigned* rows) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int o = dst[i];
+  for (int k = bounds[4 * i]; k < bounds[4 * i + 1]; ++k) rows[o++] = static_cast<unsigned>(m.v2v[k]);
+  for (int k = bounds[4 * i + 2]; k < bounds[4 * i + 3]; ++k) rows[o++] = static_cast<unsigned>(m.v2f[k]);
+}
+
+__global__ void k_gather_faces(MeshRows m, const unsigned* list, int n, unsigned* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const size_t f = list[i];
+  for (int c = 0; c < 3; ++c) {
+    out[6 * i + c] = m.faces[3 * f + c];
+    out[6 * i + 3 + c] = m.face_edges[3 * f + c];
+  }
+}
+
+__global__ void k_gather_edges(MeshRows m, const unsigned* list, int n, unsigned* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const size_t e = list[i];
+  out[4 * i + 0] = m.edges[2 * e];
+  out[4 * i + 1] = m.edges[2 * e + 1];
+  out[4 * i + 2] = m.edge_faces[2 * e];
+  out[4 * i + 3] = m.edge_faces[2 * e + 1];
+}
+
+int launch_gather_vhead(const MeshRows& m, const unsigned* list, int n, int* bounds, double* pos, void* stream) {
+  if (n <= 0) return 0;
+  k_gather_vhead<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(m, list, n, bounds, pos);
+  note_launch();
+  return static_cast<int>(cudaGetLastError());
+}
+int launch_gather_vrows(const MeshRows& m, const int* bounds, const int* dst, int n, unsigned* rows, void* stream) {
+  if (n <= 0) return 0;
+  k_gather_vrows<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(m, bounds, dst, n, rows);
+  note_launch();
+  return static_cast<int>(cudaGetLastError());
+}
+int launch_gather_faces(const MeshRows& m, const unsigned* list, int n, unsigned* out, void* stream) {
+  if (n <= 0) return 0;
+  k_gather_faces<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(m, list, n, out);
+  note_launch();
+  return static_cast<int>(cudaGetLastError());
+}
+int launch_gather_edges(const MeshRows& m, const unsigned* list, int n, unsigned* out, void* stream) {
+  if (n <= 0) return 0;
+  k_gather_edges<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(m, list, n, out);
+  note_launch();
+  return static_cast<int>(cudaGetLastError());
+}
+
 }  // namespace dtb

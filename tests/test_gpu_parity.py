@@ -179,3 +179,25 @@ def test_trail_snap_overflow_list_matches_segments(spec, steps, monkeypatch):
     for x, y in zip(ta, tb):
         assert x["layer"] == y["layer"]
         np.testing.assert_array_equal(np.asarray(x["trail"]), np.asarray(y["trail"]))
+
+
+@pytest.mark.parametrize("spec,steps", [("torus:48:24:3:1.2", 2000), ("genus:2:3", 1500)])
+def test_device_built_mesh_events_match_reference(spec, steps, monkeypatch, capfd):
+    """A device-built mesh (from_arrays) has no host copy: its splits, merges,
+    vanishes and handle loops are computed from local gathers of the rows,
+    faces and edges they touch -- bit-exact with the reference, and without
+    downloading the whole mesh."""
+    host = dt.TriangleMesh.generate(spec)
+    mesh = dt.TriangleMesh.from_arrays(host.vertices(), host.faces())
+    op, _ = ref_operator(mesh, spec)
+    monkeypatch.setenv("DTB_TIMING", "1")
+    res = dt.run_initial_pass(mesh, op, 0, dt.default_config(max_steps=steps, record_hashes=1))
+    monkeypatch.delenv("DTB_TIMING")
+    assert "host mesh download" not in capfd.readouterr().err
+    ref = refdata.ref_run(spec, max_steps=steps)
+    assert len(ref["events"]) > 5
+    mine, theirs = [int(h) for h in res.hashes()], [int(h) for h in ref["hashes"]]
+    first_bad = next((i for i, (a, b) in enumerate(zip(mine, theirs)) if a != b), None)
+    assert first_bad is None and len(mine) == len(theirs), first_bad
+    parity.compare_events(res.events(), ref["events"])
+    parity.compare_tracks(res.tracks(), ref["tracks"])
