@@ -69,6 +69,10 @@ void dtb_coefficients_default(dtb_coefficients* c);
 const char* dtb_last_error(void);
 const char* dtb_version(void);
 int dtb_device_info(int* device_count, int* sm_count, int* cc_major, int* cc_minor);
+/* Library initialisation (no reference counterpart): one small end-to-end call
+ * through the device paths, so the context exists and every kernel is loaded
+ * before the caller's first timed call.  Optional. */
+int dtb_warmup(void);
 
 /* ---- mesh (mesh.hpp, generators.hpp, mesh_io.hpp) ---------------------- */
 /* TriangleMesh(vertices, faces) (mesh.hpp:150): validates, orients, indexes. */

@@ -73,6 +73,7 @@ def load_library(path: str = LIB_PATH):
         "dtb_coefficients_default": (None, [C.POINTER(Coefficients)]),
         "dtb_last_error": (C.c_char_p, []),
         "dtb_version": (C.c_char_p, []),
+        "dtb_warmup": (C.c_int, []),
         "dtb_device_info": (C.c_int, [pI32, pI32, pI32, pI32]),
         "dtb_mesh_from_arrays": (C.c_int, [pD, U32, pU32, U32, pP]),
         "dtb_mesh_generate": (C.c_int, [C.c_char_p, pP]),
@@ -185,6 +186,12 @@ def device_info():
     rc = lib.dtb_device_info(C.byref(n), C.byref(sms), C.byref(ma), C.byref(mi))
     _check(rc)
     return {"devices": n.value, "sms": sms.value, "cc": (ma.value, mi.value)}
+
+
+def warmup():
+    """Creates the CUDA context and loads the library's kernels with one small
+    end-to-end call (dtb_warmup), so the first real call is not a cold one."""
+    _check(load_library().dtb_warmup())
 
 
 class TriangleMesh:

@@ -185,6 +185,38 @@ int dtb_device_info(int* count, int* sms, int* major, int* minor) {
   });
 }
 
+int dtb_warmup(void) {
+  return guard([&] {
+    // One small end-to-end call through the device paths (mesh build from a
+    // soup, assembly, a pass with split/merge events): creates the context
+    // and loads every kernel those paths use (CUDA loads kernels lazily, on
+    // first launch), so a caller's first real call does not pay for it.
+    const Mesh h = make_mesh("torus:32:16:2:0.5");
+    std::vector<double> xyz(3 * static_cast<size_t>(h.nv()));
+    for (Index v = 0; v < h.nv(); ++v) {
+      xyz[3 * v] = h.p(v).x;
+      xyz[3 * v + 1] = h.p(v).y;
+      xyz[3 * v + 2] = h.p(v).z;
+    }
+    std::vector<std::uint32_t> f(3 * static_cast<size_t>(h.nf()));
+    for (Index i = 0; i < h.nf(); ++i)
+      for (int c = 0; c < 3; ++c) f[3 * i + c] = h.face(i)[c];
+    cudaStream_t s = nullptr;
+    cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    {
+      std::shared_ptr<DeviceMesh> dm = DeviceMesh::from_soup(xyz.data(), h.nv(), f.data(), h.nf(), s);
+      if (!dm) dm = std::make_shared<DeviceMesh>(std::make_shared<Mesh>(h), s);
+      DeviceLaplacian op(dm, s);
+      Config cfg;
+      cfg.max_steps = 400;
+      InitialPassResult r = run_initial_pass(dm, op, 0, cfg, Coefficients{});
+      (void)r;
+    }
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  });
+}
+
 // ---- mesh
 int dtb_mesh_from_arrays(const double* xyz, uint32_t nv, const uint32_t* faces, uint32_t nf, dtb_mesh** out) {
   return guard([&] {

@@ -26,7 +26,11 @@ namespace {
 std::mutex g_alloc_mu;
 std::multimap<size_t, void*> g_free_blocks;  // size class -> block
 size_t g_cached_bytes = 0;
-constexpr size_t kCacheBytes = size_t(16) << 30;
+constexpr size_t kCacheBytes = size_t(16) << 30;  // cached large blocks (carved small ones are not counted)
+constexpr size_t kSubMax = size_t(4) << 20;        // size classes carved from chunks
+constexpr size_t kChunk = size_t(256) << 20;
+char* g_bump = nullptr;
+size_t g_bump_left = 0;
 
 size_t size_class(size_t bytes) {
   if (bytes <= 4096) return 4096;
@@ -63,18 +67,41 @@ void* dev_alloc(size_t bytes) {
     if (it != g_free_blocks.end()) {
       void* p = it->second;
       g_free_blocks.erase(it);
-      g_cached_bytes -= c;
+      if (c > kSubMax) g_cached_bytes -= c;
       return p;
     }
   }
   void* p = nullptr;
+  if (c <= kSubMax) {
+    // Small blocks are carved from 256 MiB chunks: a workspace is ~40
+    // buffers, and a cudaMalloc per buffer made a cold batch of 64 passes
+    // spend most of its time in the driver.  Carved blocks return to the
+    // cache, never to the driver.
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    if (g_bump_left < c) {
+      void* chunk = nullptr;
+      cuda_check(cudaMalloc(&chunk, kChunk), "cudaMalloc");
+      g_bump = static_cast<char*>(chunk);
+      g_bump_left = kChunk;
+    }
+    p = g_bump;
+    g_bump += c;
+    g_bump_left -= c;
+    return p;
+  }
   cudaError_t e = cudaMalloc(&p, c);
   if (e != cudaSuccess) {
     // Out of memory with blocks parked in the cache: release them and retry.
     std::lock_guard<std::mutex> lk(g_alloc_mu);
-    for (auto& kv : g_free_blocks) cudaFree(kv.second);
-    g_free_blocks.clear();
-    g_cached_bytes = 0;
+    for (auto it = g_free_blocks.begin(); it != g_free_blocks.end();) {
+      if (it->first <= kSubMax) {  // carved from a chunk: stays cached
+        ++it;
+        continue;
+      }
+      cudaFree(it->second);
+      g_cached_bytes -= it->first;
+      it = g_free_blocks.erase(it);
+    }
     cudaGetLastError();
     e = cudaMalloc(&p, c);
   }
@@ -85,6 +112,10 @@ void* dev_alloc(size_t bytes) {
 void dev_free(void* p, size_t bytes) {
   const size_t c = size_class(bytes);
   std::lock_guard<std::mutex> lk(g_alloc_mu);
+  if (c <= kSubMax) {
+    g_free_blocks.emplace(c, p);
+    return;
+  }
   if (g_cached_bytes + c > kCacheBytes) {
     cudaFree(p);
     return;
