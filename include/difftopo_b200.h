@@ -118,7 +118,10 @@ int dtb_run_initial_pass(const dtb_mesh* m, const dtb_laplacian* op, uint32_t se
 /* Batch of independent initial passes on this GPU (BASELINE configs[4]):
  * item i runs run_initial_pass(meshes[i], ops[i], seeds[i] (0 if seeds is
  * NULL)) exactly as dtb_run_initial_pass would, up to `concurrency` passes at
- * once (<= 0: 8), each a persistent kernel on its own stream over
+ * once (<= 0: 16 when the context has >= 16 hardware work queues and the
+ * host >= 16 threads, else 8; loading the library sets
+ * CUDA_DEVICE_MAX_CONNECTIONS=32 when unset and no CUDA context can exist
+ * yet), each a persistent kernel on its own stream over
  * cfg->grid_ctas CTAs (0: SMs / concurrency).  out[i] receives the result
  * (NULL on failure) and rc[i] (optional) its code; the return value is the
  * first failing item's code.  Replaces a caller's loop over

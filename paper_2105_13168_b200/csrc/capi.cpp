@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <dlfcn.h>
 #include <memory>
 #include <string>
 #include <thread>
@@ -71,7 +72,36 @@ namespace {
 
 thread_local std::string g_err;
 // Default number of passes a batch runs at once (each on SMs / lanes CTAs).
+// Concurrent persistent passes need one hardware work queue each: the context
+// has CUDA_DEVICE_MAX_CONNECTIONS of them (8 unless set), and passes whose
+// streams share a queue run one after the other. With 32 queues, 16 lanes of
+// 9 CTAs run the 64-mesh batch in 0.50 s against 0.68 s for 8 lanes of 18
+// (tools/batch_probe.py, DESIGN "Batches").
 constexpr int kBatchLanes = 8;
+constexpr int kBatchLanesWide = 16;
+int g_connections = 8;  // work queues the CUDA context is (or will be) created with
+
+// Runs when the library is loaded. The variable is read once, at context
+// creation; a context can only exist if libcuda is already mapped, so the
+// default is raised only when it is not (and the user did not set it).
+__attribute__((constructor)) void dtb_init_connections() {
+  if (const char* e = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS")) {
+    g_connections = std::max(1, std::min(32, std::atoi(e)));
+    return;
+  }
+  if (void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD)) {
+    dlclose(h);
+    return;
+  }
+  setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
+  g_connections = 32;
+}
+
+int default_batch_lanes() {
+  const int cpus = static_cast<int>(std::thread::hardware_concurrency());
+  if (g_connections >= kBatchLanesWide && (cpus == 0 || cpus >= kBatchLanesWide)) return kBatchLanesWide;
+  return kBatchLanes;
+}
 
 template <class F>
 int guard(F&& f) {
@@ -480,7 +510,7 @@ int dtb_run_initial_pass_batch(const dtb_mesh* const* meshes, const dtb_laplacia
     int dev = 0, sms = 0;
     cuda_check(cudaGetDevice(&dev), "device");
     cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms");
-    const int lanes = std::max(1, std::min<int>(concurrency > 0 ? concurrency : kBatchLanes, n));
+    const int lanes = std::max(1, std::min<int>(concurrency > 0 ? concurrency : default_batch_lanes(), n));
     Config base = to_cfg(cfg);
     // Each pass is a persistent cooperative kernel on its own stream; the
     // concurrent passes split the SMs between them.
