@@ -73,6 +73,14 @@ int dtb_device_info(int* device_count, int* sm_count, int* cc_major, int* cc_min
  * through the device paths, so the context exists and every kernel is loaded
  * before the caller's first timed call.  Optional. */
 int dtb_warmup(void);
+/* Opt-in (no reference counterpart): asks for `queues` hardware work queues
+ * (1..32) in the CUDA context this process has not created yet, by setting
+ * CUDA_DEVICE_MAX_CONNECTIONS when the caller left it unset.  Concurrent batch
+ * passes each hold a queue for their whole run, so 32 lets 16 run at once.
+ * Fails with DTB_EINVAL when a CUDA context may already exist (libcuda is
+ * mapped); call it first thing, before any CUDA use.  The library itself never
+ * changes the variable. */
+int dtb_init_work_queues(int32_t queues);
 
 /* ---- mesh (mesh.hpp, generators.hpp, mesh_io.hpp) ---------------------- */
 /* TriangleMesh(vertices, faces) (mesh.hpp:150): validates, orients, indexes. */
@@ -118,10 +126,9 @@ int dtb_run_initial_pass(const dtb_mesh* m, const dtb_laplacian* op, uint32_t se
 /* Batch of independent initial passes on this GPU (BASELINE configs[4]):
  * item i runs run_initial_pass(meshes[i], ops[i], seeds[i] (0 if seeds is
  * NULL)) exactly as dtb_run_initial_pass would, up to `concurrency` passes at
- * once (<= 0: 16 when the context has >= 16 hardware work queues and the
- * host >= 16 threads, else 8; loading the library sets
- * CUDA_DEVICE_MAX_CONNECTIONS=32 when unset and no CUDA context can exist
- * yet), each a persistent kernel on its own stream over
+ * once (<= 0: 16 when CUDA_DEVICE_MAX_CONNECTIONS asks for >= 16 hardware
+ * work queues -- see dtb_init_work_queues -- and the host has >= 16 threads,
+ * else 8), each a persistent kernel on its own stream over
  * cfg->grid_ctas CTAs (0: SMs / concurrency).  out[i] receives the result
  * (NULL on failure) and rc[i] (optional) its code; the return value is the
  * first failing item's code.  Replaces a caller's loop over

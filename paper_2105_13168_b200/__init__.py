@@ -74,6 +74,7 @@ def load_library(path: str = LIB_PATH):
         "dtb_last_error": (C.c_char_p, []),
         "dtb_version": (C.c_char_p, []),
         "dtb_warmup": (C.c_int, []),
+        "dtb_init_work_queues": (C.c_int, [I32]),
         "dtb_device_info": (C.c_int, [pI32, pI32, pI32, pI32]),
         "dtb_mesh_from_arrays": (C.c_int, [pD, U32, pU32, U32, pP]),
         "dtb_mesh_generate": (C.c_int, [C.c_char_p, pP]),
@@ -186,6 +187,14 @@ def device_info():
     rc = lib.dtb_device_info(C.byref(n), C.byref(sms), C.byref(ma), C.byref(mi))
     _check(rc)
     return {"devices": n.value, "sms": sms.value, "cc": (ma.value, mi.value)}
+
+
+def init_work_queues(queues: int = 32):
+    """Opt-in: request `queues` hardware work queues for the CUDA context this
+    process is about to create (dtb_init_work_queues; concurrent batch passes
+    hold one each).  Must run before any CUDA use; raises if a context may
+    already exist."""
+    _check(load_library().dtb_init_work_queues(int(queues)))
 
 
 def warmup():

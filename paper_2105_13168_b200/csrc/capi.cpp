@@ -79,27 +79,19 @@ thread_local std::string g_err;
 // (tools/batch_probe.py, DESIGN "Batches").
 constexpr int kBatchLanes = 8;
 constexpr int kBatchLanesWide = 16;
-int g_connections = 8;  // work queues the CUDA context is (or will be) created with
-
-// Runs when the library is loaded. The variable is read once, at context
-// creation; a context can only exist if libcuda is already mapped, so the
-// default is raised only when it is not (and the user did not set it).
-__attribute__((constructor)) void dtb_init_connections() {
-  if (const char* e = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS")) {
-    g_connections = std::max(1, std::min(32, std::atoi(e)));
-    return;
-  }
-  if (void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD)) {
-    dlclose(h);
-    return;
-  }
-  setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
-  g_connections = 32;
+// Hardware work queues of the CUDA context: CUDA_DEVICE_MAX_CONNECTIONS as
+// the caller set it (read when a batch starts, i.e. after the caller had its
+// chance to set it before creating the context), 8 when unset.  The library
+// never changes the variable on its own; dtb_init_work_queues is the opt-in.
+int context_work_queues() {
+  const char* e = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+  const int q = e ? std::atoi(e) : 8;
+  return std::max(1, std::min(32, q > 0 ? q : 8));
 }
 
 int default_batch_lanes() {
   const int cpus = static_cast<int>(std::thread::hardware_concurrency());
-  if (g_connections >= kBatchLanesWide && (cpus == 0 || cpus >= kBatchLanesWide)) return kBatchLanesWide;
+  if (context_work_queues() >= kBatchLanesWide && (cpus == 0 || cpus >= kBatchLanesWide)) return kBatchLanesWide;
   return kBatchLanes;
 }
 
@@ -215,6 +207,20 @@ int dtb_device_info(int* count, int* sms, int* major, int* minor) {
   });
 }
 
+int dtb_init_work_queues(int32_t queues) {
+  return guard([&] {
+    if (queues < 1 || queues > 32) fail(kInvalidParameter, "work queues must be in [1, 32]");
+    // The variable is read once, when the CUDA context is created; a context
+    // can only exist if libcuda is already mapped.
+    if (void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD)) {
+      dlclose(h);
+      fail(kInvalidParameter, "a CUDA context may already exist; set CUDA_DEVICE_MAX_CONNECTIONS before it is created");
+    }
+    if (std::getenv("CUDA_DEVICE_MAX_CONNECTIONS")) return;  // the caller's own setting wins
+    setenv("CUDA_DEVICE_MAX_CONNECTIONS", std::to_string(queues).c_str(), 0);
+  });
+}
+
 int dtb_warmup(void) {
   return guard([&] {
     // One small end-to-end call through the device paths (mesh build from a
@@ -231,19 +237,24 @@ int dtb_warmup(void) {
     std::vector<std::uint32_t> f(3 * static_cast<size_t>(h.nf()));
     for (Index i = 0; i < h.nf(); ++i)
       for (int c = 0; c < 3; ++c) f[3 * i + c] = h.face(i)[c];
-    cudaStream_t s = nullptr;
-    cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-    {
-      std::shared_ptr<DeviceMesh> dm = DeviceMesh::from_soup(xyz.data(), h.nv(), f.data(), h.nf(), s);
-      if (!dm) dm = std::make_shared<DeviceMesh>(std::make_shared<Mesh>(h), s);
-      DeviceLaplacian op(dm, s);
-      Config cfg;
-      cfg.max_steps = 400;
-      InitialPassResult r = run_initial_pass(dm, op, 0, cfg, Coefficients{});
-      (void)r;
-    }
-    cudaStreamSynchronize(s);
-    cudaStreamDestroy(s);
+    struct StreamGuard {  // destroyed on every exit path, including a throw
+      cudaStream_t s = nullptr;
+      ~StreamGuard() {
+        if (s) {
+          cudaStreamSynchronize(s);
+          cudaStreamDestroy(s);
+        }
+      }
+    } g;
+    cuda_check(cudaStreamCreateWithFlags(&g.s, cudaStreamNonBlocking), "stream");
+    cudaStream_t s = g.s;
+    std::shared_ptr<DeviceMesh> dm = DeviceMesh::from_soup(xyz.data(), h.nv(), f.data(), h.nf(), s);
+    if (!dm) dm = std::make_shared<DeviceMesh>(std::make_shared<Mesh>(h), s);
+    DeviceLaplacian op(dm, s);
+    Config cfg;
+    cfg.max_steps = 400;
+    InitialPassResult r = run_initial_pass(dm, op, 0, cfg, Coefficients{});
+    (void)r;
   });
 }
 

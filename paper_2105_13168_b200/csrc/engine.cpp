@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <numeric>
 #include <queue>
 #include <unordered_set>
@@ -31,6 +32,21 @@ constexpr size_t kSubMax = size_t(4) << 20;        // size classes carved from c
 constexpr size_t kChunk = size_t(256) << 20;
 char* g_bump = nullptr;
 size_t g_bump_left = 0;
+
+// Returns the cached large blocks to the driver (caller holds g_alloc_mu).
+// Blocks carved from chunks stay cached: they cannot be freed one by one.
+void release_cached_large_locked() {
+  for (auto it = g_free_blocks.begin(); it != g_free_blocks.end();) {
+    if (it->first <= kSubMax) {
+      ++it;
+      continue;
+    }
+    cudaFree(it->second);
+    g_cached_bytes -= it->first;
+    it = g_free_blocks.erase(it);
+  }
+  cudaGetLastError();
+}
 
 size_t size_class(size_t bytes) {
   if (bytes <= 4096) return 4096;
@@ -79,8 +95,23 @@ void* dev_alloc(size_t bytes) {
     // cache, never to the driver.
     std::lock_guard<std::mutex> lk(g_alloc_mu);
     if (g_bump_left < c) {
+      // The rest of the current chunk goes back to the cache as the largest
+      // power-of-two classes it holds (the bump pointer stays 4 KiB aligned).
+      while (g_bump_left >= 4096) {
+        size_t b = 4096;
+        while (b * 2 <= g_bump_left && b * 2 <= kSubMax) b *= 2;
+        g_free_blocks.emplace(b, g_bump);
+        g_bump += b;
+        g_bump_left -= b;
+      }
       void* chunk = nullptr;
-      cuda_check(cudaMalloc(&chunk, kChunk), "cudaMalloc");
+      cudaError_t e = cudaMalloc(&chunk, kChunk);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        release_cached_large_locked();
+        e = cudaMalloc(&chunk, kChunk);
+      }
+      cuda_check(e, "cudaMalloc");
       g_bump = static_cast<char*>(chunk);
       g_bump_left = kChunk;
     }
@@ -93,16 +124,8 @@ void* dev_alloc(size_t bytes) {
   if (e != cudaSuccess) {
     // Out of memory with blocks parked in the cache: release them and retry.
     std::lock_guard<std::mutex> lk(g_alloc_mu);
-    for (auto it = g_free_blocks.begin(); it != g_free_blocks.end();) {
-      if (it->first <= kSubMax) {  // carved from a chunk: stays cached
-        ++it;
-        continue;
-      }
-      cudaFree(it->second);
-      g_cached_bytes -= it->first;
-      it = g_free_blocks.erase(it);
-    }
     cudaGetLastError();
+    release_cached_large_locked();
     e = cudaMalloc(&p, c);
   }
   cuda_check(e, "cudaMalloc");
@@ -841,12 +864,16 @@ void DeviceMesh::reserve_fields(size_t count, size_t nv, size_t ne) {
     std::lock_guard<std::mutex> lk(g_pool_mu);
     for (DeviceField* f : g_pool) have += f->capacity() >= nv && f->edge_capacity() >= ne;
   }
-  std::vector<DeviceField*> made;
-  for (size_t k = have; k < count; ++k) made.push_back(new DeviceField(static_cast<DeviceMesh*>(nullptr), nullptr, nv, ne));
+  // Owned until they are in the pool: a failing allocation (OOM) must not
+  // leak the workspaces already made.
+  std::vector<std::unique_ptr<DeviceField>> made;
+  for (size_t k = have; k < count; ++k)
+    made.push_back(std::make_unique<DeviceField>(static_cast<DeviceMesh*>(nullptr), nullptr, nv, ne));
   cuda_check(cudaStreamSynchronize(nullptr), "reserve fields");
   std::lock_guard<std::mutex> lk(g_pool_mu);
+  g_pool.reserve(g_pool.size() + made.size());
   // Trim the smallest workspaces first.
-  for (DeviceField* f : made) g_pool.push_back(f);
+  for (auto& f : made) g_pool.push_back(f.release());
   std::stable_sort(g_pool.begin(), g_pool.end(),
                    [](const DeviceField* a, const DeviceField* b) { return a->capacity() < b->capacity(); });
   while (g_pool.size() > std::max(kPoolKeep, count)) {
@@ -859,6 +886,22 @@ namespace {
 int engine_blocks(int nv, int requested = 0);
 }  // namespace
 
+
+void DeviceField::set_grid(int blocks) {
+  const size_t total = bandpairs.n;
+  size_t nseg = static_cast<size_t>(std::max(1, blocks));
+  size_t seg = total / nseg;
+  if (const char* env = std::getenv("DTB_BP_SEG")) {  // tests: short segments exercise the overflow list
+    seg = std::min(total, static_cast<size_t>(std::max(1, std::atoi(env))));
+    nseg = std::min(nseg, total / seg);
+  }
+  nseg = std::min(nseg, bpcount.n);
+  work_.bandpair_cap = static_cast<int>(bp_ovf.n);
+  if (const char* env = std::getenv("DTB_BP_OVF"))  // tests: a tiny overflow list must raise, not truncate
+    work_.bandpair_cap = std::min(work_.bandpair_cap, std::max(0, std::atoi(env)));
+  work_.bp_nseg = static_cast<int>(nseg);
+  work_.bp_seg = static_cast<int>(seg);
+}
 
 void DeviceField::setup(size_t nv_cap, size_t ne_cap) {
   const size_t nv = std::max<size_t>(nv_cap, dm_ ? dm_->nv() : 0);
@@ -884,15 +927,15 @@ void DeviceField::setup(size_t nv_cap, size_t ne_cap) {
   {
     // Trail-snap band items: one segment per engine CTA (twice the CTA's
     // share of the vertices) plus a shared overflow list.
+    // The segment length follows the grid that runs the pass (set_grid): a
+    // batch pass on a few CTAs gets long segments, not 148 short ones.
     const size_t nseg = static_cast<size_t>(engine_blocks(static_cast<int>(nv)));
-    size_t seg = 2 * ((nv + nseg - 1) / nseg) + 64;
-    if (const char* env = std::getenv("DTB_BP_SEG")) seg = static_cast<size_t>(std::max(1, std::atoi(env)));  // tests
+    const size_t seg = 2 * ((nv + nseg - 1) / nseg) + 64;
     bandpairs.alloc(nseg * seg);
     bpcount.alloc(nseg);
     bp_ovf.alloc(2 * nv + 4096);
     bpcount.zero(s_);
-    work_.bp_nseg = static_cast<int>(nseg);
-    work_.bp_seg = static_cast<int>(seg);
+    set_grid(static_cast<int>(nseg));
   }
   parent.alloc(nv * kSlots);
   added.alloc(2 * (nv / 8 + 4096));  // two step-parity halves
@@ -1304,20 +1347,33 @@ int engine_blocks(int nv, int requested) {
   // One 512-thread CTA per SM regardless of mesh size: a step's work is a
   // handful of dependent loads per frontier/band item, so more groups means
   // fewer items per group; the grid barrier costs ~1.2 us at 148 CTAs.
-  static int maxco = 0, sms = 0;
-  if (!maxco) {
-    ck(dev_max_coresident_blocks(&maxco), "occupancy");
-    int dev = 0;
-    cuda_check(cudaGetDevice(&dev), "device");
-    cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "sms");
+  // Occupancy and SM count are cached per device, filled once under a lock.
+  struct Limits {
+    int maxco, sms;
+  };
+  static std::mutex mu;
+  static std::map<int, Limits> cache;
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "device");
+  Limits lim{};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(dev);
+    if (it == cache.end()) {
+      ck(dev_max_coresident_blocks(&lim.maxco), "occupancy");
+      cuda_check(cudaDeviceGetAttribute(&lim.sms, cudaDevAttrMultiProcessorCount, dev), "sms");
+      if (lim.maxco <= 0 || lim.sms <= 0) fail(kCudaError, "the engine kernel cannot be resident on this device");
+      it = cache.emplace(dev, lim).first;
+    }
+    lim = it->second;
   }
   (void)nv;
-  if (requested > 0) return std::min(requested, maxco);
+  if (requested > 0) return std::min(requested, lim.maxco);
   if (const char* env = std::getenv("DTB_BLOCKS")) {
     const int b = std::atoi(env);
-    if (b > 0) return std::min(b, maxco);
+    if (b > 0) return std::min(b, lim.maxco);
   }
-  return std::min(sms, maxco);
+  return std::min(lim.sms, lim.maxco);
 }
 
 std::vector<std::vector<Index>> groups_from_pairs(const std::vector<unsigned>& pairs) {
@@ -1351,11 +1407,11 @@ std::vector<unsigned> read_pairs(const DeviceField& field) {
 void run_check_kernel(DeviceField& field, const Config& cfg, const Coefficients& co, double dt, long s) {
   StepParams p = make_params(field, cfg, co, dt);
   p.step_begin = s;
-  static int maxco = 0;
-  if (!maxco) ck(dev_max_coresident_blocks(&maxco), "occupancy");
-  const int blocks = std::min(maxco, engine_blocks(static_cast<int>(field.mesh().nv()), cfg.grid_ctas));
+  const int blocks = engine_blocks(static_cast<int>(field.mesh().nv()), cfg.grid_ctas);
+  field.set_grid(blocks);
   ck(launch_check(field.mesh().view(), field.view(), field.work(), p, blocks, field.stream()), "check kernel");
   cuda_check(cudaStreamSynchronize(field.stream()), "check sync");
+  if (field.read_ctl().bandpair_overflow) fail(kCapacityExceeded, "band item list overflow (trail snap)");
 }
 
 std::vector<LayerStat> read_stats(const DeviceField& field, long s) {
@@ -1470,6 +1526,7 @@ class PassEngine {
     field_->mark_region(op_.view(), sv, 0, 1);
     tm.mark("pass frontier");
     blocks_ = engine_blocks(static_cast<int>(dm_->nv()), cfg_.grid_ctas);
+    field_->set_grid(blocks_);
     if (const char* env = std::getenv("DTB_PHASE_PROF"); env && env[0] == '1') {
       prof_.alloc(4 * static_cast<size_t>(std::min<long>(cfg_.max_steps, 100000)) + 8 + 2 * 64 * 3 * 160 + 64);
       prof_.zero(s_);
@@ -1602,6 +1659,7 @@ class PassEngine {
         if (c.error == kDevBlowup) fail(kNumericalBlowup, "non-finite rate; reduce dt");
         if (c.error == kDevZeroColumn)
           fail(kZeroColumn, "total field extinction at vertex " + std::to_string(c.error_vertex));
+        if (c.bandpair_overflow) fail(kCapacityExceeded, "band item list overflow (trail snap)");
         fail(kCapacityExceeded, "column capacity exceeded at vertex " + std::to_string(c.error_vertex));
       }
       if (c.stop_bits) {

@@ -250,6 +250,8 @@ class DeviceField {
 
   DevField view() const { return view_; }
   DevWork work() const { return work_; }
+  // Band-item segments for a launch grid of `blocks` CTAs (one per CTA).
+  void set_grid(int blocks);
   DeviceMesh& mesh() { return *dm_; }
   const DeviceMesh& mesh() const { return *dm_; }
   cudaStream_t stream() const { return s_; }

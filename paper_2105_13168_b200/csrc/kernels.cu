@@ -1898,7 +1898,10 @@ __device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& 
             } else {
               const int o = obase + __popc(om & ((1u << lane) - 1u));
               if (o < W.bandpair_cap) W.bp_ovf[o] = make_int2(v, a);
-              else W.ctl->bandpair_overflow = 1;
+              else {
+                W.ctl->bandpair_overflow = 1;  // the trail snap would miss items: a capacity error
+                raise_error(W.ctl, kDevCapacity, v, false);
+              }
             }
           }
         }

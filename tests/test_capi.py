@@ -71,22 +71,30 @@ def test_cpp_facade_compiles(tmp_path):
 
 _CONN_PROBE = (
     "import ctypes, sys; sys.path.insert(0, {root!r}); import paper_2105_13168_b200 as dt; dt.load_library(); "
+    "{init}"
     "libc = ctypes.CDLL(None); libc.getenv.restype = ctypes.c_char_p; "
-    "print((libc.getenv(b'CUDA_DEVICE_MAX_CONNECTIONS') or b'').decode())"
+    "print((libc.getenv(b'CUDA_DEVICE_MAX_CONNECTIONS') or b'-').decode())"
 )
 
 
-@pytest.mark.parametrize("preset,expect", [(None, "32"), ("4", "4")])
-def test_library_load_sets_work_queues_for_batches(preset, expect):
-    """Loading the library before any CUDA context raises the context's
-    hardware work queues to 32 (concurrent batch passes, capi.cpp
-    dtb_init_connections); a value the caller set is kept."""
+@pytest.mark.parametrize("preset,init,expect", [(None, False, "-"), (None, True, "32"), ("4", True, "4")])
+def test_work_queues_are_opt_in(preset, init, expect):
+    """Loading the library leaves CUDA_DEVICE_MAX_CONNECTIONS alone;
+    dtb_init_work_queues (before any CUDA context) sets it when the caller
+    left it unset, and a value the caller set is kept."""
     import subprocess
     import sys
     env = {k: v for k, v in os.environ.items() if k != "CUDA_DEVICE_MAX_CONNECTIONS"}
     if preset is not None:
         env["CUDA_DEVICE_MAX_CONNECTIONS"] = preset
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    out = subprocess.run([sys.executable, "-c", _CONN_PROBE.format(root=root)], env=env, capture_output=True,
-                         text=True, check=True, timeout=120)
+    code = _CONN_PROBE.format(root=root, init="dt.init_work_queues(32); " if init else "")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, check=True,
+                         timeout=120)
     assert out.stdout.strip() == expect
+
+
+def test_work_queues_rejects_bad_count():
+    import paper_2105_13168_b200 as dt
+    with pytest.raises(dt.DiffTopoError):
+        dt.init_work_queues(0)

@@ -181,6 +181,19 @@ def test_trail_snap_overflow_list_matches_segments(spec, steps, monkeypatch):
         np.testing.assert_array_equal(np.asarray(x["trail"]), np.asarray(y["trail"]))
 
 
+def test_trail_snap_overflow_raises_capacity_error(monkeypatch):
+    """When the band items of a check fill both the segments and the overflow
+    list, the pass fails with a capacity error instead of snapping trails from
+    a truncated list (the stop used to look like an ordinary event)."""
+    mesh = dt.TriangleMesh.generate("torus:32:16:2:0.5")
+    op = dt.assemble_laplacian(mesh)
+    monkeypatch.setenv("DTB_BP_SEG", "1")
+    monkeypatch.setenv("DTB_BP_OVF", "2")
+    res = dt.run_initial_pass(mesh, op, 0, dt.default_config(max_steps=300))
+    assert res.status == "CapacityExceeded"
+    assert "band item list overflow" in res.message
+
+
 @pytest.mark.parametrize("spec,steps", [("torus:48:24:3:1.2", 2000), ("genus:2:3", 1500)])
 def test_device_built_mesh_events_match_reference(spec, steps, monkeypatch, capfd):
     """A device-built mesh (from_arrays) has no host copy: its splits, merges,

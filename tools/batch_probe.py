@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--n", type=int, default=64)
     ap.add_argument("--ctas", default="0", help="grid CTAs per pass (0: SMs / lanes)")
     a = ap.parse_args()
+    dt.init_work_queues(32)  # opt-in, before any CUDA use
     specs = shard.batch_specs(a.n, 32, 3)
     meshes = [dt.TriangleMesh.generate(s) for s in specs]
     ops = [dt.assemble_laplacian(m) for m in meshes]

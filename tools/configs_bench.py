@@ -79,7 +79,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     dist = None
-    dt.load_library()  # before any CUDA context: the library raises CUDA_DEVICE_MAX_CONNECTIONS for batches
+    dt.init_work_queues(32)  # opt-in, before any CUDA context: 32 hardware queues for concurrent batch passes
     if world > 1:
         import torch
         import torch.distributed as tdist
