@@ -888,15 +888,15 @@ int engine_blocks(int nv, int requested = 0);
 
 
 void DeviceField::set_grid(int blocks) {
-  const size_t total = bandpairs.n;
+  const size_t total = bandpairs[0].n;
   size_t nseg = static_cast<size_t>(std::max(1, blocks));
   size_t seg = total / nseg;
   if (const char* env = std::getenv("DTB_BP_SEG")) {  // tests: short segments exercise the overflow list
     seg = std::min(total, static_cast<size_t>(std::max(1, std::atoi(env))));
     nseg = std::min(nseg, total / seg);
   }
-  nseg = std::min(nseg, bpcount.n);
-  work_.bandpair_cap = static_cast<int>(bp_ovf.n);
+  nseg = std::min(nseg, bpcount[0].n);
+  work_.bandpair_cap = static_cast<int>(bp_ovf[0].n);
   if (const char* env = std::getenv("DTB_BP_OVF"))  // tests: a tiny overflow list must raise, not truncate
     work_.bandpair_cap = std::min(work_.bandpair_cap, std::max(0, std::atoi(env)));
   work_.bp_nseg = static_cast<int>(nseg);
@@ -909,43 +909,52 @@ void DeviceField::setup(size_t nv_cap, size_t ne_cap) {
   if (nv * kSlots >= 0xFFFFFFFFull) fail(kCapacityExceeded, "more than 134M vertices (32-bit union-find items)");
   cap_ = nv;
   cap_e_ = ne;
-  cnt.alloc(nv);
-  interest.alloc(nv);
-  scnt.alloc(nv);
-  sbinfo.alloc(nv);
-  sflag.alloc(nv);
-  lay.alloc(nv * kSlots);
-  slay.alloc(nv * kSlots);
-  val.alloc(nv * kSlots);
-  sval.alloc(nv * kSlots);
-  region0.alloc(nv);
-  region1.alloc(nv);
+  for (int q = 0; q < 2; ++q) {
+    cnt[q].alloc(nv);
+    interest[q].alloc(nv);
+    binfo[q].alloc(nv);
+    lay[q].alloc(nv * kSlots);
+    val[q].alloc(nv * kSlots);
+    view_.b[q].cnt = cnt[q].p;
+    view_.b[q].lay = lay[q].p;
+    view_.b[q].val = val[q].p;
+    view_.b[q].interest = interest[q].p;
+    view_.b[q].binfo = binfo[q].p;
+  }
+  for (int q = 0; q < 4; ++q) {
+    region[q].alloc(nv);
+    ilist[q].alloc(nv);
+    work_.region[q] = region[q].p;
+    work_.ilist[q] = ilist[q].p;
+  }
   stamp.alloc(nv);
-  ilist0.alloc(nv);
-  ilist1.alloc(nv);
-  in_list.alloc(nv);
   {
-    // Trail-snap band items: one segment per engine CTA (twice the CTA's
-    // share of the vertices) plus a shared overflow list.
-    // The segment length follows the grid that runs the pass (set_grid): a
-    // batch pass on a few CTAs gets long segments, not 148 short ones.
+    // Trail-snap band items (two sets, by check parity): one segment per
+    // engine CTA (twice the CTA's share of the vertices) plus an overflow
+    // list.  The segment length follows the grid that runs the pass
+    // (set_grid): a batch pass on a few CTAs gets long segments.
     const size_t nseg = static_cast<size_t>(engine_blocks(static_cast<int>(nv)));
     const size_t seg = 2 * ((nv + nseg - 1) / nseg) + 64;
-    bandpairs.alloc(nseg * seg);
-    bpcount.alloc(nseg);
-    bp_ovf.alloc(2 * nv + 4096);
-    bpcount.zero(s_);
+    for (int q = 0; q < 2; ++q) {
+      bandpairs[q].alloc(nseg * seg);
+      bpcount[q].alloc(nseg);
+      bp_ovf[q].alloc(2 * nv + 4096);
+      bpcount[q].zero(s_);
+      work_.bandpairs[q] = bandpairs[q].p;
+      work_.bpcount[q] = bpcount[q].p;
+      work_.bp_ovf[q] = bp_ovf[q].p;
+    }
     set_grid(static_cast<int>(nseg));
   }
   parent.alloc(nv * kSlots);
-  added.alloc(2 * (nv / 8 + 4096));  // two step-parity halves
+  added.alloc(4 * (nv / 8 + 4096));  // four step slots
   add_stamp.alloc(nv);
   active.alloc(kMaxLayers + 1);
   aidx.alloc(kMaxLayers + 1);
   alist.alloc(kMaxActive);
-  stat.alloc(2 * static_cast<size_t>(kMaxActive));
+  stat.alloc(4 * static_cast<size_t>(kMaxActive));
   pair_keys.alloc(kPairCap);
-  pairs.alloc(kPairCap);
+  pairs.alloc(4 * static_cast<size_t>(kPairCap));
   lastpos.alloc(4 * static_cast<size_t>(kMaxLayers + 1));
   // Trail ring: 8 records per vertex, between 2^16 and kTrailCap (a launch
   // stops before it can wrap, see advance_until_event).
@@ -959,27 +968,7 @@ void DeviceField::setup(size_t nv_cap, size_t ne_cap) {
   lastpos.zero(s_);
   ctl.zero(s_);
   active.zero(s_);
-  view_.cnt = cnt.p;
-  view_.lay = lay.p;
-  view_.val = val.p;
-  view_.interest = interest.p;
-  work_.region[0] = region0.p;
-  work_.region[1] = region1.p;
   work_.stamp = stamp.p;
-  work_.scnt = scnt.p;
-  work_.sbinfo = sbinfo.p;
-  work_.slay = slay.p;
-  work_.sval = sval.p;
-  work_.sflag = sflag.p;
-  work_.ilist[0] = ilist0.p;
-  work_.ilist[1] = ilist1.p;
-  work_.in_list = in_list.p;
-  work_.bandpairs = bandpairs.p;
-  work_.bpcount = bpcount.p;
-  work_.bp_ovf = bp_ovf.p;
-  work_.bandpair_cap = static_cast<int>(bp_ovf.n);
-  binfo.alloc(nv);
-  view_.binfo = binfo.p;
   // Event-time scratch (layer pulls, isoline crossings, edits): allocated once
   // so host event handling never calls cudaMalloc/cudaFree.
   const size_t ncap = std::max<size_t>(nv, ne) + 1;
@@ -991,7 +980,7 @@ void DeviceField::setup(size_t nv_cap, size_t ne_cap) {
   acnt.alloc(16);
   work_.parent = parent.p;
   work_.added = added.p;
-  work_.added_cap = static_cast<int>(added.n / 2);
+  work_.added_cap = static_cast<int>(added.n / 4);
   work_.add_stamp = add_stamp.p;
   work_.active = active.p;
   work_.aidx = aidx.p;
@@ -1123,11 +1112,18 @@ void DeviceField::normalize_columns() {
   if (read_ctl().error == kDevZeroColumn) fail(kZeroColumn, "total field extinction at a vertex");
 }
 
-void DeviceField::mark_region(const DevMesh& op_view, const std::vector<int>& verts, long stamp_value, int parity) {
+void DeviceField::mark_region(const DevMesh& op_view, const std::vector<int>& verts, long stamp_value) {
   if (verts.empty()) return;
   ai1.upload(verts.data(), verts.size(), s_);
-  ck(launch_mark_region(op_view, work_, ai1.p, static_cast<int>(verts.size()), stamp_value, parity, s_), "mark region");
+  ck(launch_mark_region(op_view, work_, ai1.p, static_cast<int>(verts.size()), stamp_value, slot4(stamp_value + 1), s_),
+     "mark region");
   cuda_check(cudaStreamSynchronize(s_), "mark region sync");
+}
+
+void DeviceField::rebuild_band_list(long t) {
+  const int q = slot4(t);
+  cuda_check(cudaMemsetAsync(&ctl.p->ilcount[q], 0, sizeof(int), s_), "memset");
+  ck(launch_rebuild_list(view_, work_, static_cast<int>(dm_->nv()), q, s_), "band list");
 }
 
 std::vector<Index> DeviceField::split_layer(Index layer, const std::vector<std::vector<Index>>& comps, long step_) {
@@ -1396,10 +1392,18 @@ std::vector<std::vector<Index>> groups_from_pairs(const std::vector<unsigned>& p
   return out;
 }
 
-std::vector<unsigned> read_pairs(const DeviceField& field) {
+std::vector<unsigned> read_pairs(const DeviceField& field, long s) {
   const Ctl c = field.read_ctl();
-  if (c.pair_overflow) fail(kCapacityExceeded, "collision pair table overflow");
-  return to_host(field.pairs, static_cast<size_t>(c.npairs), field.stream());
+  const int q = slot4(s);
+  if (c.pair_overflow[q]) fail(kCapacityExceeded, "collision pair table overflow");
+  std::vector<unsigned> out(static_cast<size_t>(c.npairs[q]));
+  if (!out.empty()) {
+    cuda_check(cudaMemcpyAsync(out.data(), field.pairs.p + static_cast<size_t>(q) * kPairCap, sizeof(unsigned) * out.size(),
+                               cudaMemcpyDeviceToHost, field.stream()),
+               "pairs");
+    cuda_check(cudaStreamSynchronize(field.stream()), "pairs sync");
+  }
+  return out;
 }
 
 // Check-only kernel (stats, CCL, collisions of the current state) into the
@@ -1409,6 +1413,7 @@ void run_check_kernel(DeviceField& field, const Config& cfg, const Coefficients&
   p.step_begin = s;
   const int blocks = engine_blocks(static_cast<int>(field.mesh().nv()), cfg.grid_ctas);
   field.set_grid(blocks);
+  field.rebuild_band_list(s);
   ck(launch_check(field.mesh().view(), field.view(), field.work(), p, blocks, field.stream()), "check kernel");
   cuda_check(cudaStreamSynchronize(field.stream()), "check sync");
   if (field.read_ctl().bandpair_overflow) fail(kCapacityExceeded, "band item list overflow (trail snap)");
@@ -1418,7 +1423,7 @@ std::vector<LayerStat> read_stats(const DeviceField& field, long s) {
   const size_t n = field.active_nonbase().size();
   std::vector<LayerStat> out(n);
   if (n) {
-    cuda_check(cudaMemcpyAsync(out.data(), field.stat.p + static_cast<size_t>(s & 1) * kMaxActive, sizeof(LayerStat) * n,
+    cuda_check(cudaMemcpyAsync(out.data(), field.stat.p + static_cast<size_t>(slot4(s)) * kMaxActive, sizeof(LayerStat) * n,
                                cudaMemcpyDeviceToHost, field.stream()),
                "stats");
     cuda_check(cudaStreamSynchronize(field.stream()), "stats sync");
@@ -1434,7 +1439,7 @@ std::vector<std::vector<Index>> detect_collisions(DeviceField& field, const Conf
   field.sync_active();
   if (field.active_nonbase().size() < 2) return {};
   run_check_kernel(field, cfg, Coefficients{}, 0.0, 0);
-  return groups_from_pairs(read_pairs(field));
+  return groups_from_pairs(read_pairs(field, 0));
 }
 
 void step(DeviceField& field, const DeviceLaplacian& op, const Config& cfg, const Coefficients& c) {
@@ -1448,12 +1453,13 @@ void step(DeviceField& field, const DeviceLaplacian& op, const Config& cfg, cons
   DevWork w = field.work();
   w.stamp = field.stamp.p;
   Ctl ctl = field.read_ctl();
-  ctl.rcount[0] = ctl.rcount[1] = 0;
+  for (int q = 0; q < 4; ++q) ctl.rcount[q] = 0;
   ctl.error = 0;
   ctl.stop_bits = 0;
   field.ctl.upload(&ctl, 1, s);
   const DevMesh m = op.view();
-  ck(launch_mark_all_support(m, field.view(), w, 0, 1, s), "mark support");
+  ck(launch_mark_all_support(m, field.view(), w, 0, slot4(1), s), "mark support");
+  field.rebuild_band_list(1);
   StepParams p = make_params(field, cfg, c, dt);
   p.step_begin = 1;
   p.step_end = 2;
@@ -1523,7 +1529,7 @@ class PassEngine {
     res_.events.push_back(ev);
     track(1).created_event = 0;
     std::vector<int> sv(seeds.begin(), seeds.end());
-    field_->mark_region(op_.view(), sv, 0, 1);
+    field_->mark_region(op_.view(), sv, 0);
     tm.mark("pass frontier");
     blocks_ = engine_blocks(static_cast<int>(dm_->nv()), cfg_.grid_ctas);
     field_->set_grid(blocks_);
@@ -1604,13 +1610,7 @@ class PassEngine {
   StepParams params() const {
     StepParams p = make_params(*field_, cfg_, co_, dt_);
     p.stop_every_check = cfg_.on_check ? 1 : 0;
-    if (const char* env = std::getenv("DTB_SPLIT_A"); env && env[0] == '1') p.split_a = 1;
-    if (const char* env = std::getenv("DTB_NO_UNITE"); env && env[0] == '1') p.split_a_no_unite = 1;
     if (const char* env = std::getenv("DTB_D_FULL"); env && env[0] == '1') p.d_full = 1;
-    // E, B and D spread round-robin over the CTAs, A filled from each CTA's
-    // last warp so it overlaps E (measured: E+A 14.4 -> 13.4 us per step).
-    p.map_mode = 1 | 2 | 4 | 8;
-    if (const char* env = std::getenv("DTB_MAP")) p.map_mode = std::atoi(env);
     return p;
   }
 
@@ -1643,6 +1643,10 @@ class PassEngine {
       }
       p.step_begin = begin;
       p.step_end = end;
+      // The first check's band list, and an empty list for the frontier the
+      // prologue queues (a discarded speculative update may have left one).
+      field_->rebuild_band_list(begin);
+      cuda_check(cudaMemsetAsync(&field_->ctl.p->rcount[slot4(begin + 1)], 0, sizeof(int), s_), "memset");
       cuda_check(cudaEventRecord(ev0k_, s_), "event record");
       ck(launch_run(op_.view(), field_->view(), work(), p, blocks_, s_), "engine launch");
       cuda_check(cudaEventRecord(ev1k_, s_), "event record");
@@ -1895,7 +1899,7 @@ class PassEngine {
       field_->sync_active();
       run_check_kernel(*field_, cfg_, co_, dt_, s);
     }
-    const auto groups = groups_from_pairs(read_pairs(*field_));
+    const auto groups = groups_from_pairs(read_pairs(*field_, s));
     for (const auto& g : groups) {
       handle_merge(g, s);
       changed = true;
@@ -1926,7 +1930,7 @@ class PassEngine {
     bool done = false;
     const double bmax = [&] {
       double d;
-      std::memcpy(&d, &c.base_max_bits, 8);
+      std::memcpy(&d, &c.base_max_bits[slot4(s)], 8);
       return d;
     }();
     if (c.base_one == 0 && bmax < 1.0 - cfg_.saturation) {
@@ -1938,7 +1942,7 @@ class PassEngine {
     field_->sync_active();
     // Vertices logged by split/merge join the next frontier (change log).
     if (!field_->pending_moved.empty()) {
-      field_->mark_region(op_.view(), field_->pending_moved, s, static_cast<int>((s + 1) & 1));
+      field_->mark_region(op_.view(), field_->pending_moved, s);
       field_->pending_moved.clear();
     }
     (void)vanished;
@@ -1967,7 +1971,7 @@ class PassEngine {
       ++n;
     }
     if (n)
-      std::fprintf(stderr, "[dtb] phase us/step over %ld steps: B %.2f  D %.2f  E(+A) %.2f  step %.2f (blocks %d)\n", n,
+      std::fprintf(stderr, "[dtb] phase us/step over %ld steps: D+A %.2f  E+A %.2f  extra %.2f  step %.2f (blocks %d)\n", n,
                    sum[0] / n / 1e3, sum[1] / n / 1e3, sum[2] / n / 1e3, tot / n / 1e3, blocks_);
     {
       const size_t tb = t.size() - 64 * 3 * static_cast<size_t>(blocks_) - 16;

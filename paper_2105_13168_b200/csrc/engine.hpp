@@ -265,22 +265,25 @@ class DeviceField {
   }
   Ctl read_ctl() const;
   // Queues verts and their stiffness rows as the frontier of step stamp+1.
-  void mark_region(const DevMesh& op_view, const std::vector<int>& verts, long stamp, int parity);
+  void mark_region(const DevMesh& op_view, const std::vector<int>& verts, long stamp);
+  // Before an engine or check launch whose first check is step t: the band
+  // list E(t) reads, rebuilt from the interest flags (host edits and a
+  // discarded speculative update leave the incremental list stale).
+  void rebuild_band_list(long t);
   double prune_epsilon = 1e-9;
   // Vertices logged by split/merge edits since the last take (change log).
   std::vector<int> pending_moved;
 
-  // storage
-  DevBuf<unsigned char> cnt, interest, scnt, sflag, active, in_list;
-  DevBuf<uint4> sbinfo;  // band index of each scratch column (computed by the update)
-  DevBuf<unsigned short> lay, slay;
-  DevBuf<double> val, sval, lastpos;
-  DevBuf<int> region0, region1, stamp, ilist0, ilist1, aidx, alist;
-  DevBuf<int2> bandpairs, bp_ovf;
-  DevBuf<int> bpcount;
+  // storage: the two field copies (DevField::b), lists by slot4(step)
+  DevBuf<unsigned char> cnt[2], interest[2], active;
+  DevBuf<unsigned short> lay[2];
+  DevBuf<double> val[2], lastpos;
+  DevBuf<uint4> binfo[2];
+  DevBuf<int> region[4], ilist[4], stamp, aidx, alist;
+  DevBuf<int2> bandpairs[2], bp_ovf[2];
+  DevBuf<int> bpcount[2];
   DevBuf<int> ai0, ai1, acnt;       // event-time scratch (see setup())
   DevBuf<double> ad0, ad1, ad2;
-  DevBuf<uint4> binfo;
   DevBuf<unsigned long long> parent, pair_keys, hashes;
   DevBuf<int2> added;   // band items gained this step (split certificate)
   DevBuf<int> add_stamp;  // per vertex: last step it gained a band item

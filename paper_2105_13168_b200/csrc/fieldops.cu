@@ -3,6 +3,8 @@
 // covered_set:238, dense_row:256, normalize_columns:143; isoline.hpp
 // edge_crossings:30; diffusion.hpp finished():795).  Dense passes over the
 // column storage; they run only at events, never inside the step loop.
+// Between engine launches both copies of the field (DevField::b) are
+// identical: queries read b[0], edits write b[0] and mirror the column to b[1].
 #include <cuda_runtime.h>
 
 #include "kernels.h"
@@ -14,7 +16,7 @@ namespace {
 constexpr int T = 256;
 inline int nblk(long long n) { return static_cast<int>((n + T - 1) / T); }
 
-__device__ __forceinline__ double value_of(const DevField& F, int v, int layer) {
+__device__ __forceinline__ double value_of(const FieldBuf& F, int v, int layer) {
   const int c = F.cnt[v];
   const size_t b = static_cast<size_t>(v) * kSlots;
   for (int j = 0; j < c; ++j) {
@@ -25,9 +27,23 @@ __device__ __forceinline__ double value_of(const DevField& F, int v, int layer) 
   return 0.0;
 }
 
-// Recomputes the interest flag of an edited column and appends the vertex to
-// the current band list if it became interesting.
-__device__ __forceinline__ void refresh_interest(const DevField& F, const DevWork& W, int v) {
+// Copies column v (entries, count, interest, band index) from b[0] to b[1].
+__device__ __forceinline__ void mirror_col(const DevField& F, int v) {
+  const FieldBuf &A = F.b[0], &B = F.b[1];
+  const int c = A.cnt[v];
+  const size_t b = static_cast<size_t>(v) * kSlots;
+  for (int j = 0; j < c; ++j) {
+    B.lay[b + j] = A.lay[b + j];
+    B.val[b + j] = A.val[b + j];
+  }
+  B.cnt[v] = static_cast<unsigned char>(c);
+  B.interest[v] = A.interest[v];
+  B.binfo[v] = A.binfo[v];
+}
+
+// Recomputes the interest flag and band index of an edited column of b[0].
+// (The band list is rebuilt from the flags before the next engine launch.)
+__device__ __forceinline__ void refresh_interest(const FieldBuf& F, const DevWork& W, int v) {
   const int c = F.cnt[v];
   bool inter = false;
   for (int j = 0; j < c; ++j) {
@@ -38,47 +54,45 @@ __device__ __forceinline__ void refresh_interest(const DevField& F, const DevWor
   F.binfo[v] = inter ? make_binfo(F.lay + static_cast<size_t>(v) * kSlots, F.val + static_cast<size_t>(v) * kSlots, c,
                                   W.band_lo, W.sat)
                      : make_uint4(0, 0, 0, 0);
-  if (inter && !W.in_list[v]) {
-    W.in_list[v] = 1;
-    const int par = W.ctl->lpar;
-    W.ilist[par][atomicAdd(&W.ctl->ilcount[par], 1)] = v;
-  }
 }
 
 __global__ void k_init(DevField F, DevWork W, int nv) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= nv) return;
-  F.cnt[v] = 1;
-  F.lay[static_cast<size_t>(v) * kSlots] = 0;
-  F.val[static_cast<size_t>(v) * kSlots] = 1.0;
-  F.interest[v] = 0;
-  F.binfo[v] = make_uint4(0, 0, 0, 0);
-  W.in_list[v] = 0;
+  for (int q = 0; q < 2; ++q) {
+    F.b[q].cnt[v] = 1;
+    F.b[q].lay[static_cast<size_t>(v) * kSlots] = 0;
+    F.b[q].val[static_cast<size_t>(v) * kSlots] = 1.0;
+    F.b[q].interest[v] = 0;
+    F.b[q].binfo[v] = make_uint4(0, 0, 0, 0);
+  }
   W.stamp[v] = -1;
 }
 
 __global__ void k_seed(DevField F, const int* seeds, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  F.lay[static_cast<size_t>(seeds[i]) * kSlots] = 1;
+  F.b[0].lay[static_cast<size_t>(seeds[i]) * kSlots] = 1;
+  F.b[1].lay[static_cast<size_t>(seeds[i]) * kSlots] = 1;
 }
 
-__device__ __forceinline__ void queue(const DevWork& W, int u, int stamp, int parity) {
+__device__ __forceinline__ void queue(const DevWork& W, int u, int stamp, int slot) {
   if (atomicExch(W.stamp + u, stamp) != stamp) {
-    const int pos = atomicAdd(&W.ctl->rcount[parity], 1);
-    W.region[parity][pos] = u;
+    const int pos = atomicAdd(&W.ctl->rcount[slot], 1);
+    W.region[slot][pos] = u;
   }
 }
 
-__global__ void k_mark(DevMesh M, DevWork W, const int* verts, int n, int stamp, int parity) {
+__global__ void k_mark(DevMesh M, DevWork W, const int* verts, int n, int stamp, int slot) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int v = verts[i];
-  queue(W, v, stamp, parity);
-  for (int k = M.s_off[v]; k < M.s_off[v + 1]; ++k) queue(W, M.s_col[k], stamp, parity);
+  queue(W, v, stamp, slot);
+  for (int k = M.s_off[v]; k < M.s_off[v + 1]; ++k) queue(W, M.s_col[k], stamp, slot);
 }
 
-__global__ void k_mark_support(DevMesh M, DevField F, DevWork W, int stamp, int parity) {
+__global__ void k_mark_support(DevMesh M, DevField Fd, DevWork W, int stamp, int slot) {
+  const FieldBuf& F = Fd.b[0];
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= M.nv) return;
   const int c = F.cnt[v];
@@ -88,11 +102,26 @@ __global__ void k_mark_support(DevMesh M, DevField F, DevWork W, int stamp, int 
     if (l == 0 || W.active[l]) any = true;
   }
   if (!any) return;
-  queue(W, v, stamp, parity);
-  for (int k = M.s_off[v]; k < M.s_off[v + 1]; ++k) queue(W, M.s_col[k], stamp, parity);
+  queue(W, v, stamp, slot);
+  for (int k = M.s_off[v]; k < M.s_off[v + 1]; ++k) queue(W, M.s_col[k], stamp, slot);
 }
 
-__global__ void k_pull(DevField F, int nv, int layer, int* out_v, double* out_x, int* out_n) {
+// Band list of the next engine launch: every vertex whose column holds a
+// value strictly inside (0, 1), by warp-aggregated appends.
+__global__ void k_rebuild_list(DevField Fd, DevWork W, int nv, int slot) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool in = v < nv && Fd.b[0].interest[v];
+  const unsigned m = __ballot_sync(0xffffffffu, in);
+  if (!m) return;
+  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(&W.ctl->ilcount[slot], __popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (in) W.ilist[slot][base + __popc(m & ((1u << lane) - 1u))] = v;
+}
+
+__global__ void k_pull(DevField Fd, int nv, int layer, int* out_v, double* out_x, int* out_n) {
+  const FieldBuf& F = Fd.b[0];
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= nv) return;
   const int c = F.cnt[v];
@@ -111,7 +140,8 @@ __global__ void k_pull(DevField F, int nv, int layer, int* out_v, double* out_x,
 
 // Moves the value of `oldlayer` at each listed vertex to its new layer id
 // (split_layer: row ownership changes, values do not).
-__global__ void k_relabel(DevField F, DevWork W, const int* verts, const int* newlayer, int n, int oldlayer) {
+__global__ void k_relabel(DevField Fd, DevWork W, const int* verts, const int* newlayer, int n, int oldlayer) {
+  const FieldBuf& F = Fd.b[0];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int v = verts[i];
@@ -137,12 +167,14 @@ __global__ void k_relabel(DevField F, DevWork W, const int* verts, const int* ne
   F.val[b + p] = x;
   F.cnt[v] = static_cast<unsigned char>(c + 1);
   if (F.interest[v]) F.binfo[v] = make_binfo(F.lay + b, F.val + b, c + 1, W.band_lo, W.sat);
+  mirror_col(Fd, v);
 }
 
 // merge_layers: per vertex, the group's values summed in ascending layer
 // order from 0.0, clamped by min(., 1), stored under the new id.
-__global__ void k_merge(DevField F, DevWork W, int nv, const int* group, int ngroup, int result, int* touched,
+__global__ void k_merge(DevField Fd, DevWork W, int nv, const int* group, int ngroup, int result, int* touched,
                         int* ntouched) {
+  const FieldBuf& F = Fd.b[0];
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= nv) return;
   const size_t b = static_cast<size_t>(v) * kSlots;
@@ -175,10 +207,12 @@ __global__ void k_merge(DevField F, DevWork W, int nv, const int* group, int ngr
   F.val[b + p] = clamped;
   F.cnt[v] = static_cast<unsigned char>(out + 1);
   refresh_interest(F, W, v);
+  mirror_col(Fd, v);
   touched[atomicAdd(ntouched, 1)] = v;
 }
 
-__global__ void k_covered(DevField F, int nv, double threshold, int* out_v, int* out_n) {
+__global__ void k_covered(DevField Fd, int nv, double threshold, int* out_v, int* out_n) {
+  const FieldBuf& F = Fd.b[0];
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= nv) return;
   const double b = (F.cnt[v] > 0 && F.lay[static_cast<size_t>(v) * kSlots] == 0) ? F.val[static_cast<size_t>(v) * kSlots]
@@ -192,8 +226,9 @@ __device__ __forceinline__ double signed_value(double value, double level) {
   return s;
 }
 
-__global__ void k_crossings(DevMesh M, DevField F, int layer, double level, int* out_e, double* out_t, double* out_ba,
+__global__ void k_crossings(DevMesh M, DevField Fd, int layer, double level, int* out_e, double* out_t, double* out_ba,
                             double* out_bb, int* out_n) {
+  const FieldBuf& F = Fd.b[0];
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= M.ne) return;
   const int a = M.edges[2 * e], b = M.edges[2 * e + 1];
@@ -210,7 +245,8 @@ __global__ void k_crossings(DevMesh M, DevField F, int layer, double level, int*
 // finished() (diffusion.hpp:795) neighbour test: clears *flag if any mesh
 // neighbour of the layer's support still holds base mass above the prune
 // epsilon.
-__global__ void k_finished(DevMesh M, DevField F, int layer, double prune, int* flag) {
+__global__ void k_finished(DevMesh M, DevField Fd, int layer, double prune, int* flag) {
+  const FieldBuf& F = Fd.b[0];
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= M.nv) return;
   if (value_of(F, v, layer) == 0.0) return;
@@ -228,7 +264,8 @@ __device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
   return x ^ (x >> 31);
 }
 
-__global__ void k_hash(DevField F, int nv, unsigned long long* out) {
+__global__ void k_hash(DevField Fd, int nv, unsigned long long* out) {
+  const FieldBuf& F = Fd.b[0];
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long h = 0;
   if (v < nv) {
@@ -244,7 +281,8 @@ __global__ void k_hash(DevField F, int nv, unsigned long long* out) {
   if ((threadIdx.x & 31) == 0 && h) atomicAdd(out, h);
 }
 
-__global__ void k_normalize(DevField F, DevWork W, int nv, double prune) {
+__global__ void k_normalize(DevField Fd, DevWork W, int nv, double prune) {
+  const FieldBuf& F = Fd.b[0];
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= nv) return;
   const size_t b = static_cast<size_t>(v) * kSlots;
@@ -267,15 +305,18 @@ __global__ void k_normalize(DevField F, DevWork W, int nv, double prune) {
   }
   F.cnt[v] = static_cast<unsigned char>(out);
   refresh_interest(F, W, v);
+  mirror_col(Fd, v);
 }
 
-__global__ void k_dense_row(DevField F, int nv, int layer, double* out) {
+__global__ void k_dense_row(DevField Fd, int nv, int layer, double* out) {
+  const FieldBuf& F = Fd.b[0];
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= nv) return;
   out[v] = value_of(F, v, layer);
 }
 
-__global__ void k_base_one(DevField F, int nv, int* out) {
+__global__ void k_base_one(DevField Fd, int nv, int* out) {
+  const FieldBuf& F = Fd.b[0];
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   bool one = false;
   if (v < nv) one = value_of(F, v, 0) == 1.0;
@@ -298,15 +339,19 @@ int launch_init_field(const DevField& f, const DevWork& w, int nv, const int* se
   }
   DTB_RET;
 }
-int launch_mark_region(const DevMesh& m, const DevWork& w, const int* verts, int n, long long stamp, int parity,
+int launch_mark_region(const DevMesh& m, const DevWork& w, const int* verts, int n, long long stamp, int slot,
                        void* stream) {
   if (n <= 0) return 0;
-  k_mark<<<nblk(n), T, 0, static_cast<cudaStream_t>(stream)>>>(m, w, verts, n, static_cast<int>(stamp), parity);
+  k_mark<<<nblk(n), T, 0, static_cast<cudaStream_t>(stream)>>>(m, w, verts, n, static_cast<int>(stamp), slot);
   DTB_RET;
 }
-int launch_mark_all_support(const DevMesh& m, const DevField& f, const DevWork& w, long long stamp, int parity,
+int launch_mark_all_support(const DevMesh& m, const DevField& f, const DevWork& w, long long stamp, int slot,
                             void* stream) {
-  k_mark_support<<<nblk(m.nv), T, 0, static_cast<cudaStream_t>(stream)>>>(m, f, w, static_cast<int>(stamp), parity);
+  k_mark_support<<<nblk(m.nv), T, 0, static_cast<cudaStream_t>(stream)>>>(m, f, w, static_cast<int>(stamp), slot);
+  DTB_RET;
+}
+int launch_rebuild_list(const DevField& f, const DevWork& w, int nv, int slot, void* stream) {
+  k_rebuild_list<<<nblk(nv), T, 0, static_cast<cudaStream_t>(stream)>>>(f, w, nv, slot);
   DTB_RET;
 }
 int launch_pull_layer(const DevField& f, int nv, int layer, int* out_v, double* out_x, int* out_n, void* stream) {

@@ -133,27 +133,23 @@ __device__ __forceinline__ void grid_sync(Ctl*) {
 // memory: 148 requests to the control line instead of one per warp (2,368),
 // which the L2 slice holding that line would serve one by one.
 struct CtlSnap {
-  int rcount[2];
-  int ilcount[2];
-  int lpar;
+  int rcount[4];
+  int ilcount[4];
   int error;
-  int error_vertex;
   int spec_error;
-  int dchange[2];
-  int nadded[2];
-  int anchor_fail[2];
-  int nbandpairs;
-  int pad_;
+  int dchange[4];
+  int nadded[4];
+  int anchor_fail[4];
+  int nbandpairs[4];
+  int pad_[2];
 };
-static_assert(sizeof(CtlSnap) == 64, "CtlSnap mirrors the first 64 bytes of Ctl");
+static_assert(sizeof(CtlSnap) == 112, "CtlSnap mirrors the first 112 bytes of Ctl");
 __device__ __forceinline__ void ctl_snap(const Ctl* ctl, CtlSnap& sc) {
   if (threadIdx.x == 0) {
     const int4* src = reinterpret_cast<const int4*>(ctl);
     int4* dst = reinterpret_cast<int4*>(&sc);
-    dst[0] = __ldcg(src);
-    dst[1] = __ldcg(src + 1);
-    dst[2] = __ldcg(src + 2);
-    dst[3] = __ldcg(src + 3);
+#pragma unroll
+    for (int q = 0; q < 7; ++q) dst[q] = __ldcg(src + q);
   }
   __syncthreads();
 }
@@ -161,6 +157,15 @@ __device__ __forceinline__ void grid_sync_snap(Ctl* ctl, CtlSnap& sc) {
   cooperative_groups::this_grid().sync();
   ctl_snap(ctl, sc);
 }
+
+// What an update tells the bookkeeping that follows it (post_update): flag
+// bits 1 changed, 2 base was exactly 1, 4 base is exactly 1, 8 the new column
+// is interesting, 0x80 valid (clear when the update raised an error); bi is
+// the new column's band index.  Valid on the group's lane 0.
+struct Hdr {
+  unsigned flag;
+  uint4 bi;
+};
 
 // set_value semantics (layer_field.hpp:102): clamp above 1, prune below the
 // epsilon, erase zeros; `changed` records whether the stored value moved.
@@ -248,14 +253,14 @@ __device__ __forceinline__ void cand_add(unsigned short* cl, double* ca, int& nc
   ca[c] = ca[c] + t;
 }
 
-// The committed column's band index and interest flag, computed where the
-// column is produced (so phase B only copies them): make_binfo's definition
-// over the new entries, interest = some value strictly inside (0, 1).
-// NMAX > 0: register arrays of that capacity (fully unrolled, constant
-// indices); NMAX == 0: pointers into shared memory.
+// The new column's band index and interest flag, computed where the column is
+// produced and stored with it: make_binfo's definition over the new entries,
+// interest = some value strictly inside (0, 1).  NMAX > 0: register arrays of
+// that capacity (fully unrolled, constant indices); NMAX == 0: pointers into
+// shared memory.
 template <int NMAX, class LT, class XT>
-__device__ __forceinline__ void scratch_header(const DevWork& W, int i, int n, const LT& lay, const XT& val, bool changed,
-                                               bool old_one, bool new_one) {
+__device__ __forceinline__ void column_header(const FieldBuf& Fo, const DevWork& W, int v, int n, const LT& lay,
+                                              const XT& val, bool changed, bool old_one, bool new_one, Hdr& h) {
   unsigned L[4] = {0, 0, 0, 0}, S[4] = {0, 0, 0, 0};
   int nb = 0;
   bool over = false, inter = false;
@@ -282,13 +287,15 @@ __device__ __forceinline__ void scratch_header(const DevWork& W, int i, int n, c
     bi.z = S[0] | (S[1] << 16);
     bi.w = S[2] | ((over ? kBandOverflow : S[3]) << 16);
   }
-  W.sbinfo[i] = bi;
-  W.scnt[i] = static_cast<unsigned char>(n);
-  W.sflag[i] = static_cast<unsigned char>((changed ? 1 : 0) | (old_one ? 2 : 0) | (new_one ? 4 : 0) | (inter ? 8 : 0));
+  Fo.binfo[v] = bi;
+  Fo.cnt[v] = static_cast<unsigned char>(n);
+  Fo.interest[v] = inter ? 1 : 0;
+  h.bi = bi;
+  h.flag = 0x80u | (changed ? 1u : 0u) | (old_one ? 2u : 0u) | (new_one ? 4u : 0u) | (inter ? 8u : 0u);
 }
 
-__device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P,
-                              int i, int v, bool spec, int lane, unsigned gm) {
+__device__ void update_vertex(const DevMesh& M, const FieldBuf& F, const FieldBuf& Fo, const DevWork& W,
+                              const StepParams& P, int v, bool spec, int lane, unsigned gm, Hdr& h) {
   // Work arrays in the group's shared-memory slab.  Every lane of the group
   // runs this code with the same values, so each lane reads back what it
   // (and its siblings, identically) wrote.
@@ -507,12 +514,12 @@ __device__ void update_vertex(const DevMesh& M, const DevField& F, const DevWork
   }
   const bool old_one = cv > 0 && ol[0] == 0 && ox[0] == 1.0;
   const bool new_one = nn > 0 && nl[0] == 0 && nx[0] == 1.0;
-  const size_t o = static_cast<size_t>(i) * kSlots;
+  const size_t o = static_cast<size_t>(v) * kSlots;
   for (int j = 0; j < nn; ++j) {
-    W.slay[o + j] = nl[j];
-    W.sval[o + j] = nx[j];
+    Fo.lay[o + j] = nl[j];
+    Fo.val[o + j] = nx[j];
   }
-  scratch_header<0>(W, i, nn, nl, nx, changed, old_one, new_one);
+  column_header<0>(Fo, W, v, nn, nl, nx, changed, old_one, new_one, h);
   INSTR_CP(15, tU);
 }
 
@@ -584,7 +591,7 @@ static_assert(kG * kFoldCols * 8 <= kSlabBytes, "the fold staging of a group fit
 // replaces the per-(neighbour, slot) candidate insertion of the generic loop
 // (the longest dependent instruction chain of the step).  Returns false, with
 // no side effects, when the case does not fit.
-__device__ __forceinline__ bool gather_fold(const DevMesh& M, const DevField& F, const DevWork& W, int v, int cv,
+__device__ __forceinline__ bool gather_fold(const DevMesh& M, const FieldBuf& F, const DevWork& W, int v, int cv,
                                             const int (&Ol)[kF], int k0, int k1, int lane, unsigned gm, int (&Cl)[kF],
                                             double (&Ca)[kF], int& nc, double& lapb, double& lapt, bool& bnear) {
   INSTR_C0(tG);
@@ -705,8 +712,8 @@ __device__ __forceinline__ bool gather_fold(const DevMesh& M, const DevField& F,
 // sequential update (the general fast path's arithmetic, term for term);
 // lanes 0..n-1 store the new column.  Returns false, with no side effects,
 // when the case does not apply.
-__device__ bool update_vertex_single(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P,
-                                     int i, int v, bool spec, int lane, unsigned gm) {
+__device__ bool update_vertex_single(const DevMesh& M, const FieldBuf& F, const FieldBuf& Fo, const DevWork& W,
+                                     const StepParams& P, int v, bool spec, int lane, unsigned gm, Hdr& h) {
   const int cv = F.cnt[v];
   const size_t vb = static_cast<size_t>(v) * kSlots;
   const unsigned own_lw = *reinterpret_cast<const unsigned*>(F.lay + vb);  // slots 0, 1
@@ -911,10 +918,10 @@ __device__ bool update_vertex_single(const DevMesh& M, const DevField& F, const 
   }
   const bool old_one = cv > 0 && o0 == 0 && own_x.x == 1.0;
   const bool new_one = n > 0 && El[0] == 0 && Ex[0] == 1.0;
-  const size_t o = static_cast<size_t>(i) * kSlots;
+  const size_t o = static_cast<size_t>(v) * kSlots;
   if (lane < n) {
-    W.slay[o + lane] = static_cast<unsigned short>(lane == 0 ? El[0] : El[1]);
-    W.sval[o + lane] = lane == 0 ? Ex[0] : Ex[1];
+    Fo.lay[o + lane] = static_cast<unsigned short>(lane == 0 ? El[0] : El[1]);
+    Fo.val[o + lane] = lane == 0 ? Ex[0] : Ex[1];
   }
   if (lane == 0) {
     // Header of a column of at most [base, L]: one band entry at most.
@@ -928,16 +935,17 @@ __device__ bool update_vertex_single(const DevMesh& M, const DevField& F, const 
       bi.x = bj == 0 ? El[0] : El[1];
       bi.z = static_cast<unsigned>(bj);
     }
-    W.sbinfo[i] = bi;
-    W.scnt[i] = static_cast<unsigned char>(n);
-    W.sflag[i] =
-        static_cast<unsigned char>((changed ? 1 : 0) | (old_one ? 2 : 0) | (new_one ? 4 : 0) | (inter ? 8 : 0));
+    Fo.binfo[v] = bi;
+    Fo.cnt[v] = static_cast<unsigned char>(n);
+    Fo.interest[v] = inter ? 1 : 0;
+    h.bi = bi;
+    h.flag = 0x80u | (changed ? 1u : 0u) | (old_one ? 2u : 0u) | (new_one ? 4u : 0u) | (inter ? 8u : 0u);
   }
   return true;
 }
 
-__device__ bool update_vertex_fast(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P, int i,
-                                   int v, bool spec, int lane, unsigned gm) {
+__device__ bool update_vertex_fast(const DevMesh& M, const FieldBuf& F, const FieldBuf& Fo, const DevWork& W,
+                                   const StepParams& P, int v, bool spec, int lane, unsigned gm, Hdr& h) {
   INSTR_C0(tA);
   // Every load below is independent of the counts it is masked with, so the
   // column, stiffness row and neighbour columns arrive in three dependent
@@ -1286,14 +1294,14 @@ __device__ bool update_vertex_fast(const DevMesh& M, const DevField& F, const De
   INSTR_CP(3, tA);
   const bool old_one = cv > 0 && Ol[0] == 0 && Ox[0] == 1.0;
   const bool new_one = n > 0 && El[0] == 0 && Ex[0] == 1.0;
-  const size_t o = static_cast<size_t>(i) * kSlots;
+  const size_t o = static_cast<size_t>(v) * kSlots;
 #pragma unroll
   for (int j = 0; j < kN; ++j)
     if (j == lane && j < n) {
-      W.slay[o + j] = static_cast<unsigned short>(El[j]);
-      W.sval[o + j] = Ex[j];
+      Fo.lay[o + j] = static_cast<unsigned short>(El[j]);
+      Fo.val[o + j] = Ex[j];
     }
-  if (lane == 0) scratch_header<kN>(W, i, n, El, Ex, changed, old_one, new_one);
+  if (lane == 0) column_header<kN>(Fo, W, v, n, El, Ex, changed, old_one, new_one, h);
   return true;
 }
 
@@ -1336,103 +1344,114 @@ __device__ __forceinline__ void bq_push(BlockQueueT<T>& q, int* gcount, T* glist
   }
 }
 
+// Flushes the CTA's staged appends.  Threads [t0, t0 + nthreads) take part:
+// the whole CTA (bar 0 = __syncthreads) or the warps of one role behind a
+// named barrier, so the other roles of the phase never wait for it.  The next
+// use of the queue is after a grid barrier, so no trailing barrier is needed.
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 template <class T>
-__device__ void bq_flush(BlockQueueT<T>& q, int* gcount, T* glist, int cap = 0x7fffffff, int* overflow = nullptr) {
-  __syncthreads();
+__device__ void bq_flush(BlockQueueT<T>& q, int* gcount, T* glist, int bar = 0, int t0 = 0, int nthreads = 0) {
+  if (bar == 0) __syncthreads();
+  else named_sync(bar, nthreads);
   const int n = min(q.n, kQCap);
-  if (threadIdx.x == 0) q.base = n ? atomicAdd(gcount, n) : 0;
-  __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    if (q.base + i < cap) glist[q.base + i] = q.buf[i];
-    else if (overflow) *overflow = 1;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) q.n = 0;
-  __syncthreads();
+  const int r = static_cast<int>(threadIdx.x) - t0;
+  if (r == 0) q.base = n ? atomicAdd(gcount, n) : 0;
+  if (bar == 0) __syncthreads();
+  else named_sync(bar, nthreads);
+  const int stride = bar == 0 ? static_cast<int>(blockDim.x) : nthreads;
+  const int rr = bar == 0 ? static_cast<int>(threadIdx.x) : r;
+  for (int i = rr; i < n; i += stride) glist[q.base + i] = q.buf[i];
+  if (bar == 0) __syncthreads();
+  else named_sync(bar, nthreads);
+  if (r == 0 || (bar == 0 && threadIdx.x == 0)) q.n = 0;
 }
 
-__device__ __forceinline__ void queue_region(const DevWork& W, int u, int stamp, int nxt, BlockQueue& Q) {
-  if (atomicExch(W.stamp + u, stamp) != stamp) bq_push(Q, &W.ctl->rcount[nxt], W.region[nxt], u);
+__device__ __forceinline__ void queue_region(const DevWork& W, int u, int stamp, int slot, BlockQueue& Q) {
+  if (atomicExch(W.stamp + u, stamp) != stamp) bq_push(Q, &W.ctl->rcount[slot], W.region[slot], u);
 }
 
-// Phase B for frontier slot i (8-lane group): scatter the new column,
-// maintain the interest flag / band list and the base==1 counter, queue the
-// one-ring (lane j queues entries j, j+8, ... of {v} U row(v)).
-__device__ void commit_vertex(const DevMesh& M, const DevField& F, const DevWork& W, int i, int v, int stamp,
-                              int nxt, int lpar, int lane, unsigned gm, BlockQueue& Q) {
-  INSTR_C0(tB);
-  // Every load that depends only on (i, v) is issued up front: the scratch
-  // header and this lane's scratch slot, the stiffness row bounds and the
-  // band-list flag.  The commit then needs two more dependent rounds (row
-  // entries, stamp exchange) instead of six.
-  const size_t o = static_cast<size_t>(i) * kSlots, d = static_cast<size_t>(v) * kSlots;
-  const int flag = W.sflag[i];
-  const int nn = W.scnt[i];
-  const unsigned short sl = W.slay[o + lane];
-  const double sx = W.sval[o + lane];
-  const int rlen = __ldg(M.e_len + v);  // the one-ring from the padded row: no s_off round trip
-  const int ue = lane >= 1 ? __ldg(M.e_col + static_cast<size_t>(v) * kEll + lane - 1) : v;
-  const unsigned char listed = W.in_list[v];
-  const uint4 old_bi = F.binfo[v];  // band layers before this commit (change tracking)
-  const uint4 bi = W.sbinfo[i];     // the new column's band index (computed by the update)
-  if (!(flag & 1)) return;
-  INSTR_CP(4, tB);
-  const int t0 = lane;  // first row entry of this lane: t = 0 is v itself
-  const int u0 = t0 == 0 ? v : (t0 <= rlen ? ue : -1);
-  // Claim the one-ring for frontier s+1 now; the exchange's round trip
-  // overlaps the column writes below.
-  const bool first = u0 >= 0 && atomicExch(W.stamp + u0, stamp) != stamp;
-  const bool inter = (flag & 8) != 0;
-  if (lane < nn) {
-    F.lay[d + lane] = sl;
-    F.val[d + lane] = sx;
+// What phase B (commit) did before the field was double-buffered, now run by
+// the updating group right after its update of v at step t (reference:
+// diffusion.hpp:253-271 change log -> next frontier): queue the one-ring of a
+// changed column as frontier t+1, list a column that became interesting in
+// the band list E(t) reads, record band-item changes for the split
+// certificate, and carry the base==1 count.  The column itself was written to
+// the step's buffer by the update.  old_bi / old_inter describe v's column
+// before the step; rlen / ue are v's padded stiffness row (lane j: entry j-1).
+__device__ void post_update(const DevMesh& M, const DevWork& W, int v, int t, const Hdr& h0, uint4 old_bi,
+                            bool old_inter, int rlen, int ue, int lane, unsigned gm, BlockQueue& Q) {
+  const unsigned flag = __shfl_sync(gm, h0.flag, 0, kG);
+  if (!(flag & 0x80u)) return;  // the update raised an error: the step is void
+  const int nslot = slot4(t + 1);
+  if (flag & 1u) {
+    // Claim the one-ring for frontier t+1 (lane 0: v itself, lane j: entry j-1).
+    const int u0 = lane == 0 ? v : (lane <= rlen ? ue : -1);
+    const bool first = u0 >= 0 && atomicExch(W.stamp + u0, t) != t;
+    if (first) bq_push(Q, &W.ctl->rcount[nslot], W.region[nslot], u0);
+    for (int k = lane + kG; k <= rlen; k += kG)  // entries past the group: padded row, then the CSR
+      queue_region(W, k - 1 < kEll ? __ldg(M.e_col + static_cast<size_t>(v) * kEll + k - 1)
+                                   : __ldg(M.s_col + __ldg(M.s_off + v) + k - 1),
+                   t, nslot, Q);
   }
-  for (int j = lane + kG; j < nn; j += kG) {  // columns longer than kG (slow-path results)
-    F.lay[d + j] = W.slay[o + j];
-    F.val[d + j] = W.sval[o + j];
-  }
-  if (lane == 0) {
-    // Band-item changes for the split certificate of phase D (see
-    // skip_union_ok): a lost band layer (or an overflowing band index) marks
-    // the step; gained layers are listed.
-    const int cp = stamp & 1;  // change-tracking slot of this step
+  if (lane != 0) return;
+  const int cp = slot4(t);
+  if (flag & 1u) {
+    // Band-item changes for the split certificate (see anchor_test): a lost
+    // band layer (or an overflowing band index) marks the step; gained layers
+    // are listed.  An unchanged column has the same band index.
+    const uint4 bi = h0.bi;
     if (binfo_overflow(old_bi) || binfo_overflow(bi)) {
       W.ctl->dchange[cp] = 1;
     } else {
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const unsigned lo = binfo_layer(old_bi, t), ln = binfo_layer(bi, t);
+      for (int q = 0; q < 4; ++q) {
+        const unsigned lo = binfo_layer(old_bi, q), ln = binfo_layer(bi, q);
         bool lo_kept = false, ln_old = false;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          lo_kept |= lo != 0 && binfo_layer(bi, q) == lo;
-          ln_old |= ln != 0 && binfo_layer(old_bi, q) == ln;
+        for (int r = 0; r < 4; ++r) {
+          lo_kept |= lo != 0 && binfo_layer(bi, r) == lo;
+          ln_old |= ln != 0 && binfo_layer(old_bi, r) == ln;
         }
         if (lo != 0 && !lo_kept) W.ctl->dchange[cp] = 1;
         if (ln != 0 && !ln_old) {
-          W.add_stamp[v] = stamp;
+          W.add_stamp[v] = t;
           const int pos = atomicAdd(&W.ctl->nadded[cp], 1);
           if (pos < W.added_cap) W.added[static_cast<size_t>(cp) * W.added_cap + pos] = make_int2(v, static_cast<int>(ln));
           else W.ctl->dchange[cp] = 1;
         }
       }
     }
-    F.cnt[v] = static_cast<unsigned char>(nn);
-    F.interest[v] = inter ? 1 : 0;
-    F.binfo[v] = bi;
-    if (inter && !listed) {
-      W.in_list[v] = 1;
-      W.ilist[lpar][atomicAdd(&W.ctl->ilcount[lpar], 1)] = v;
-    }
-    const int delta = ((flag >> 2) & 1) - ((flag >> 1) & 1);
-    if (delta) atomicAdd(&W.ctl->base_one, delta);
   }
-  INSTR_CP(5, tB);
-  if (first) bq_push(Q, &W.ctl->rcount[nxt], W.region[nxt], u0);
-  for (int t = lane + kG; t <= rlen; t += kG)  // entries past the group: padded row, then the CSR
-    queue_region(W, t - 1 < kEll ? __ldg(M.e_col + static_cast<size_t>(v) * kEll + t - 1) : __ldg(M.s_col + __ldg(M.s_off + v) + t - 1),
-                 stamp, nxt, Q);
-  INSTR_CP(7, tB);
+  // A column that became interesting joins the list E(t) reads (the check
+  // before this one carried over every column that already was).
+  if ((flag & 8u) && !old_inter) W.ilist[cp][atomicAdd(&W.ctl->ilcount[cp], 1)] = v;
+  const int delta = static_cast<int>((flag >> 2) & 1u) - static_cast<int>((flag >> 1) & 1u);
+  if (delta) atomicAdd(&W.ctl->base_d[cp], delta);
+}
+
+// Update of frontier entry i of step t (reading the field after t-1, writing
+// the field after t) and its bookkeeping, by one 8-lane group.
+__device__ __forceinline__ void update_item(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P,
+                                            int t, int i, bool spec, BlockQueue& Q) {
+  const int lane = threadIdx.x & (kG - 1);
+  const unsigned gm = group_mask();
+  const int v = W.region[slot4(t)][i];
+  const FieldBuf& Fi = F.b[(t - 1) & 1];
+  const FieldBuf& Fo = F.b[t & 1];
+  // Loads of the bookkeeping that depend only on v, issued with the update's.
+  const uint4 old_bi = Fi.binfo[v];
+  const bool old_inter = Fi.interest[v] != 0;
+  const int rlen = __ldg(M.e_len + v);
+  const int ue = lane >= 1 ? __ldg(M.e_col + static_cast<size_t>(v) * kEll + lane - 1) : v;
+  Hdr h;
+  h.flag = 0;
+  h.bi = make_uint4(0, 0, 0, 0);
+  if (!update_vertex_single(M, Fi, Fo, W, P, v, spec, lane, gm, h) &&
+      !update_vertex_fast(M, Fi, Fo, W, P, v, spec, lane, gm, h))
+    update_vertex(M, Fi, Fo, W, P, v, spec, lane, gm, h);
+  post_update(M, W, v, t, h, old_bi, old_inter, rlen, ue, lane, gm, Q);
 }
 
 __device__ __forceinline__ bool is_band(const DevWork& W, const StepParams& P, int l, double x) {
@@ -1495,7 +1514,7 @@ __device__ void uf_unite(unsigned long long* par, unsigned a, unsigned b, unsign
   }
 }
 
-__device__ void insert_pair(const DevWork& W, unsigned key, unsigned long long ep) {
+__device__ void insert_pair(const DevWork& W, unsigned key, unsigned long long ep, int cs) {
   const unsigned long long tagged = (ep << 32) | key;
   unsigned h = (key * 2654435761u) & (kPairCap - 1);
   for (int probe = 0; probe < kPairCap; ++probe) {
@@ -1504,9 +1523,9 @@ __device__ void insert_pair(const DevWork& W, unsigned key, unsigned long long e
     if ((cur >> 32) != ep) {
       const unsigned long long prev = atomicCAS(W.pair_keys + h, cur, tagged);
       if (prev == cur) {
-        const int pos = atomicAdd(&W.ctl->npairs, 1);
-        if (pos < kPairCap) W.pairs[pos] = key;
-        else W.ctl->pair_overflow = 1;
+        const int pos = atomicAdd(&W.ctl->npairs[cs], 1);
+        if (pos < kPairCap) W.pairs[static_cast<size_t>(cs) * kPairCap + pos] = key;
+        else W.ctl->pair_overflow[cs] = 1;
         return;
       }
       if (prev == tagged) return;
@@ -1514,7 +1533,7 @@ __device__ void insert_pair(const DevWork& W, unsigned key, unsigned long long e
     }
     h = (h + 1) & (kPairCap - 1);
   }
-  W.ctl->pair_overflow = 1;
+  W.ctl->pair_overflow[cs] = 1;
 }
 
 __device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
@@ -1533,7 +1552,7 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long x)
 }
 
 // Dense field digest (parity tooling only).
-__device__ void phase_hash(const DevField& F, const DevWork& W, int nv) {
+__device__ void phase_hash(const FieldBuf& F, unsigned long long* acc, int nv) {
   unsigned long long h = 0;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv + 31; v += gridDim.x * blockDim.x) {
     if (v < nv) {
@@ -1544,14 +1563,14 @@ __device__ void phase_hash(const DevField& F, const DevWork& W, int nv) {
     }
   }
   h = warp_sum_u64(h);
-  if ((threadIdx.x & 31) == 0 && h) atomicAdd(&W.ctl->hash_acc, h);
+  if ((threadIdx.x & 31) == 0 && h) atomicAdd(acc, h);
 }
 
 // Phase D: union band items that share a band triangle pair (extract_front's
 // edge-adjacency of band triangles, expressed on band vertices).  An 8-lane
 // group per list entry; lane j probes the higher-numbered related vertices
 // j, j+8, ... through their band index (one 16-byte load per probe).
-__device__ __forceinline__ int band_slot_of(const DevField& F, const DevWork& W, const StepParams& P, int u,
+__device__ __forceinline__ int band_slot_of(const FieldBuf& F, const DevWork& W, const StepParams& P, int u,
                                             unsigned l) {
   const uint4 bu = F.binfo[u];
   if (!binfo_overflow(bu)) {
@@ -1570,9 +1589,9 @@ __device__ __forceinline__ int band_slot_of(const DevField& F, const DevWork& W,
   return -1;
 }
 
-__device__ void phase_union(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P, int lpar,
+__device__ void phase_union(const DevMesh& M, const FieldBuf& F, const DevWork& W, const StepParams& P, int lslot,
                             unsigned long long ep, int g0, int ng, int n) {
-  const int* list = W.ilist[lpar];
+  const int* list = W.ilist[lslot];
   const int lane = threadIdx.x & (kG - 1);
   const bool trace = W.prof && blockIdx.x == 0 && threadIdx.x == 0;
   unsigned long long* tr = trace ? W.prof + (W.prof_cap - 64LL * 3 * gridDim.x - 16) : nullptr;
@@ -1605,7 +1624,7 @@ __device__ void phase_union(const DevMesh& M, const DevField& F, const DevWork& 
         const int u = __ldg(M.c_col + c);  // higher-numbered related vertices only
         const int j = band_slot_of(F, W, P, u, l);
         if (trace) tr[3] = gtimer_raw() + (j & 0);
-        if (j >= 0 && !P.split_a_no_unite) uf_unite(W.parent, item, static_cast<unsigned>(u) * kSlots + j, ep);
+        if (j >= 0) uf_unite(W.parent, item, static_cast<unsigned>(u) * kSlots + j, ep);
         if (trace) tr[4] = gtimer_raw();
       }
     }
@@ -1642,23 +1661,24 @@ __device__ __forceinline__ unsigned long long block_bmax(const BlockStats& S) {
   return m;
 }
 
-// Length of this CTA's band-item segment (E's flush); CTA 0 clears the
-// segments of CTAs beyond the grid.
-__device__ __forceinline__ void record_segment(const BlockStats& S, const DevWork& W) {
-  if (blockIdx.x < W.bp_nseg) W.bpcount[blockIdx.x] = min(S.nbp, W.bp_seg);
-  if (blockIdx.x == 0)
-    for (int c = gridDim.x; c < W.bp_nseg; ++c) W.bpcount[c] = 0;
-}
-
-__device__ void block_stats_flush(BlockStats& S, LayerStat* g, int n_active, Ctl* ctl = nullptr,
-                                  const DevWork* W = nullptr) {
-  __syncthreads();
-  if (ctl && threadIdx.x == 0) {
+// E's CTA-level flush for check `step` by threads [t0, t0 + nthreads) behind
+// barrier `bar` (0: __syncthreads for the whole CTA; else a named barrier of
+// E's own warps, so the CTA's A warps never wait for it): the base maximum,
+// the CTA's band-item segment length, and the per-layer sums.
+__device__ void e_flush(BlockStats& S, const DevWork& W, int n_active, long long step, int bar, int t0, int nthreads) {
+  if (bar == 0) __syncthreads();
+  else named_sync(bar, nthreads);
+  const int cs = slot4(step), set = static_cast<int>(step & 1);
+  LayerStat* g = W.stat + static_cast<size_t>(cs) * kMaxActive;
+  const int r = static_cast<int>(threadIdx.x) - t0;
+  if (r == 0) {
     const unsigned long long m = block_bmax(S);
-    if (m) atomicMax(&ctl->base_max_bits, m);
-    if (W) record_segment(S, *W);
+    if (m) atomicMax(&W.ctl->base_max_bits[cs], m);
+    if (blockIdx.x < W.bp_nseg) W.bpcount[set][blockIdx.x] = min(S.nbp, W.bp_seg);
+    if (blockIdx.x == 0)  // segments of CTAs beyond the grid
+      for (int c = gridDim.x; c < W.bp_nseg; ++c) W.bpcount[set][c] = 0;
   }
-  for (int a = threadIdx.x; a < n_active && a < kSmemLayers; a += blockDim.x) {
+  for (int a = r; a < n_active && a < kSmemLayers; a += nthreads) {
     if (S.cnt[a][0]) atomicAdd(&g[a].ncomp, S.cnt[a][0]);
     if (S.cnt[a][1]) atomicAdd(&g[a].nband, S.cnt[a][1]);
     if (S.cnt[a][2]) atomicAdd(&g[a].nunsat, S.cnt[a][2]);
@@ -1666,32 +1686,6 @@ __device__ void block_stats_flush(BlockStats& S, LayerStat* g, int n_active, Ctl
       if (S.sum[a][c])
         atomicAdd(reinterpret_cast<unsigned long long*>(c == 0 ? &g[a].sx : (c == 1 ? &g[a].sy : &g[a].sz)),
                   static_cast<unsigned long long>(S.sum[a][c]));
-    if (S.snap[a] != ~0ull) atomicMin(&g[a].snap, S.snap[a]);
-  }
-}
-
-// E's flush when E runs on warps of its own (the first nE threads): a named
-// barrier among those warps replaces __syncthreads, so the CTA's A warps
-// never wait for it.  Same effect as block_stats_flush.
-__device__ __forceinline__ void named_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-__device__ void flush_e_named(BlockStats& S, LayerStat* g, int n_active, Ctl* ctl, const DevWork& W, int nE) {
-  named_sync(1, nE);
-  if (threadIdx.x == 0) {
-    const unsigned long long m = block_bmax(S);
-    if (m) atomicMax(&ctl->base_max_bits, m);
-    record_segment(S, W);
-  }
-  for (int a = threadIdx.x; a < n_active && a < kSmemLayers; a += nE) {
-    if (S.cnt[a][0]) atomicAdd(&g[a].ncomp, S.cnt[a][0]);
-    if (S.cnt[a][1]) atomicAdd(&g[a].nband, S.cnt[a][1]);
-    if (S.cnt[a][2]) atomicAdd(&g[a].nunsat, S.cnt[a][2]);
-    for (int c = 0; c < 3; ++c)
-      if (S.sum[a][c])
-        atomicAdd(reinterpret_cast<unsigned long long*>(c == 0 ? &g[a].sx : (c == 1 ? &g[a].sy : &g[a].sz)),
-                  static_cast<unsigned long long>(S.sum[a][c]));
-    if (S.snap[a] != ~0ull) atomicMin(&g[a].snap, S.snap[a]);
   }
 }
 
@@ -1722,21 +1716,23 @@ __device__ __forceinline__ unsigned long long seg_max_u64(unsigned peers, unsign
 // neighbour that was a band item of its layer before the step, each layer's
 // band is still connected or empty, so no split can occur and the union-find
 // is not needed.  This marks the added items that are not so anchored.
-__device__ void anchor_test(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P, int nadded,
-                            int stamp) {
-  const int cp = stamp & 1;
+__device__ void anchor_test(const DevMesh& M, const FieldBuf& F, const DevWork& W, const StepParams& P, int nadded,
+                            int stamp, int rank, int stride) {
+  const int cp = slot4(stamp);
   const int n = min(nadded, W.added_cap);
-  // Warp 3 of every CTA: the warps between E's (first) and A's (last).
-  if ((threadIdx.x >> 5) != 3) return;
-  for (int i = (threadIdx.x & 31) * gridDim.x + blockIdx.x; i < n; i += 32 * gridDim.x) {
+  for (int i = rank; i < n; i += stride) {
     const int2 a = W.added[static_cast<size_t>(cp) * W.added_cap + i];
     const int v = a.x;
     const unsigned l = static_cast<unsigned>(a.y);
     if (!W.active[l]) continue;
     bool anchored = false;
+    // u anchors v when it is a band item of l after the step and gained no
+    // band item at the step.  add_stamp[u] may already carry the next step's
+    // (its update runs beside this test): a stamp past `stamp` proves
+    // nothing, so it does not anchor (conservative, never a wrong skip).
     for (int o = M.n_off[v]; o < M.n_off[v + 1] && !anchored; ++o) {
       const int u = M.n_col[o];
-      anchored = W.add_stamp[u] != stamp && band_slot_of(F, W, P, u, l) >= 0;
+      anchored = W.add_stamp[u] < stamp && band_slot_of(F, W, P, u, l) >= 0;
     }
     if (!anchored) W.ctl->anchor_fail[cp] = 1;
   }
@@ -1744,10 +1740,10 @@ __device__ void anchor_test(const DevMesh& M, const DevField& F, const DevWork& 
 
 // Component roots of the band items (ncomp of phase E), for a check whose
 // statistics were gathered under the split certificate that then failed.
-__device__ void phase_roots(const DevField& F, const DevWork& W, const StepParams& P, int lpar, int spar,
+__device__ void phase_roots(const FieldBuf& F, const DevWork& W, const StepParams& P, int lslot, int sslot,
                             unsigned long long ep, int n) {
-  LayerStat* g = W.stat + static_cast<size_t>(spar) * kMaxActive;
-  const int* list = W.ilist[lpar];
+  LayerStat* g = W.stat + static_cast<size_t>(sslot) * kMaxActive;
+  const int* list = W.ilist[lslot];
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
     const int v = list[idx];
     if (!F.interest[v]) continue;
@@ -1769,16 +1765,22 @@ __device__ void phase_roots(const DevField& F, const DevWork& W, const StepParam
 // extinction data, band items for the trail snap, and compaction of the band
 // list into the other buffer (dead entries dropped).  Lanes walk their
 // vertex's slots in lock step so contributions can be combined per warp.
-__device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P, int lpar,
-                            int spar, unsigned long long ep, bool compact, BlockStats& S, BlockQueue& Q,
-                            int n, bool count_roots = true) {
-  LayerStat* g = W.stat + static_cast<size_t>(spar) * kMaxActive;
-  const int* list = W.ilist[lpar];
+// Check t = `step`: reads the field after t (F), the band list of slot4(t),
+// writes stats slot4(t), band items of set t & 1, pairs slot4(t); compacts
+// the list's live entries into slot4(t+1).  Threads [t0, t0 + nthreads) of
+// each CTA take part (rank-major over the CTAs, so a short list spreads over
+// every SM).
+__device__ void phase_stats(const DevMesh& M, const FieldBuf& F, const DevWork& W, const StepParams& P, long long step,
+                            unsigned long long ep, bool compact, BlockStats& S, int n, bool count_roots, int t0,
+                            int nthreads) {
+  const int lslot = slot4(step), nslot = slot4(step + 1), cs = slot4(step), set = static_cast<int>(step & 1);
+  LayerStat* g = W.stat + static_cast<size_t>(cs) * kMaxActive;
+  const int* list = W.ilist[lslot];
   const int lane = threadIdx.x & 31;
-  const int trip = (n + gridDim.x * blockDim.x - 1) / (gridDim.x * blockDim.x);
+  const int rank = static_cast<int>(threadIdx.x) - t0;
+  const int trip = (n + gridDim.x * nthreads - 1) / (gridDim.x * nthreads);
   for (int r = 0; r < trip; ++r) {
-    const int idx = (P.map_mode & 1) ? (r * blockDim.x + threadIdx.x) * gridDim.x + blockIdx.x
-                                     : (r * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+    const int idx = (r * nthreads + rank) * gridDim.x + blockIdx.x;
     INSTR_T0(t0);
     INSTR_C0(tE);
     const int v = idx < n ? list[idx] : -1;
@@ -1808,11 +1810,10 @@ __device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& 
       if (lm) {
         const int leader = __ffs(lm) - 1;
         int base = 0;
-        if (lane == leader) base = atomicAdd(&W.ctl->ilcount[lpar ^ 1], __popc(lm));
+        if (lane == leader) base = atomicAdd(&W.ctl->ilcount[nslot], __popc(lm));
         base = __shfl_sync(0xffffffffu, base, leader);
-        if (live) W.ilist[lpar ^ 1][base + __popc(lm & ((1u << lane) - 1u))] = v;
+        if (live) W.ilist[nslot][base + __popc(lm & ((1u << lane) - 1u))] = v;
       }
-      if (!live && v >= 0) W.in_list[v] = 0;
     }
     const int cv = live ? cnt_v : 0;
     const double base = (cv > 0 && L4[0] == 0) ? X4[0] : 0.0;
@@ -1889,15 +1890,15 @@ __device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& 
           if (base + __popc(bm) > seg) {
             om = __ballot_sync(0xffffffffu, band && pos >= seg);
             const int ol = __ffs(om) - 1;
-            if (lane == ol) obase = atomicAdd(&W.ctl->nbandpairs, __popc(om));
+            if (lane == ol) obase = atomicAdd(&W.ctl->nbandpairs[cs], __popc(om));
             obase = __shfl_sync(0xffffffffu, obase, ol);
           }
           if (band) {
             if (pos < seg) {
-              W.bandpairs[static_cast<size_t>(blockIdx.x) * W.bp_seg + pos] = make_int2(v, a);
+              W.bandpairs[set][static_cast<size_t>(blockIdx.x) * W.bp_seg + pos] = make_int2(v, a);
             } else {
               const int o = obase + __popc(om & ((1u << lane) - 1u));
-              if (o < W.bandpair_cap) W.bp_ovf[o] = make_int2(v, a);
+              if (o < W.bandpair_cap) W.bp_ovf[set][o] = make_int2(v, a);
               else {
                 W.ctl->bandpair_overflow = 1;  // the trail snap would miss items: a capacity error
                 raise_error(W.ctl, kDevCapacity, v, false);
@@ -1943,7 +1944,7 @@ __device__ void phase_stats(const DevMesh& M, const DevField& F, const DevWork& 
         if (l == 0 || !W.active[l]) continue;
         if (F.val[b + k] < P.kappa) continue;
         if (first < 0) first = l;
-        else insert_pair(W, (static_cast<unsigned>(first) << 16) | static_cast<unsigned>(l), ep);
+        else insert_pair(W, (static_cast<unsigned>(first) << 16) | static_cast<unsigned>(l), ep, cs);
       }
     }
     INSTR_REC(2, t0, live);
@@ -1958,15 +1959,12 @@ __device__ __forceinline__ void band_mean(const DevMesh& M, const LayerStat& st,
   mz = (static_cast<double>(st.sz) * M.fx_scale) / n;
 }
 
-// snap_to_band (diffusion.hpp:590) over the recorded band items: nearest band
+// snap_to_band (diffusion.hpp:590) over recorded band items: nearest band
 // vertex to the band mean; key = distance bits (27 low bits dropped) | vertex.
-// Items are spread round-robin over the CTAs from each CTA's last warp, so the
-// snap runs beside the commits of phase B (mapped from the first warps).
-// Trail snap of one list of band items: lane `rank` of `stride` walks it
-// (every lane runs the same number of rounds so the warp-level minimum is
-// well defined).
-__device__ void snap_list(const DevMesh& M, LayerStat* g, BlockStats& S, const int2* items, int n, int rank,
-                          int stride) {
+// Lane `rank` of `stride` walks the list (every lane of a warp runs the same
+// number of rounds so the warp-level minimum is well defined); each warp
+// leader folds its minimum into the layer's statistics with one atomic.
+__device__ void snap_list(const DevMesh& M, LayerStat* g, const int2* items, int n, int rank, int stride) {
   const int lane = threadIdx.x & 31;
   const int trip = (n + stride - 1) / stride;
   for (int r = 0; r < trip; ++r) {
@@ -1985,24 +1983,23 @@ __device__ void snap_list(const DevMesh& M, LayerStat* g, BlockStats& S, const i
     }
     const unsigned peers = __match_any_sync(0xffffffffu, a);
     const unsigned long long kmin = seg_min_u64(peers, key);
-    if (a >= 0 && lane == __ffs(peers) - 1) {
-      if (a < kSmemLayers) atomicMin(&S.snap[a], kmin);
-      else atomicMin(&g[a].snap, kmin);
-    }
+    if (a >= 0 && lane == __ffs(peers) - 1) atomicMin(&g[a].snap, kmin);
   }
 }
 
-// Trail snap over the band items of the last check: each CTA takes the
-// segments c = blockIdx.x (mod grid) -- in the engine its own -- and a
-// grid-strided share of the overflow list.  Threads are used from the last
-// warp down (the first warps run the commits beside it in phase B).
-__device__ void phase_snap(const DevMesh& M, const DevWork& W, int spar, BlockStats& S, int n_ovf) {
-  LayerStat* g = W.stat + static_cast<size_t>(spar) * kMaxActive;
-  const int rev = static_cast<int>(blockDim.x) - 1 - static_cast<int>(threadIdx.x);
+// Trail snap of check `step` (its band items: set step & 1, n_ovf of them in
+// the overflow list) by threads [t0, t0 + nthreads) of every CTA: each CTA
+// takes the segments c = blockIdx.x (mod grid) -- in the engine its own --
+// and a grid-strided share of the overflow list.
+__device__ void phase_snap(const DevMesh& M, const DevWork& W, long long step, int n_ovf, int t0, int nthreads) {
+  LayerStat* g = W.stat + static_cast<size_t>(slot4(step)) * kMaxActive;
+  const int set = static_cast<int>(step & 1);
+  const int rank = static_cast<int>(threadIdx.x) - t0;
   for (int c = blockIdx.x; c < W.bp_nseg; c += gridDim.x)
-    snap_list(M, g, S, W.bandpairs + static_cast<size_t>(c) * W.bp_seg, min(W.bpcount[c], W.bp_seg), rev,
-              blockDim.x);
-  snap_list(M, g, S, W.bp_ovf, min(n_ovf, W.bandpair_cap), rev * gridDim.x + blockIdx.x, gridDim.x * blockDim.x);
+    snap_list(M, g, W.bandpairs[set] + static_cast<size_t>(c) * W.bp_seg, min(W.bpcount[set][c], W.bp_seg), rank,
+              nthreads);
+  snap_list(M, g, W.bp_ovf[set], min(n_ovf, W.bandpair_cap), rank * static_cast<int>(gridDim.x) + blockIdx.x,
+            static_cast<int>(gridDim.x) * nthreads);
 }
 
 __device__ void reset_stat(LayerStat* st) {
@@ -2013,12 +2010,11 @@ __device__ void reset_stat(LayerStat* st) {
   st->snap = ~0ull;
 }
 
-// Writes the trail / last-position record of active index a for check step
-// `step` (stats parity spar) and resets those stats for reuse two steps later.
-__device__ void flush_stat(const DevMesh& M, const DevWork& W, const StepParams& P, int a, int spar, long long step,
-                           bool write) {
-  LayerStat* st = W.stat + static_cast<size_t>(spar) * kMaxActive + a;
-  if (write && st->nband > 0) {
+// Writes the trail / last-position record of active index a for check `step`
+// and resets its statistics slot for the check four steps later.
+__device__ void flush_stat(const DevMesh& M, const DevWork& W, const StepParams& P, int a, long long step) {
+  LayerStat* st = W.stat + static_cast<size_t>(slot4(step)) * kMaxActive + a;
+  if (st->nband > 0) {
     const int layer = W.alist[a];
     double mx, my, mz;
     band_mean(M, *st, mx, my, mz);
@@ -2043,19 +2039,29 @@ __device__ void flush_stat(const DevMesh& M, const DevWork& W, const StepParams&
   }
   reset_stat(st);
 }
+__device__ void flush_range(const DevMesh& M, const DevWork& W, const StepParams& P, long long step, int t0,
+                            int nthreads) {
+  for (int a = (static_cast<int>(threadIdx.x) - t0) * static_cast<int>(gridDim.x) + blockIdx.x; a < P.n_active;
+       a += nthreads * static_cast<int>(gridDim.x))
+    flush_stat(M, W, P, a, step);
+}
 
-__device__ int decide(const DevWork& W, const StepParams& P, int spar) {
-  const LayerStat* g = W.stat + static_cast<size_t>(spar) * kMaxActive;
+// The stop decision of check `step` (diffusion.hpp:807-845): a split, a
+// collision, a vanishing layer, base extinction, or a device error.  Every
+// CTA reads the same words, right after the barrier that completed them.
+__device__ int decide(const DevWork& W, const StepParams& P, long long step) {
+  const int cs = slot4(step);
+  const LayerStat* g = W.stat + static_cast<size_t>(cs) * kMaxActive;
   int bits = 0;
   for (int a = threadIdx.x; a < P.n_active; a += blockDim.x) {
     const LayerStat& st = g[a];
-    if (st.ncomp >= 2 && !P.split_a_no_unite) bits |= kStopSplit;
+    if (st.ncomp >= 2) bits |= kStopSplit;
     if (st.nband == 0 && st.nunsat == 0) bits |= kStopVanish;
   }
   if (threadIdx.x == 0) {
-    if (W.ctl->npairs > 0 || W.ctl->pair_overflow) bits |= kStopMerge;
-    const double bmax = __longlong_as_double(static_cast<long long>(W.ctl->base_max_bits));
-    if (W.ctl->base_one == 0 && bmax < P.extinct_limit) bits |= kStopExtinct;
+    if (W.ctl->npairs[cs] > 0 || W.ctl->pair_overflow[cs]) bits |= kStopMerge;
+    const double bmax = __longlong_as_double(static_cast<long long>(W.ctl->base_max_bits[cs]));
+    if (W.ctl->base_cum[cs] == 0 && bmax < P.extinct_limit) bits |= kStopExtinct;
     if (W.ctl->bandpair_overflow) bits |= kStopError;
   }
   __shared__ int s_bits;
@@ -2068,17 +2074,57 @@ __device__ int decide(const DevWork& W, const StepParams& P, int spar) {
   return r;
 }
 
-// mode 0: run steps; mode 1: check only (stats of the current state into
-// stat[step_begin & 1]); mode 2: snap for that check; mode 3: flush it.
+// The band list carried over a step without a check: the entries of the list
+// of `step` whose column is interesting after the step join the list of
+// step + 1 (what E's compaction does at a check).
+__device__ void carry_list(const FieldBuf& F, const DevWork& W, long long step, int n) {
+  const int* list = W.ilist[slot4(step)];
+  int* next = W.ilist[slot4(step + 1)];
+  int* count = &W.ctl->ilcount[slot4(step + 1)];
+  const int lane = threadIdx.x & 31;
+  const int stride = gridDim.x * blockDim.x;
+  // The loop condition is warp-uniform (idx - lane is the warp's first index).
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx - lane < n; idx += stride) {
+    const int v = idx < n ? list[idx] : -1;
+    const bool live = v >= 0 && F.interest[v];
+    const unsigned m = __ballot_sync(0xffffffffu, live);
+    if (!m) continue;
+    const int leader = __ffs(m) - 1;
+    int b = 0;
+    if (lane == leader) b = atomicAdd(count, __popc(m));
+    b = __shfl_sync(0xffffffffu, b, leader);
+    if (live) next[b + __popc(m & ((1u << lane) - 1u))] = v;
+  }
+}
+
+// Slot clears of the phase that starts step t (one thread; see slot4):
+// the frontier list A(t) read, the band list / change tracking / check
+// outputs of step t+2, the base delta of step t-1 (consumed), the digest of
+// check t+1.
+__device__ __forceinline__ void phase_resets(Ctl* ctl, long long t) {
+  const int c0 = slot4(t), c2 = slot4(t + 2);
+  ctl->rcount[c0] = 0;
+  ctl->ilcount[c2] = 0;
+  ctl->dchange[c2] = 0;
+  ctl->nadded[c2] = 0;
+  ctl->anchor_fail[c2] = 0;
+  ctl->npairs[c2] = 0;
+  ctl->pair_overflow[c2] = 0;
+  ctl->base_max_bits[c2] = 0;
+  ctl->nbandpairs[c2] = 0;
+  ctl->base_d[slot4(t - 1)] = 0;
+  ctl->hash_acc[slot4(t + 1)] = 0;
+}
+
+// mode 0: run steps; mode 1: check only (stats of the current state, step
+// step_begin); mode 2: snap for that check; mode 3: flush it.
 template <int kMode>
 __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, DevWork W, StepParams P) {
   __shared__ BlockStats S;
   __shared__ BlockQueue Q;
   __shared__ CtlSnap SC;
   Ctl* ctl = W.ctl;
-  if (threadIdx.x == 0) {
-    Q.n = 0;
-  }
+  if (threadIdx.x == 0) Q.n = 0;
 #ifdef DTB_INSTR
   for (int i = threadIdx.x; i < 6 * 16; i += blockDim.x) s_hist[i / 16][i % 16] = 0;
   for (int i = threadIdx.x; i < 32; i += blockDim.x) s_cp[i / 2][i % 2] = 0;
@@ -2086,283 +2132,276 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
   __syncthreads();
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int gsz = gridDim.x * blockDim.x;
+  const int nthr = static_cast<int>(blockDim.x);
   unsigned long long ep = static_cast<unsigned long long>(ctl->epoch);
-  int lpar = ctl->lpar;
 
   if (kMode == 1) {
-    const int spar = static_cast<int>(P.step_begin & 1);
-    LayerStat* g = W.stat + static_cast<size_t>(spar) * kMaxActive;
+    // The field copies are identical between launches; the band list of
+    // slot4(s) was rebuilt by the host.
+    const long long s = P.step_begin;
+    const int cs = slot4(s);
+    LayerStat* g = W.stat + static_cast<size_t>(cs) * kMaxActive;
     for (int a = gtid; a < kMaxActive; a += gsz) reset_stat(g + a);
     if (gtid == 0) {
-      ctl->npairs = 0;
-      ctl->pair_overflow = 0;
-      ctl->base_max_bits = 0;
-      ctl->nbandpairs = 0;
+      ctl->npairs[cs] = 0;
+      ctl->pair_overflow[cs] = 0;
+      ctl->base_max_bits[cs] = 0;
+      ctl->nbandpairs[cs] = 0;
       ctl->bandpair_overflow = 0;
     }
     grid_sync_snap(ctl, SC);
     ++ep;
-    phase_union(M, F, W, P, lpar, ep, group_rank(P.map_mode & 8 ? 1 : 0), gsz / kG, SC.ilcount[lpar]);
-    grid_sync_snap(ctl, SC);
+    const FieldBuf& Fc = F.b[s & 1];
+    const int n = SC.ilcount[cs];
+    phase_union(M, Fc, W, P, cs, ep, group_rank(1), gsz / kG, n);
+    grid_sync(ctl);
     block_stats_init(S);
-    phase_stats(M, F, W, P, lpar, spar, ep, false, S, Q, SC.ilcount[lpar]);
-    block_stats_flush(S, g, P.n_active, ctl, &W);
+    phase_stats(M, Fc, W, P, s, ep, false, S, n, true, 0, nthr);
+    e_flush(S, W, P.n_active, s, 0, 0, nthr);
     grid_sync(ctl);
     if (gtid == 0) ctl->epoch = static_cast<long long>(ep);
     return;
   }
   if (kMode == 2) {
-    const int spar = static_cast<int>(P.step_begin & 1);
-    block_stats_init(S);
-    phase_snap(M, W, spar, S, W.ctl->nbandpairs);
-    block_stats_flush(S, W.stat + static_cast<size_t>(spar) * kMaxActive, P.n_active);
+    phase_snap(M, W, P.step_begin, ctl->nbandpairs[slot4(P.step_begin)], 0, nthr);
     return;
   }
   if (kMode == 3) {
-    const int spar = static_cast<int>(P.step_begin & 1);
-    if (gtid < P.n_active) flush_stat(M, W, P, gtid, spar, P.step_begin, true);
+    if (gtid < P.n_active) flush_stat(M, W, P, gtid, P.step_begin);
     return;
   }
 
-  // ---- mode 0: the step loop.  Per step s:
-  //   1  B(s)  commit, band-list append, next frontier  (+ snap of check s-1)
-  //   2  D(s)  union-find                                (+ trail flush of s-1)
-  //   3  E(s)  stats, collisions, list compaction        (+ speculative A(s+1))
-  // with a grid barrier after each; non-check steps run only 1 and A(s+1).
-  long long step = P.step_begin;
+  // ---- mode 0: the step loop.  Step s is one phase in the common case:
+  //   E(s)   the check of the field after s (stats, collisions, list compaction)
+  //   A(s+1) the update of step s+1 (b[s & 1] -> b[(s+1) & 1]) with its
+  //          bookkeeping (next frontier, band list, certificate items)
+  //   and, on other warps, the split certificate of s, the trail snap of
+  //   check s-1 and the trail records of check s-2.
+  // Without the certificate (4 % of the steps on configs[1]) the union-find
+  // D(s) runs beside A(s+1) and E(s) takes a phase of its own.  A(s+1) is
+  // speculative: when check s stops the run it is discarded (the host
+  // relaunches at s+1), and its errors count only if check s does not stop.
+  long long s = P.step_begin;
   int stop = 0;
-  bool pend = false;
-  bool first_check = true;  // the first check of a launch follows host edits: always the union-find
-  long long pend_step = 0;
-  {  // prologue: A(step_begin)
-    const int cur = static_cast<int>(step & 1);
+  bool first_check = true;     // the first check of a launch follows host edits: always the union-find
+  bool ran_spec = false;       // the stopping phase ran A(s+1)
+  long long snap_step = -1;    // check whose trail snap runs in the next phase
+  long long flush_step = -1;   // check whose trail records are written in the next phase
+  long long last_snapped = -1; // check snapped in the phase just ended
+  {  // prologue: A(step_begin), reading the field after step_begin - 1
     ctl_snap(ctl, SC);
-    const int nR = SC.rcount[cur];
+    const long long b = P.step_begin;
+    const int nR = SC.rcount[slot4(b)];
     if (gtid == 0) {
-      ctl->rcount[cur ^ 1] = 0;
+      phase_resets(ctl, b - 1);
+      ctl->base_cum[slot4(b - 1)] = ctl->base_one;
       ctl->sum_region += static_cast<unsigned long long>(nR);
-      for (int q = 0; q < 2; ++q) {
-        ctl->dchange[q] = 0;
-        ctl->nadded[q] = 0;
-        ctl->anchor_fail[q] = 0;
-      }
     }
-    for (int i = group_rank(P.map_mode & 2 ? 2 : 0); i < nR; i += gsz / kG)
-      if (!update_vertex_single(M, F, W, P, i, W.region[cur][i], false, threadIdx.x & (kG - 1), group_mask()) &&
-              !update_vertex_fast(M, F, W, P, i, W.region[cur][i], false, threadIdx.x & (kG - 1), group_mask()))
-        update_vertex(M, F, W, P, i, W.region[cur][i], false, threadIdx.x & (kG - 1), group_mask());
+    for (int i = group_rank(2); i < nR; i += gsz / kG) update_item(M, F, W, P, b, i, false, Q);
+    bq_flush(Q, &ctl->rcount[slot4(b + 1)], W.region[slot4(b + 1)]);
     grid_sync_snap(ctl, SC);
     if (SC.error) stop = kStopError;
   }
-  for (; stop == 0 && step < P.step_end; ++step) {
-    const int cur = static_cast<int>(step & 1), nxt = cur ^ 1;
-    const bool check = P.do_check && (step % P.check_interval == 0);
-    const bool more = step + 1 < P.step_end;
-    const long long pslot = (step - P.step_begin) * 4;
+  for (; stop == 0 && s < P.step_end; ++s) {
+    const bool check = P.do_check && (s % P.check_interval == 0);
+    const bool more = s + 1 < P.step_end;
+    const int c0 = slot4(s);
+    const FieldBuf& Fs = F.b[s & 1];  // the field after step s
+    const int nR1 = more ? SC.rcount[slot4(s + 1)] : 0;  // frontier s+1, final since the last barrier
+    const int nband = SC.ilcount[c0];
+    const long long pslot = (s - P.step_begin) * 4;
     const bool prof = W.prof && gtid == 0 && pslot + 3 < W.prof_cap;
     if (prof) W.prof[pslot] = gtimer();
-    // ---- 1: B(s)   (SC: snapshot taken after the previous barrier)
-    block_start(W, step - (P.step_end - 64), 0);
-    {
-      // The commits (first warps) and the trail snap of check s-1 (last
-      // warps) are independent and run side by side; both flush at the end.
-      const int nR = SC.rcount[cur];
-      block_stats_init(S);
-      for (int i = group_rank(P.map_mode & 4 ? 1 : 0); i < nR; i += gsz / kG)
-      {
-        INSTR_T0(t0);
-        commit_vertex(M, F, W, i, W.region[cur][i], static_cast<int>(step), nxt, lpar, threadIdx.x & (kG - 1),
-                      group_mask(), Q);
-        INSTR_REC(0, t0, (threadIdx.x & (kG - 1)) == 0);
-      }
-      if (pend && P.record_trails) phase_snap(M, W, static_cast<int>(pend_step & 1), S, SC.nbandpairs);
-      bq_flush(Q, &ctl->rcount[nxt], W.region[nxt]);
-      block_stats_flush(S, W.stat + static_cast<size_t>(pend_step & 1) * kMaxActive, pend ? P.n_active : 0);
-      if (gtid == 0) {
-        ctl->spec_error = 0;
-        ctl->hash_acc = 0;
-        ctl->dchange[nxt] = 0;  // the slot B(s+1) will fill; step s-1 is done with it
-        ctl->nadded[nxt] = 0;
-        ctl->anchor_fail[nxt] = 0;
-        // Outputs of E(s), appended while E runs: reset here, a barrier ahead.
-        // (This phase's trail snap reads the band pairs of check s-1 through
-        // the snapshot's count.)
-        ctl->ilcount[lpar ^ 1] = 0;
-        ctl->npairs = 0;
-        ctl->pair_overflow = 0;
-        ctl->base_max_bits = 0;
-        ctl->nbandpairs = 0;
-      }
+    if (gtid == 0) {
+      phase_resets(ctl, s);
+      ctl->base_cum[c0] = ctl->base_cum[slot4(s - 1)] + ctl->base_d[c0];
+      ctl->sum_region += static_cast<unsigned long long>(nR1);
+      if (check) ctl->sum_interest += static_cast<unsigned long long>(nband);
     }
-    block_done(W, step - (P.step_end - 64), 0);
-    grid_sync_snap(ctl, SC);
-    if (prof) W.prof[pslot + 1] = gtimer();
-    block_start(W, step - (P.step_end - 64), 1);
-    if (check) {
-      ++ep;
-      // ---- 2: D(s) + flush of the previous check's trail records
-      if (pend)
-        // Trail records of check s-1 on warp 4 of every CTA (idle in this
-        // phase), not on CTA 0's first warp, which runs E.
-        if ((threadIdx.x >> 5) == 4)
-          for (int a = (threadIdx.x & 31) * gridDim.x + blockIdx.x; a < P.n_active; a += 32 * gridDim.x)
-            flush_stat(M, W, P, a, static_cast<int>(pend_step & 1), pend_step, true);
-      pend = false;
-      const int nband = SC.ilcount[lpar];
-      const int nR1 = SC.rcount[nxt];  // final since B(s)
-      if (gtid == 0) ctl->sum_interest += static_cast<unsigned long long>(nband);
-      // Under the split certificate (anchor_test) the union-find is not
-      // needed, and E(s) runs in one phase with the speculative A(s+1).
-      const int spar = cur;
-      const bool skip = !P.d_full && P.check_interval == 1 && !first_check && !SC.dchange[cur];
-      // Frontier s+2 starts empty; the counter update is by thread 0 of the
-      // grid whichever warp role it has in this phase.
-      if (more && gtid == 0) {
-        ctl->rcount[cur] = 0;
-        ctl->sum_region += static_cast<unsigned long long>(nR1);
-      }
-      auto run_a = [&] {
-        for (int i = group_rank(P.map_mode & 2 ? 2 : 0); i < nR1; i += gsz / kG) {
-          INSTR_T0(t0);
-          if (!update_vertex_single(M, F, W, P, i, W.region[nxt][i], true, threadIdx.x & (kG - 1), group_mask()) &&
-              !update_vertex_fast(M, F, W, P, i, W.region[nxt][i], true, threadIdx.x & (kG - 1), group_mask())) {
-            update_vertex(M, F, W, P, i, W.region[nxt][i], true, threadIdx.x & (kG - 1), group_mask());
-            INSTR_REC(4, t0, (threadIdx.x & (kG - 1)) == 0);
-          } else {
-            INSTR_REC(3, t0, (threadIdx.x & (kG - 1)) == 0);
-          }
-        }
-      };
-      // The CTA-level flushes of E (each a __syncthreads) come after A, so
-      // the warps running A do not wait for the warps running E.
-      auto flush_e = [&] { block_stats_flush(S, W.stat + static_cast<size_t>(spar) * kMaxActive, P.n_active, ctl, &W); };
-      if (skip) {
-        // ---- 2+3: certificate, E(s) without roots, speculative A(s+1)
-        block_start(W, step - (P.step_end - 64), 2);
-        anchor_test(M, F, W, P, SC.nadded[cur], static_cast<int>(step));
-        if (P.do_hash) phase_hash(F, W, M.nv);
-        if (prof) W.prof[pslot + 2] = W.prof[pslot + 1];
-        block_stats_init(S);
-        // E occupies the first warps (spread map), A the last ones.  When they
-        // are disjoint, E flushes behind a named barrier of its own warps and
-        // A never waits for it; otherwise A runs first and E flushes at the
-        // end with __syncthreads.
-        const int e_per_cta = (nband + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x);
-        const int a_per_cta = (nR1 + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x);
-        const int e_warps = (e_per_cta + 31) / 32, a_warps = (a_per_cta + 3) / 4;
-        const bool e_alone = (P.map_mode & 3) == 3 && e_per_cta <= static_cast<int>(blockDim.x) &&
-                             a_per_cta <= static_cast<int>(blockDim.x) / kG &&
-                             e_warps + a_warps <= static_cast<int>(blockDim.x) / 32 && e_warps > 0;
-        if (e_alone) {
-          const int warp = threadIdx.x >> 5;
-          if (warp < e_warps) {
-            phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, nband, false);
-            flush_e_named(S, W.stat + static_cast<size_t>(spar) * kMaxActive, P.n_active, ctl, W, e_warps * 32);
-          } else if (more) {
-            run_a();
-          }
-        } else {
-          if (more) run_a();
-          phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, nband, false);
-          flush_e();
-        }
-        block_done(W, step - (P.step_end - 64), 2);
-        grid_sync_snap(ctl, SC);
-        if (SC.anchor_fail[cur]) {  // an unanchored new band item: the union-find after all
-          phase_union(M, F, W, P, lpar, ep, group_rank(P.map_mode & 8 ? 1 : 0), gsz / kG, nband);
-          grid_sync(ctl);
-          phase_roots(F, W, P, lpar, spar, ep, nband);
-          grid_sync(ctl);
-        }
-      } else {
-        // ---- 2: D(s) union-find
-        phase_union(M, F, W, P, lpar, ep, group_rank(P.map_mode & 8 ? 1 : 0), gsz / kG, nband);
-        if (P.do_hash) phase_hash(F, W, M.nv);
-        block_done(W, step - (P.step_end - 64), 1);
-        grid_sync(ctl);
-        if (prof) W.prof[pslot + 2] = gtimer();
-        block_start(W, step - (P.step_end - 64), 2);
-        // ---- 3: E(s) + speculative A(s+1)
-        block_stats_init(S);
-        phase_stats(M, F, W, P, lpar, spar, ep, true, S, Q, nband, true);
-        if (!more || P.split_a) flush_e();
-        if (more) {
-          if (P.split_a) {
-            grid_sync(ctl);
-            if (prof) W.prof[pslot + 3] = gtimer();
-          }
-          run_a();
-          if (!P.split_a) flush_e();
-        }
-        block_done(W, step - (P.step_end - 64), 2);
-        grid_sync_snap(ctl, SC);
-      }
-      if (prof && !P.split_a) W.prof[pslot + 3] = gtimer();
-      lpar ^= 1;
-      if (P.do_hash && gtid == 0) {
-        const long long slot = step - W.hash_base;
-        if (slot >= 0 && slot < W.hash_cap) W.hashes[slot] = ctl->hash_acc;
-      }
-      int bits = decide(W, P, spar);
-      if (P.stop_every_check) bits |= kStopEveryCheck;
-      if (bits) {
-        stop = bits;
-        break;  // the speculative A(s+1) is discarded; the host relaunches at s+1
-      }
-      if (SC.spec_error) {
-        if (gtid == 0) {
-          ctl->error = ctl->spec_error;
-          ctl->error_vertex = ctl->spec_error_vertex;
-        }
-        stop = kStopError;
-        ++step;  // the failing update belongs to step s+1
-        break;
-      }
-      pend = true;
-      pend_step = step;
-      first_check = false;
-    } else {
-      // ---- 3': trail flush of the previous check (its stats parity is
-      // reused two steps later) + A(s+1)
-      if (pend)
-        // Trail records of check s-1 on warp 4 of every CTA (idle in this
-        // phase), not on CTA 0's first warp, which runs E.
-        if ((threadIdx.x >> 5) == 4)
-          for (int a = (threadIdx.x & 31) * gridDim.x + blockIdx.x; a < P.n_active; a += 32 * gridDim.x)
-            flush_stat(M, W, P, a, static_cast<int>(pend_step & 1), pend_step, true);
-      pend = false;
-      if (more) {
-        const int nR1 = SC.rcount[nxt];  // snapshot after B(s)
-        if (gtid == 0) {
-          ctl->rcount[cur] = 0;
-          ctl->sum_region += static_cast<unsigned long long>(nR1);
-        }
-        for (int i = group_rank(P.map_mode & 2 ? 2 : 0); i < nR1; i += gsz / kG)
-          if (!update_vertex_single(M, F, W, P, i, W.region[nxt][i], false, threadIdx.x & (kG - 1), group_mask()) &&
-              !update_vertex_fast(M, F, W, P, i, W.region[nxt][i], false, threadIdx.x & (kG - 1), group_mask()))
-            update_vertex(M, F, W, P, i, W.region[nxt][i], false, threadIdx.x & (kG - 1), group_mask());
-      }
+    const long long fl = flush_step, sn = P.record_trails ? snap_step : -1;
+    const int n_ovf = sn >= 0 ? SC.nbandpairs[slot4(sn)] : 0;
+    // Earlier checks' trail work (no CTA barrier inside), by threads [t0, t0 + n).
+    auto side = [&](int t0, int n) {
+      if (fl >= 0) flush_range(M, W, P, fl, t0, n);
+      if (sn >= 0) phase_snap(M, W, sn, n_ovf, t0, n);
+    };
+    auto run_a = [&](bool spec) {
+      for (int i = group_rank(2); i < nR1; i += gsz / kG) update_item(M, F, W, P, s + 1, i, spec, Q);
+    };
+    const int q2 = slot4(s + 2);  // A(s+1) queues frontier s+2
+    last_snapped = snap_step;
+    if (!check) {
+      block_start(W, s - (P.step_end - 64), 1);
+      if (more) run_a(false);
+      carry_list(Fs, W, s, nband);
+      side(0, nthr);
+      bq_flush(Q, &ctl->rcount[q2], W.region[q2]);
+      block_done(W, s - (P.step_end - 64), 1);
       grid_sync_snap(ctl, SC);
+      if (prof) W.prof[pslot + 1] = W.prof[pslot + 2] = W.prof[pslot + 3] = gtimer();
+      flush_step = snap_step;
+      snap_step = -1;
       if (SC.error) {
         stop = kStopError;
-        ++step;
+        ++s;  // the failing update belongs to step s+1
         break;
       }
+      continue;
     }
-  }
-  if (stop == 0 && pend) {
-    // Budget exhausted right after a quiet check: finish its trail records.
+    ++ep;
+    const bool skip = !P.d_full && P.check_interval == 1 && !first_check && !SC.dchange[c0];
     block_stats_init(S);
-    if (P.record_trails) phase_snap(M, W, static_cast<int>(pend_step & 1), S, W.ctl->nbandpairs);
-    block_stats_flush(S, W.stat + static_cast<size_t>(pend_step & 1) * kMaxActive, P.n_active);
-    grid_sync(ctl);
-    for (int a = gtid; a < P.n_active; a += gsz) flush_stat(M, W, P, a, static_cast<int>(pend_step & 1), pend_step, true);
+    if (skip) {
+      // ---- certificate holds: one phase.  E on the first warps, A on the
+      // last ones, the certificate and the trail work in between; each role
+      // flushes behind a barrier of its own warps.
+      if (prof) W.prof[pslot + 1] = W.prof[pslot];
+      block_start(W, s - (P.step_end - 64), 1);
+      const int nwarps = nthr / 32;
+      const int e_per_cta = (nband + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x);
+      const int a_per_cta = (nR1 + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x);
+      const int e_warps = max(1, (e_per_cta + 31) / 32), a_warps = (a_per_cta + 3) / 4;
+      const bool split = !P.do_hash && e_per_cta <= nthr && a_per_cta <= nthr / kG && e_warps + a_warps <= nwarps;
+      if (split) {
+        const int warp = threadIdx.x >> 5;
+        const int m0 = e_warps, m1 = nwarps - a_warps;  // middle warps [m0, m1)
+        if (warp < m0) {
+          phase_stats(M, Fs, W, P, s, ep, true, S, nband, false, 0, m0 * 32);
+          if (m1 == m0) {  // no middle warps: E's warps take the rest
+            anchor_test(M, Fs, W, P, SC.nadded[c0], static_cast<int>(s),
+                        static_cast<int>(threadIdx.x) * static_cast<int>(gridDim.x) + blockIdx.x,
+                        m0 * 32 * static_cast<int>(gridDim.x));
+            side(0, m0 * 32);
+          }
+          e_flush(S, W, P.n_active, s, 1, 0, m0 * 32);
+        } else if (warp >= m1) {
+          if (more) run_a(true);
+          if (a_warps > 0) bq_flush(Q, &ctl->rcount[q2], W.region[q2], 2, m1 * 32, a_warps * 32);
+        } else {
+          const int r = static_cast<int>(threadIdx.x) - m0 * 32, nm = (m1 - m0) * 32;
+          anchor_test(M, Fs, W, P, SC.nadded[c0], static_cast<int>(s), r * static_cast<int>(gridDim.x) + blockIdx.x,
+                      nm * static_cast<int>(gridDim.x));
+          side(m0 * 32, nm);
+        }
+      } else {
+        if (more) run_a(true);
+        phase_stats(M, Fs, W, P, s, ep, true, S, nband, false, 0, nthr);
+        anchor_test(M, Fs, W, P, SC.nadded[c0], static_cast<int>(s), gtid, gsz);
+        side(0, nthr);
+        if (P.do_hash) phase_hash(Fs, &ctl->hash_acc[c0], M.nv);
+        e_flush(S, W, P.n_active, s, 0, 0, nthr);
+        bq_flush(Q, &ctl->rcount[q2], W.region[q2]);
+      }
+      block_done(W, s - (P.step_end - 64), 1);
+      grid_sync_snap(ctl, SC);
+      if (prof) W.prof[pslot + 2] = gtimer();
+      if (SC.anchor_fail[c0]) {  // an unanchored new band item: the union-find after all
+        block_start(W, s - (P.step_end - 64), 2);
+        phase_union(M, Fs, W, P, c0, ep, group_rank(1), gsz / kG, nband);
+        grid_sync(ctl);
+        phase_roots(Fs, W, P, c0, c0, ep, nband);
+        block_done(W, s - (P.step_end - 64), 2);
+        grid_sync(ctl);
+      }
+      if (prof) W.prof[pslot + 3] = gtimer();
+    } else {
+      // ---- D(s) beside A(s+1) and the trail work, then E(s) with roots.
+      block_start(W, s - (P.step_end - 64), 0);
+      if (more) run_a(true);
+      phase_union(M, Fs, W, P, c0, ep, group_rank(1), gsz / kG, nband);
+      side(0, nthr);
+      if (P.do_hash) phase_hash(Fs, &ctl->hash_acc[c0], M.nv);
+      bq_flush(Q, &ctl->rcount[q2], W.region[q2]);
+      block_done(W, s - (P.step_end - 64), 0);
+      grid_sync(ctl);
+      if (prof) W.prof[pslot + 1] = gtimer();
+      block_start(W, s - (P.step_end - 64), 1);
+      phase_stats(M, Fs, W, P, s, ep, true, S, nband, true, 0, nthr);
+      e_flush(S, W, P.n_active, s, 0, 0, nthr);
+      block_done(W, s - (P.step_end - 64), 1);
+      grid_sync_snap(ctl, SC);
+      if (prof) W.prof[pslot + 2] = W.prof[pslot + 3] = gtimer();
+    }
+    if (P.do_hash && gtid == 0) {
+      const long long slot = s - W.hash_base;
+      if (slot >= 0 && slot < W.hash_cap) W.hashes[slot] = ctl->hash_acc[c0];
+    }
+    first_check = false;
+    int bits = decide(W, P, s);
+    if (P.stop_every_check) bits |= kStopEveryCheck;
+    if (bits) {
+      stop = bits;
+      ran_spec = more;
+      break;  // A(s+1) is discarded; the host relaunches at s+1
+    }
+    if (SC.spec_error) {
+      if (gtid == 0) {
+        ctl->error = ctl->spec_error;
+        ctl->error_vertex = ctl->spec_error_vertex;
+      }
+      stop = kStopError;
+      ++s;  // the failing update belongs to step s+1
+      break;
+    }
+    flush_step = snap_step;
+    snap_step = s;
+  }
+  // ---- epilogue.  `last` is the last step whose results stand.
+  const long long last = stop ? s : s - 1;
+  if (!(stop & kStopError)) {
+    if (stop) {
+      // Stopped at check `last`: the host runs its snap and records; the
+      // check before it was snapped in the last phase.
+      if (last_snapped >= 0) flush_range(M, W, P, last_snapped, 0, nthr);
+    } else {
+      // Budget exhausted: finish the pending checks' trail work.
+      if (flush_step >= 0) flush_range(M, W, P, flush_step, 0, nthr);
+      if (snap_step >= 0) {
+        if (P.record_trails) phase_snap(M, W, snap_step, SC.nbandpairs[slot4(snap_step)], 0, nthr);
+        grid_sync(ctl);
+        flush_range(M, W, P, snap_step, 0, nthr);
+      }
+    }
+    // Both field copies identical again: the columns of frontier last+1 (every
+    // column step `last` changed, and every column a discarded A(last+1)
+    // overwrote) copied from the field after `last`.
+    {
+      const FieldBuf& A = F.b[last & 1];
+      const FieldBuf& B = F.b[(last + 1) & 1];
+      const int* list = W.region[slot4(last + 1)];
+      const int n = SC.rcount[slot4(last + 1)];
+      for (int i = gtid; i < n; i += gsz) {
+        const int v = list[i];
+        const int c = A.cnt[v];
+        const size_t vb = static_cast<size_t>(v) * kSlots;
+        for (int j = 0; j < c; ++j) {
+          B.lay[vb + j] = A.lay[vb + j];
+          B.val[vb + j] = A.val[vb + j];
+        }
+        B.cnt[v] = static_cast<unsigned char>(c);
+        B.interest[v] = A.interest[v];
+        B.binfo[v] = A.binfo[v];
+      }
+    }
+    if (ran_spec) {
+      // Unclaim the frontier the discarded A(last+1) queued, then re-stamp
+      // frontier last+1 (a vertex in both carried the newer stamp): the host
+      // adds to frontier last+1 and the relaunch queues frontier last+2.
+      const int* list = W.region[slot4(last + 2)];
+      const int n = SC.rcount[slot4(last + 2)];
+      for (int i = gtid; i < n; i += gsz) W.stamp[list[i]] = -1;
+      grid_sync(ctl);
+      const int* cur = W.region[slot4(last + 1)];
+      const int nc = SC.rcount[slot4(last + 1)];
+      for (int i = gtid; i < nc; i += gsz) W.stamp[cur[i]] = static_cast<int>(last);
+    }
   }
   if (gtid == 0) {
     ctl->stop_bits = stop;
-    ctl->stop_step = stop ? step : step - 1;
+    ctl->stop_step = last;
     ctl->epoch = static_cast<long long>(ep);
-    ctl->lpar = lpar;
+    if (!(stop & kStopError)) ctl->base_one = ctl->base_cum[slot4(last)];
+    for (int q = 0; q < 4; ++q) ctl->base_d[q] = 0;
   }
 #ifdef DTB_INSTR
   __syncthreads();

@@ -113,32 +113,44 @@ struct DevMesh {
   const int *n_off = nullptr, *n_col = nullptr;                   // mesh neighbours
 };
 
-// Control block in device memory (one per engine).
+// Per-step rotating slots.  The step loop runs E(s) (the check of step s)
+// and A(s+1) (the update of step s+1) in one phase, so every list and
+// counter that one step fills while another reads it rotates over four
+// slots, slot4(t) = t & 3: a slot is cleared only two grid barriers after its
+// last reader took it (the words read right after a barrier must stay put
+// through the phase that follows) and before its next writer starts.
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline int slot4(long long t) { return static_cast<int>(t & 3); }
+
+// Control block in device memory (one per engine).  The first 112 bytes are
+// the words every CTA snapshots after a grid barrier (CtlSnap).
 struct Ctl {
-  int rcount[2];             // frontier list sizes (parity = step & 1)
-  int ilcount[2];            // band-list sizes (double buffer, parity lpar)
-  int lpar;                  // which band list is current
-  int error;                 // DevError of a committed step
+  int rcount[4];       // frontier list sizes: frontier t is region[slot4(t)]
+  int ilcount[4];      // band-list sizes: the list E(t) reads is ilist[slot4(t)]
+  int error;           // DevError of a committed step
+  int spec_error;      // error raised by a speculative update (next step)
+  int dchange[4];      // by slot4(step): the step removed a band item (or overflowed a band index / list)
+  int nadded[4];       // by slot4(step): band items added (W.added)
+  int anchor_fail[4];  // by slot4(step): an added band item lacks a neighbour of the previous band
+  int nbandpairs[4];   // by slot4(check): band items of that check in the overflow list
+  int pad_[2];
   int error_vertex;
-  int spec_error;            // error raised by a speculative update (next step)
-  int dchange[2];            // by step parity: the step removed a band item (or overflowed a band index / list)
-  int nadded[2];             // by step parity: band items added (W.added)
-  int anchor_fail[2];        // by step parity: an added band item lacks a neighbour of the previous band
-  int nbandpairs;            // band items of the last check in the overflow list
-  int pad_;
   int spec_error_vertex;
   int stop_bits;
+  int pad0_;
   long long stop_step;       // last step executed by the kernel
   long long epoch;           // union-find / pair-set version
-  int base_one;              // number of vertices whose base value is exactly 1.0
-  unsigned long long base_max_bits;  // max base value in (0,1) (as ordered bits)
-  int npairs;                // collision pairs recorded this check
-  int pair_overflow;
+  int base_one;              // vertices whose base value is exactly 1.0 (between launches)
+  int base_d[4];             // by slot4(step): that step's change of the count
+  int base_cum[4];           // by slot4(step): the count after that step
+  unsigned long long base_max_bits[4];  // by slot4(check): max base value in (0,1) (as ordered bits)
+  int npairs[4];             // by slot4(check): collision pairs recorded
+  int pair_overflow[4];
   int ntrail;                // trail records written (ring index)
   int bandpair_overflow;
-  unsigned bar_count;        // grid barrier
-  unsigned bar_gen;
-  unsigned long long hash_acc;  // field digest accumulator
+  unsigned long long hash_acc[4];   // by slot4(check): field digest accumulator
   unsigned long long sum_region;    // work counters: frontier vertices updated
   unsigned long long sum_interest;  // band-list vertices checked
 };
@@ -156,7 +168,8 @@ struct TrailRec {
   double vx, vy, vz;  // position of `vertex` (the trail point)
 };
 
-struct DevField {
+// One copy of the field columns.
+struct FieldBuf {
   unsigned char *cnt = nullptr;   // nv
   unsigned short *lay = nullptr;  // nv * kSlots
   double *val = nullptr;          // nv * kSlots
@@ -166,35 +179,36 @@ struct DevField {
   uint4 *binfo = nullptr;
 };
 
+// The field Phi^T, double-buffered by step parity: the update of step t
+// reads b[(t-1) & 1] and writes b[t & 1] directly (no scratch, no commit
+// phase).  Between launches both copies are identical; host edits write both.
+struct DevField {
+  FieldBuf b[2];
+};
+
 struct DevWork {
-  int *region[2] = {nullptr, nullptr};  // region lists
-  int *stamp = nullptr;                 // per vertex: step whose advance queued it
-  unsigned char *scnt = nullptr;        // scratch columns per region slot
-  unsigned short *slay = nullptr;
-  double *sval = nullptr;
-  unsigned char *sflag = nullptr;         // bit 0 changed, 1 old base==1, 2 new base==1, 3 interest
-  uint4 *sbinfo = nullptr;               // band index of each scratch column
-  int *ilist[2] = {nullptr, nullptr};   // band lists (double buffer); dead entries skipped
-  unsigned char *in_list = nullptr;     // vertex is in the current band list
-  // (vertex, dense active index) band items of the last check: one segment
-  // of bp_seg entries per CTA (appended with a shared-memory counter, length
-  // in bpcount[cta]), entries beyond a full segment in the shared overflow
-  // list bp_ovf (length Ctl::nbandpairs).
-  int2 *bandpairs = nullptr;
-  int *bpcount = nullptr;
+  int *region[4] = {nullptr, nullptr, nullptr, nullptr};  // frontier lists by slot4(step)
+  int *stamp = nullptr;                 // per vertex: step whose update queued it
+  int *ilist[4] = {nullptr, nullptr, nullptr, nullptr};   // band lists by slot4(step); dead entries skipped
+  // (vertex, dense active index) band items of a check: one segment of bp_seg
+  // entries per CTA (appended with a shared-memory counter, length in
+  // bpcount[set][cta]), entries beyond a full segment in the overflow list
+  // bp_ovf[set] (length Ctl::nbandpairs[slot4(check)]); set = check & 1.
+  int2 *bandpairs[2] = {nullptr, nullptr};
+  int *bpcount[2] = {nullptr, nullptr};
   int bp_nseg = 0, bp_seg = 0;
-  int2 *bp_ovf = nullptr;
-  int bandpair_cap = 0;                 // capacity of bp_ovf
+  int2 *bp_ovf[2] = {nullptr, nullptr};
+  int bandpair_cap = 0;                 // capacity of each bp_ovf
   unsigned long long *parent = nullptr; // nv * kSlots versioned UF parents
-  int2 *added = nullptr;                // 2 x added_cap band items (vertex, layer) gained, by step parity
+  int2 *added = nullptr;                // 4 x added_cap band items (vertex, layer) gained, by slot4(step)
   int added_cap = 0;
   int *add_stamp = nullptr;             // per vertex: last step at which it gained a band item
   unsigned char *active = nullptr;      // kMaxLayers + 1
   int *aidx = nullptr;                  // layer -> dense active index or -1
   int *alist = nullptr;                 // dense active index -> layer
-  LayerStat *stat = nullptr;            // 2 x kMaxActive (parity = step & 1)
+  LayerStat *stat = nullptr;            // 4 x kMaxActive (slot4(check))
   unsigned long long *pair_keys = nullptr;  // kPairCap versioned keys
-  unsigned *pairs = nullptr;            // recorded pairs (first << 16 | second)
+  unsigned *pairs = nullptr;            // 4 x kPairCap recorded pairs (first << 16 | second), slot4(check)
   double *lastpos = nullptr;            // 4 * (kMaxLayers + 1): x, y, z, valid
   TrailRec *trail = nullptr;            // trail_mask + 1 records (a power of two <= kTrailCap)
   int trail_mask = 0;
@@ -217,10 +231,7 @@ struct StepParams {
   int do_hash;
   int stop_every_check;
   int do_check;  // 0: advance only (one-shot step())
-  int split_a;   // diagnostics: run the next step's update in its own phase
-  int split_a_no_unite;  // diagnostics only: skip unions (wrong results; timing)
-  int d_full;            // diagnostics: never skip the front union-find (DTB_D_FULL=1)
-  int map_mode;          // work-to-CTA maps, bits: 1 spread E, 2 A from the last warp, 4 spread B, 8 spread D
+  int d_full;    // diagnostics: never skip the front union-find (DTB_D_FULL=1)
 };
 
 // --- launchers (kernels.cu) -------------------------------------------------
@@ -305,10 +316,13 @@ int launch_spmv(int nv, const int* off, const int* col, const double* val, const
 // Field edit / query helpers (fieldops.cu).
 int launch_init_field(const DevField& f, const DevWork& w, int nv, const int* seeds, int nseeds,
                       void* stream);
+// Queues verts and their stiffness rows into region[slot] with `stamp`.
 int launch_mark_region(const DevMesh& m, const DevWork& w, const int* verts, int n, long long stamp,
-                       int parity, void* stream);
+                       int slot, void* stream);
 int launch_mark_all_support(const DevMesh& m, const DevField& f, const DevWork& w, long long stamp,
-                            int parity, void* stream);
+                            int slot, void* stream);
+// The band list ilist[slot] rebuilt from the interest flags (order free).
+int launch_rebuild_list(const DevField& f, const DevWork& w, int nv, int slot, void* stream);
 int launch_pull_layer(const DevField& f, int nv, int layer, int* out_v, double* out_x, int* out_n,
                       void* stream);
 int launch_relabel(const DevField& f, const DevWork& w, const int* verts, const int* newlayer, int n,
