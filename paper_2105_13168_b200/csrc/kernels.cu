@@ -86,6 +86,24 @@ __device__ __forceinline__ void instr_cp(int idx, unsigned long long t0) {
     atomicAdd(&s_cp[idx][1], 1u);
   }
 }
+// Phase timeline: cycles since the CTA's phase start (set where the control
+// snapshot is taken), checkpoint `idx` recorded by the first lane of each
+// 8-lane group (or of each warp with instr_at_w); `dep` orders the clock read
+// after the value it depends on.
+__shared__ unsigned long long s_pt0;
+__device__ __forceinline__ void instr_at(int idx, unsigned dep, unsigned lanes = 7) {
+  // The clock read is predicated on `dep`, so it cannot issue before dep arrives.
+  unsigned long long c = 0;
+  asm volatile("{ .reg .pred p; setp.ne.u32 p, %1, 0x7fffffff; @p mov.u64 %0, %%clock64; }" : "+l"(c) : "r"(dep));
+  if ((threadIdx.x & lanes) == 0) {
+    atomicAdd(&s_cp[idx][0], static_cast<unsigned>((c - s_pt0) >> 4));
+    atomicAdd(&s_cp[idx][1], 1u);
+  }
+}
+#define INSTR_AT(idx, dep) instr_at(idx, static_cast<unsigned>(dep))
+#define INSTR_AT_W(idx, dep) instr_at(idx, static_cast<unsigned>(dep), 31)
+#define INSTR_PHASE() \
+  if (threadIdx.x == 0) s_pt0 = static_cast<unsigned long long>(clock64())
 #define INSTR_CP(idx, t0) instr_cp(idx, t0)
 #define INSTR_C0(name) const unsigned long long name = static_cast<unsigned long long>(clock64())
 #define INSTR_T0(name) const unsigned long long name = gtimer()
@@ -98,6 +116,9 @@ __device__ __forceinline__ void instr_cp(int idx, unsigned long long t0) {
 #define INSTR_REC(ph, name, cond)
 #define INSTR_CP(idx, t0)
 #define INSTR_C0(name)
+#define INSTR_AT(idx, dep)
+#define INSTR_AT_W(idx, dep)
+#define INSTR_PHASE()
 #endif
 
 // Diagnostics (DTB_PHASE_PROF): per-CTA completion time of phase `ph` of the
@@ -150,6 +171,7 @@ __device__ __forceinline__ void ctl_snap(const Ctl* ctl, CtlSnap& sc) {
     int4* dst = reinterpret_cast<int4*>(&sc);
 #pragma unroll
     for (int q = 0; q < 7; ++q) dst[q] = __ldcg(src + q);
+    INSTR_PHASE();
   }
   __syncthreads();
 }
@@ -166,6 +188,7 @@ struct Hdr {
   unsigned flag;
   uint4 bi;
 };
+constexpr unsigned kHandled = 0x100u;  // Hdr::flag: the update path applied (on every lane of the group)
 
 // set_value semantics (layer_field.hpp:102): clamp above 1, prune below the
 // epsilon, erase zeros; `changed` records whether the stored value moved.
@@ -217,6 +240,55 @@ constexpr int kG = 8;    // lanes per vertex group
 constexpr int kReg = 4;  // neighbour-column slots kept in registers (packed as 2x2 u16 below)
 
 __device__ __forceinline__ unsigned group_mask() { return 0xFFu << (threadIdx.x & 24); }
+
+// 8-lane group operations on the lanes that execute them together: the mask
+// is __activemask() (as in cooperative_groups::coalesced_threads), which
+// holds whole groups -- the lanes of a group never diverge from each other in
+// the update paths -- and is the same on every participating lane.  A
+// per-group mask (0xFF << group) differs between the groups of a warp and
+// makes each vote / reduction / shuffle ~10x slower on sm_100a
+// (tools/fp64_lat.cu: redux 345 vs 31 cycles, vote.any 304 vs 44).
+constexpr unsigned kFull = 0xffffffffu;
+__device__ __forceinline__ bool seg_any8(bool p) {
+  return ((__ballot_sync(__activemask(), p) >> (threadIdx.x & 24)) & 0xFFu) != 0;
+}
+__device__ __forceinline__ unsigned seg_min8(unsigned x) {
+  const unsigned am = __activemask();
+  x = min(x, __shfl_xor_sync(am, x, 4));
+  x = min(x, __shfl_xor_sync(am, x, 2));
+  return min(x, __shfl_xor_sync(am, x, 1));
+}
+__device__ __forceinline__ unsigned seg_max8(unsigned x) {
+  const unsigned am = __activemask();
+  x = max(x, __shfl_xor_sync(am, x, 4));
+  x = max(x, __shfl_xor_sync(am, x, 2));
+  return max(x, __shfl_xor_sync(am, x, 1));
+}
+
+// Element i of a small pointer array held in a kernel parameter, by selects:
+// a dynamic index into a parameter array makes the compiler copy the whole
+// parameter struct to local memory and load the pointer back from there (a
+// dependent memory round trip in front of every use).
+template <class T>
+__device__ __forceinline__ T pick2(const T (&a)[2], int i) {
+  return i ? a[1] : a[0];
+}
+template <class T>
+__device__ __forceinline__ T pick4(const T (&a)[4], int i) {
+  const T lo = (i & 1) ? a[1] : a[0];
+  const T hi = (i & 1) ? a[3] : a[2];
+  return (i & 2) ? hi : lo;
+}
+__device__ __forceinline__ FieldBuf pickf(const DevField& F, long long t) {  // F.b[t & 1]
+  FieldBuf r;
+  const bool odd = (t & 1) != 0;
+  r.cnt = odd ? F.b[1].cnt : F.b[0].cnt;
+  r.lay = odd ? F.b[1].lay : F.b[0].lay;
+  r.val = odd ? F.b[1].val : F.b[0].val;
+  r.interest = odd ? F.b[1].interest : F.b[0].interest;
+  r.binfo = odd ? F.b[1].binfo : F.b[0].binfo;
+  return r;
+}
 
 // Dynamic shared memory: one slab per 8-lane group, used either for the fold
 // staging of the fast update or for the work arrays of the general update
@@ -272,8 +344,12 @@ __device__ __forceinline__ void column_header(const FieldBuf& Fo, const DevWork&
     inter |= x > 0.0 && x < 1.0;
     if (l != 0 && x > W.band_lo && x < W.sat) {
       if (nb < 4) {
-        L[nb] = l;
-        S[nb] = static_cast<unsigned>(j);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)  // constant indices: L and S stay in registers
+          if (q == nb) {
+            L[q] = l;
+            S[q] = static_cast<unsigned>(j);
+          }
         ++nb;
       } else {
         over = true;
@@ -291,11 +367,14 @@ __device__ __forceinline__ void column_header(const FieldBuf& Fo, const DevWork&
   Fo.cnt[v] = static_cast<unsigned char>(n);
   Fo.interest[v] = inter ? 1 : 0;
   h.bi = bi;
-  h.flag = 0x80u | (changed ? 1u : 0u) | (old_one ? 2u : 0u) | (new_one ? 4u : 0u) | (inter ? 8u : 0u);
+  h.flag = kHandled | 0x80u | (changed ? 1u : 0u) | (old_one ? 2u : 0u) | (new_one ? 4u : 0u) | (inter ? 8u : 0u);
 }
 
-__device__ void update_vertex(const DevMesh& M, const FieldBuf& F, const FieldBuf& Fo, const DevWork& W,
-                              const StepParams& P, int v, bool spec, int lane, unsigned gm, Hdr& h) {
+__device__ Hdr update_vertex(const DevMesh& M, const FieldBuf& F, const FieldBuf& Fo, const DevWork& W,
+                             const StepParams& P, int v, bool spec, int lane, unsigned gm) {
+  Hdr h;
+  h.flag = kHandled;
+  h.bi = make_uint4(0, 0, 0, 0);
   // Work arrays in the group's shared-memory slab.  Every lane of the group
   // runs this code with the same values, so each lane reads back what it
   // (and its siblings, identically) wrote.
@@ -417,7 +496,6 @@ __device__ void update_vertex(const DevMesh& M, const FieldBuf& F, const FieldBu
       }
     }
   }
-  INSTR_CP(6, tU);
   // From here on lane 0 alone: the candidate list and the working column live
   // in the group's slab, so only one lane may write them.  (Its siblings meet
   // it again at the group's next shuffle or __syncwarp.)
@@ -441,7 +519,7 @@ __device__ void update_vertex(const DevMesh& M, const FieldBuf& F, const FieldBu
   }
   if (overflow) {
     raise_error(W.ctl, kDevCapacity, v, spec);
-    return;
+    return h;
   }
 
   const double mass = __ldg(M.mass + v);
@@ -464,7 +542,7 @@ __device__ void update_vertex(const DevMesh& M, const FieldBuf& F, const FieldBu
     const double rate = -P.mu_n * inner;
     if (!isfinite(rate)) {
       raise_error(W.ctl, kDevBlowup, v, spec);
-      return;
+      return h;
     }
     const double next = clamp01(phi + P.dt * rate);
     if (next != phi) {
@@ -483,7 +561,7 @@ __device__ void update_vertex(const DevMesh& M, const FieldBuf& F, const FieldBu
                         P.m_mu_n * (P.w * phib + P.half_a2 * lap_b);
     if (!isfinite(rate)) {
       raise_error(W.ctl, kDevBlowup, v, spec);
-      return;
+      return h;
     }
     const double next = clamp01(phib + P.dt * rate);
     if (next != phib) {
@@ -497,7 +575,7 @@ __device__ void update_vertex(const DevMesh& M, const FieldBuf& F, const FieldBu
     for (int j = 0; j < nn; ++j) s = s + nx[j];
     if (s <= 0.0) {
       raise_error(W.ctl, kDevZeroColumn, v, spec);
-      return;
+      return h;
     }
     if (!(fabs(s - 1.0) < 1e-15)) {
       const int sn = nn;
@@ -510,7 +588,7 @@ __device__ void update_vertex(const DevMesh& M, const FieldBuf& F, const FieldBu
   }
   if (!ok || nn > kSlots) {
     raise_error(W.ctl, kDevCapacity, v, spec);
-    return;
+    return h;
   }
   const bool old_one = cv > 0 && ol[0] == 0 && ox[0] == 1.0;
   const bool new_one = nn > 0 && nl[0] == 0 && nx[0] == 1.0;
@@ -520,7 +598,7 @@ __device__ void update_vertex(const DevMesh& M, const FieldBuf& F, const FieldBu
     Fo.val[o + j] = nx[j];
   }
   column_header<0>(Fo, W, v, nn, nl, nx, changed, old_one, new_one, h);
-  INSTR_CP(15, tU);
+  return h;
 }
 
 // ---------------------------------------------------------------------------
@@ -635,7 +713,6 @@ __device__ __forceinline__ bool gather_fold(const DevMesh& M, const FieldBuf& F,
       }
   }
   if (__any_sync(gm, cu > kReg)) return false;
-  INSTR_CP(12, tG);
   unsigned omask = 0;
 #pragma unroll
   for (int q = 0; q < kF; ++q)
@@ -659,7 +736,6 @@ __device__ __forceinline__ bool gather_fold(const DevMesh& M, const FieldBuf& F,
     last = m;
     ++nc;
   }
-  INSTR_CP(13, tG);
   // Contributions, staged per lane.
   double* s_fold = reinterpret_cast<double*>(group_slab());  // [lane][kFoldCols]
   const int base = threadIdx.x & ~(kG - 1);
@@ -694,7 +770,6 @@ __device__ __forceinline__ bool gather_fold(const DevMesh& M, const FieldBuf& F,
       if ((use >> jj) & 1) acc = acc + s_fold[jj * kFoldCols + lane];
   }
   __syncwarp(gm);  // s_fold is reused by the group's next vertex
-  INSTR_CP(14, tG);
 #pragma unroll
   for (int c = 0; c < kF; ++c) Ca[c] = __shfl_sync(gm, acc, c, kG);
   lapb = __shfl_sync(gm, acc, kF, kG);
@@ -710,10 +785,17 @@ __device__ __forceinline__ bool gather_fold(const DevMesh& M, const FieldBuf& F,
 // neighbours without L, which leaves a sum of positive-valued terms (never
 // -0.0) unchanged.  Every lane folds the two sums from shuffles and runs the
 // sequential update (the general fast path's arithmetic, term for term);
-// lanes 0..n-1 store the new column.  Returns false, with no side effects,
-// when the case does not apply.
-__device__ bool update_vertex_single(const DevMesh& M, const FieldBuf& F, const FieldBuf& Fo, const DevWork& W,
-                                     const StepParams& P, int v, bool spec, int lane, unsigned gm, Hdr& h) {
+// lanes 0..n-1 store the new column.
+//
+// The group-level votes and reductions use the mask of the lanes executing
+// together (seg_any8): in the common case the whole warp, a single fast
+// instruction.  Not handled (flag 0, no side effects) when the case does not
+// apply; with act false the group only rides along (no side effects).
+__device__ Hdr update_vertex_single(const DevMesh& M, const FieldBuf& F, const FieldBuf& Fo, const DevWork& W,
+                                    const StepParams& P, int v, bool act, bool spec, int lane) {
+  Hdr h;
+  h.flag = 0;
+  h.bi = make_uint4(0, 0, 0, 0);
   const int cv = F.cnt[v];
   const size_t vb = static_cast<size_t>(v) * kSlots;
   const unsigned own_lw = *reinterpret_cast<const unsigned*>(F.lay + vb);  // slots 0, 1
@@ -726,18 +808,18 @@ __device__ bool update_vertex_single(const DevMesh& M, const FieldBuf& F, const 
   const bool valid = lane < rlen;
   const int u = valid ? u_e : 0;
   const double s = valid ? s_e : 0.0;
-  const int k0 = 0, k1 = rlen;
   const size_t ub = static_cast<size_t>(u) * kSlots;
   const int cu = valid ? static_cast<int>(F.cnt[u]) : 0;
   const unsigned nlw = valid ? *reinterpret_cast<const unsigned*>(F.lay + ub) : 0u;
   const double2 nx = valid ? *reinterpret_cast<const double2*>(F.val + ub) : make_double2(0.0, 0.0);
-  if (cv > 2 || k1 - k0 > kG) return false;  // group-uniform
+  INSTR_AT(2, own_lw);
+  INSTR_AT(3, nlw);
   // Own column: [base][, L] or [L].
   const unsigned o0 = own_lw & 0xFFFFu, o1 = own_lw >> 16;
   const double phib = (cv > 0 && o0 == 0) ? own_x.x : 0.0;
   unsigned ol = 0;  // own non-base layer (0: none)
   double ox = 0.0;
-  bool bad = false;
+  bool bad = cv > 2 || rlen > kG;
   if (cv == 1 && o0 != 0) {
     ol = o0;
     ox = own_x.x;
@@ -769,28 +851,32 @@ __device__ bool update_vertex_single(const DevMesh& M, const FieldBuf& F, const 
   // Activity of the non-base layers, looked up as soon as each is known
   // (not after the group agrees on L, which would add a dependent round).
   const bool act_ok = (ol == 0 || W.active[ol]) && (nl == 0 || W.active[nl]);
-  if (__any_sync(gm, bad || !act_ok)) return false;
   // One common non-base layer L across v and its neighbours.
-  const unsigned lo = __reduce_min_sync(gm, min(nl ? nl : 0xFFFFFFFFu, ol ? ol : 0xFFFFFFFFu));
-  const unsigned hi = __reduce_max_sync(gm, max(nl, ol));
+  const unsigned lo = seg_min8(min(nl ? nl : 0xFFFFFFFFu, ol ? ol : 0xFFFFFFFFu));
+  const unsigned hi = seg_max8(max(nl, ol));
   const bool has_l = lo != 0xFFFFFFFFu;
-  if (has_l && lo != hi) return false;
+  const bool fits = !seg_any8(bad || !act_ok) && !(has_l && lo != hi);
+  if (!fits) return h;  // this group falls back (group-uniform)
+  INSTR_AT(11, 1u);
   const unsigned L = has_l ? lo : 0u;
   // Ordered folds of s_j * bu_j and s_j * x_j(L) (au_j) over the row.
   const double tb = s * bu, tt = s * xl;
   const bool bpos = valid && bu > 0.0;
   double lapb = 0.0, lapt = 0.0;
-  const int nvalid = k1 - k0;
+  const int nvalid = rlen;
+  const unsigned am = __activemask();  // whole groups, see seg_any8
 #pragma unroll
   for (int jj = 0; jj < kG; ++jj) {
-    const double b_ = __shfl_sync(gm, tb, jj, kG);
-    const double t_ = __shfl_sync(gm, tt, jj, kG);
+    const double b_ = __shfl_sync(am, tb, jj, kG);
+    const double t_ = __shfl_sync(am, tt, jj, kG);
     if (jj < nvalid) {
       lapb = lapb + b_;
       lapt = lapt + t_;
     }
   }
-  const bool bnear = phib > 0.0 || __any_sync(gm, bpos);
+  const bool bnear = phib > 0.0 || seg_any8(bpos);
+  h.flag = kHandled;
+  if (!act) return h;
   // ---- the sequential update (uniform across the group's lanes)
   const double lap_b = lapb / mass;
   bool touched = false, cupd = false, bupd = false;
@@ -803,7 +889,7 @@ __device__ bool update_vertex_single(const DevMesh& M, const FieldBuf& F, const 
       const double rate = -P.mu_n * inner;
       if (!isfinite(rate)) {
         if (lane == 0) raise_error(W.ctl, kDevBlowup, v, spec);
-        return true;
+        return h;
       }
       const double next = clamp01(phi + P.dt * rate);
       if (next != phi) {
@@ -813,6 +899,7 @@ __device__ bool update_vertex_single(const DevMesh& M, const FieldBuf& F, const 
       }
     }
   }
+  INSTR_AT(12, static_cast<unsigned>(__double_as_longlong(lapt)) ^ static_cast<unsigned>(__double_as_longlong(lapb)));
   if (bnear) {
     double total = 0.0, contact = 0.0;
     if (ol != 0) total = total + ox;  // ol == L, active
@@ -822,7 +909,7 @@ __device__ bool update_vertex_single(const DevMesh& M, const FieldBuf& F, const 
                         P.m_mu_n * (P.w * phib + P.half_a2 * lap_b);
     if (!isfinite(rate)) {
       if (lane == 0) raise_error(W.ctl, kDevBlowup, v, spec);
-      return true;
+      return h;
     }
     const double next = clamp01(phib + P.dt * rate);
     if (next != phib) {
@@ -831,6 +918,7 @@ __device__ bool update_vertex_single(const DevMesh& M, const FieldBuf& F, const 
       bnext = next;
     }
   }
+  INSTR_AT(13, static_cast<unsigned>(__double_as_longlong(bnext)) ^ static_cast<unsigned>(__double_as_longlong(cn)));
   // set_value into the (at most two-entry) column, sorted by layer.
   bool changed = false;
   unsigned El[2] = {0, 0};
@@ -892,30 +980,47 @@ __device__ bool update_vertex_single(const DevMesh& M, const FieldBuf& F, const 
       changed = true;
     }
   }
-  // Column normalisation of touched vertices (layer_field.hpp:143).
+  INSTR_AT(14, static_cast<unsigned>(__double_as_longlong(Ex[0])));
+  // Column normalisation of touched vertices (layer_field.hpp:143), written
+  // out for n <= 2 so the column stays in registers (the loop's sums and
+  // divisions, term for term; both divisions issue together).
   if (touched) {
     double ssum = 0.0;
-    for (int j = 0; j < n; ++j) ssum = ssum + Ex[j];
+    if (n > 0) ssum = ssum + Ex[0];
+    if (n > 1) ssum = ssum + Ex[1];
     if (ssum <= 0.0) {
       if (lane == 0) raise_error(W.ctl, kDevZeroColumn, v, spec);
-      return true;
+      return h;
     }
     if (!(fabs(ssum - 1.0) < 1e-15)) {
+      double q0 = Ex[0] / ssum, q1 = Ex[1] / ssum;
+      if (q0 > 1.0) q0 = 1.0;
+      if (q0 < P.prune) q0 = 0.0;
+      if (q1 > 1.0) q1 = 1.0;
+      if (q1 < P.prune) q1 = 0.0;
+      if (n > 0 && q0 != Ex[0]) changed = true;
+      if (n > 1 && q1 != Ex[1]) changed = true;
+      const unsigned l0 = El[0], l1 = El[1];
       int m = 0;
-      for (int j = 0; j < n; ++j) {
-        double q = Ex[j] / ssum;
-        if (q > 1.0) q = 1.0;
-        if (q < P.prune) q = 0.0;
-        if (q != Ex[j]) changed = true;
-        if (q != 0.0) {
-          El[m] = El[j];
-          Ex[m] = q;
-          ++m;
+      if (n > 0 && q0 != 0.0) {
+        El[0] = l0;
+        Ex[0] = q0;
+        m = 1;
+      }
+      if (n > 1 && q1 != 0.0) {
+        if (m == 0) {
+          El[0] = l1;
+          Ex[0] = q1;
+        } else {
+          El[1] = l1;
+          Ex[1] = q1;
         }
+        ++m;
       }
       n = m;
     }
   }
+  INSTR_AT(15, static_cast<unsigned>(n));
   const bool old_one = cv > 0 && o0 == 0 && own_x.x == 1.0;
   const bool new_one = n > 0 && El[0] == 0 && Ex[0] == 1.0;
   const size_t o = static_cast<size_t>(v) * kSlots;
@@ -939,13 +1044,16 @@ __device__ bool update_vertex_single(const DevMesh& M, const FieldBuf& F, const 
     Fo.cnt[v] = static_cast<unsigned char>(n);
     Fo.interest[v] = inter ? 1 : 0;
     h.bi = bi;
-    h.flag = 0x80u | (changed ? 1u : 0u) | (old_one ? 2u : 0u) | (new_one ? 4u : 0u) | (inter ? 8u : 0u);
+    h.flag = kHandled | 0x80u | (changed ? 1u : 0u) | (old_one ? 2u : 0u) | (new_one ? 4u : 0u) | (inter ? 8u : 0u);
   }
-  return true;
+  return h;
 }
 
-__device__ bool update_vertex_fast(const DevMesh& M, const FieldBuf& F, const FieldBuf& Fo, const DevWork& W,
-                                   const StepParams& P, int v, bool spec, int lane, unsigned gm, Hdr& h) {
+__device__ Hdr update_vertex_fast(const DevMesh& M, const FieldBuf& F, const FieldBuf& Fo, const DevWork& W,
+                                  const StepParams& P, int v, bool spec, int lane, unsigned gm) {
+  Hdr h;
+  h.flag = 0;
+  h.bi = make_uint4(0, 0, 0, 0);
   INSTR_C0(tA);
   // Every load below is independent of the counts it is masked with, so the
   // column, stiffness row and neighbour columns arrive in three dependent
@@ -970,8 +1078,7 @@ __device__ bool update_vertex_fast(const DevMesh& M, const FieldBuf& F, const Fi
   }
   const int k0 = __ldg(M.s_off + v), k1 = __ldg(M.s_off + v + 1);
   const double mass = __ldg(M.mass + v);
-  if (cv > kF) return false;
-  INSTR_CP(0, tA);
+  if (cv > kF) return h;
 #pragma unroll
   for (int q = 0; q < kF; ++q)
     if (q >= cv) {
@@ -993,7 +1100,6 @@ __device__ bool update_vertex_fast(const DevMesh& M, const FieldBuf& F, const Fi
   bool bnear = phib > 0.0;
   const bool folded =
       k1 - k0 <= kG && gather_fold(M, F, W, v, cv, Ol, k0, k1, lane, gm, Cl, Ca, nc, lapb, lapt, bnear);
-  INSTR_CP(1, tA);
   if (!folded) {
   for (int kb = k0; kb < k1; kb += kG) {
     const int k = kb + lane;
@@ -1083,7 +1189,7 @@ __device__ bool update_vertex_fast(const DevMesh& M, const FieldBuf& F, const Fi
       if (!found) cand_add_reg(Cl, Ca, nc, over, Ol[q], 0.0);
     }
   }  // generic gather
-  if (over) return false;
+  if (over) return h;
 
   const double lap_b = lapb / mass;
   // Candidate updates run one per lane (lanes 0..nc-1) and the base update on
@@ -1157,7 +1263,8 @@ __device__ bool update_vertex_fast(const DevMesh& M, const FieldBuf& F, const Fi
   }
   if (__any_sync(gm, my_blow)) {  // every path raises the same error for v
     if (lane == 0) raise_error(W.ctl, kDevBlowup, v, spec);
-    return true;
+    h.flag = kHandled;
+    return h;
   }
   bool Cupd[kF];
   double Cn[kF];
@@ -1171,7 +1278,6 @@ __device__ bool update_vertex_fast(const DevMesh& M, const FieldBuf& F, const Fi
   bool touched = bupd;
 #pragma unroll
   for (int c = 0; c < kF; ++c) touched |= Cupd[c];
-  INSTR_CP(2, tA);
   // Apply the updates with set_value semantics into a sorted register column.
   bool changed = false;
   int El[kN];
@@ -1247,7 +1353,8 @@ __device__ bool update_vertex_fast(const DevMesh& M, const FieldBuf& F, const Fi
       if (j < n) ssum = ssum + Ex[j];
     if (ssum <= 0.0) {
       raise_error(W.ctl, kDevZeroColumn, v, spec);
-      return true;
+      h.flag = kHandled;
+      return h;
     }
     if (!(fabs(ssum - 1.0) < 1e-15)) {
       // One entry per lane (n <= kN == kG): divide, clamp, prune, then drop
@@ -1291,7 +1398,6 @@ __device__ bool update_vertex_fast(const DevMesh& M, const FieldBuf& F, const Fi
         }
     }
   }
-  INSTR_CP(3, tA);
   const bool old_one = cv > 0 && Ol[0] == 0 && Ox[0] == 1.0;
   const bool new_one = n > 0 && El[0] == 0 && Ex[0] == 1.0;
   const size_t o = static_cast<size_t>(v) * kSlots;
@@ -1301,8 +1407,9 @@ __device__ bool update_vertex_fast(const DevMesh& M, const FieldBuf& F, const Fi
       Fo.lay[o + j] = static_cast<unsigned short>(El[j]);
       Fo.val[o + j] = Ex[j];
     }
+  h.flag = kHandled;
   if (lane == 0) column_header<kN>(Fo, W, v, n, El, Ex, changed, old_one, new_one, h);
-  return true;
+  return h;
 }
 
 // Warp-aggregated slot reservation: one atomic per warp and round instead of
@@ -1369,7 +1476,7 @@ __device__ void bq_flush(BlockQueueT<T>& q, int* gcount, T* glist, int bar = 0, 
 }
 
 __device__ __forceinline__ void queue_region(const DevWork& W, int u, int stamp, int slot, BlockQueue& Q) {
-  if (atomicExch(W.stamp + u, stamp) != stamp) bq_push(Q, &W.ctl->rcount[slot], W.region[slot], u);
+  if (atomicExch(W.stamp + u, stamp) != stamp) bq_push(Q, &W.ctl->rcount[slot], pick4(W.region, slot), u);
 }
 
 // What phase B (commit) did before the field was double-buffered, now run by
@@ -1381,15 +1488,16 @@ __device__ __forceinline__ void queue_region(const DevWork& W, int u, int stamp,
 // the step's buffer by the update.  old_bi / old_inter describe v's column
 // before the step; rlen / ue are v's padded stiffness row (lane j: entry j-1).
 __device__ void post_update(const DevMesh& M, const DevWork& W, int v, int t, const Hdr& h0, uint4 old_bi,
-                            bool old_inter, int rlen, int ue, int lane, unsigned gm, BlockQueue& Q) {
-  const unsigned flag = __shfl_sync(gm, h0.flag, 0, kG);
+                            bool old_inter, int rlen, int ue, int lane, BlockQueue& Q) {
+  const unsigned flag = __shfl_sync(__activemask(), h0.flag, 0, kG);  // whole groups, see seg_any8
   if (!(flag & 0x80u)) return;  // the update raised an error: the step is void
   const int nslot = slot4(t + 1);
   if (flag & 1u) {
     // Claim the one-ring for frontier t+1 (lane 0: v itself, lane j: entry j-1).
     const int u0 = lane == 0 ? v : (lane <= rlen ? ue : -1);
     const bool first = u0 >= 0 && atomicExch(W.stamp + u0, t) != t;
-    if (first) bq_push(Q, &W.ctl->rcount[nslot], W.region[nslot], u0);
+    INSTR_AT(5, first);
+    if (first) bq_push(Q, &W.ctl->rcount[nslot], pick4(W.region, nslot), u0);
     for (int k = lane + kG; k <= rlen; k += kG)  // entries past the group: padded row, then the CSR
       queue_region(W, k - 1 < kEll ? __ldg(M.e_col + static_cast<size_t>(v) * kEll + k - 1)
                                    : __ldg(M.s_col + __ldg(M.s_off + v) + k - 1),
@@ -1426,32 +1534,41 @@ __device__ void post_update(const DevMesh& M, const DevWork& W, int v, int t, co
   }
   // A column that became interesting joins the list E(t) reads (the check
   // before this one carried over every column that already was).
-  if ((flag & 8u) && !old_inter) W.ilist[cp][atomicAdd(&W.ctl->ilcount[cp], 1)] = v;
+  if ((flag & 8u) && !old_inter) pick4(W.ilist, cp)[atomicAdd(&W.ctl->ilcount[cp], 1)] = v;
   const int delta = static_cast<int>((flag >> 2) & 1u) - static_cast<int>((flag >> 1) & 1u);
   if (delta) atomicAdd(&W.ctl->base_d[cp], delta);
 }
 
 // Update of frontier entry i of step t (reading the field after t-1, writing
-// the field after t) and its bookkeeping, by one 8-lane group.
+// the field after t) and its bookkeeping, by one 8-lane group (act false:
+// no item, no side effects).
 __device__ __forceinline__ void update_item(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P,
-                                            int t, int i, bool spec, BlockQueue& Q) {
+                                            int t, int i, bool act, bool spec, BlockQueue& Q) {
   const int lane = threadIdx.x & (kG - 1);
-  const unsigned gm = group_mask();
-  const int v = W.region[slot4(t)][i];
-  const FieldBuf& Fi = F.b[(t - 1) & 1];
-  const FieldBuf& Fo = F.b[t & 1];
+  INSTR_AT(0, i);
+  const int v = act ? pick4(W.region, slot4(t))[i] : 0;
+  INSTR_AT(1, v);
+  const FieldBuf Fi = pickf(F, t - 1);
+  const FieldBuf Fo = pickf(F, t);
   // Loads of the bookkeeping that depend only on v, issued with the update's.
   const uint4 old_bi = Fi.binfo[v];
   const bool old_inter = Fi.interest[v] != 0;
   const int rlen = __ldg(M.e_len + v);
   const int ue = lane >= 1 ? __ldg(M.e_col + static_cast<size_t>(v) * kEll + lane - 1) : v;
-  Hdr h;
-  h.flag = 0;
-  h.bi = make_uint4(0, 0, 0, 0);
-  if (!update_vertex_single(M, Fi, Fo, W, P, v, spec, lane, gm, h) &&
-      !update_vertex_fast(M, Fi, Fo, W, P, v, spec, lane, gm, h))
-    update_vertex(M, Fi, Fo, W, P, v, spec, lane, gm, h);
-  post_update(M, W, v, t, h, old_bi, old_inter, rlen, ue, lane, gm, Q);
+  Hdr h = update_vertex_single(M, Fi, Fo, W, P, v, act, spec, lane);
+  if (act && !(h.flag & kHandled)) {
+    h = update_vertex_fast(M, Fi, Fo, W, P, v, spec, lane, group_mask());
+    if (!(h.flag & kHandled)) h = update_vertex(M, Fi, Fo, W, P, v, spec, lane, group_mask());
+  }
+  INSTR_AT(4, h.flag);
+  post_update(M, W, v, t, h, old_bi, old_inter && act, rlen, ue, lane, Q);
+  INSTR_AT(6, v);
+}
+
+// Updates of step t for the items rank0, rank0 + stride, ... < n of this group.
+__device__ __forceinline__ void update_items(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P,
+                                             int t, int n, int rank0, int stride, bool spec, BlockQueue& Q) {
+  for (int i = rank0; i < n; i += stride) update_item(M, F, W, P, t, i, true, spec, Q);
 }
 
 __device__ __forceinline__ bool is_band(const DevWork& W, const StepParams& P, int l, double x) {
@@ -1591,7 +1708,7 @@ __device__ __forceinline__ int band_slot_of(const FieldBuf& F, const DevWork& W,
 
 __device__ void phase_union(const DevMesh& M, const FieldBuf& F, const DevWork& W, const StepParams& P, int lslot,
                             unsigned long long ep, int g0, int ng, int n) {
-  const int* list = W.ilist[lslot];
+  const int* list = pick4(W.ilist, lslot);
   const int lane = threadIdx.x & (kG - 1);
   const bool trace = W.prof && blockIdx.x == 0 && threadIdx.x == 0;
   unsigned long long* tr = trace ? W.prof + (W.prof_cap - 64LL * 3 * gridDim.x - 16) : nullptr;
@@ -1674,9 +1791,9 @@ __device__ void e_flush(BlockStats& S, const DevWork& W, int n_active, long long
   if (r == 0) {
     const unsigned long long m = block_bmax(S);
     if (m) atomicMax(&W.ctl->base_max_bits[cs], m);
-    if (blockIdx.x < W.bp_nseg) W.bpcount[set][blockIdx.x] = min(S.nbp, W.bp_seg);
+    if (blockIdx.x < W.bp_nseg) pick2(W.bpcount, set)[blockIdx.x] = min(S.nbp, W.bp_seg);
     if (blockIdx.x == 0)  // segments of CTAs beyond the grid
-      for (int c = gridDim.x; c < W.bp_nseg; ++c) W.bpcount[set][c] = 0;
+      for (int c = gridDim.x; c < W.bp_nseg; ++c) pick2(W.bpcount, set)[c] = 0;
   }
   for (int a = r; a < n_active && a < kSmemLayers; a += nthreads) {
     if (S.cnt[a][0]) atomicAdd(&g[a].ncomp, S.cnt[a][0]);
@@ -1693,6 +1810,13 @@ __device__ void e_flush(BlockStats& S, const DevWork& W, int n_active, long long
 // index) combine their contributions with 32-bit __reduce_*_sync, so each
 // warp issues one shared-memory atomic per layer (64-bit shared atomics are
 // CAS spin loops on this architecture).
+// Full-warp sum of fixed-point values (every lane converged).
+__device__ __forceinline__ long long warp_sum_fx(long long x) {
+  // |x| < 2^39: low 24 bits and the signed rest each sum exactly in 32 bits.
+  const unsigned lo = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(x & 0xFFFFFF));
+  const int hi = __reduce_add_sync(0xffffffffu, static_cast<int>(x >> 24));
+  return (static_cast<long long>(hi) << 24) + static_cast<long long>(lo);
+}
 __device__ __forceinline__ long long seg_sum_fx(unsigned peers, long long x) {
   // |x| < 2^39: low 24 bits and the signed rest each sum exactly in 32 bits.
   const unsigned lo = __reduce_add_sync(peers, static_cast<unsigned>(x & 0xFFFFFF));
@@ -1743,7 +1867,7 @@ __device__ void anchor_test(const DevMesh& M, const FieldBuf& F, const DevWork& 
 __device__ void phase_roots(const FieldBuf& F, const DevWork& W, const StepParams& P, int lslot, int sslot,
                             unsigned long long ep, int n) {
   LayerStat* g = W.stat + static_cast<size_t>(sslot) * kMaxActive;
-  const int* list = W.ilist[lslot];
+  const int* list = pick4(W.ilist, lslot);
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
     const int v = list[idx];
     if (!F.interest[v]) continue;
@@ -1775,7 +1899,7 @@ __device__ void phase_stats(const DevMesh& M, const FieldBuf& F, const DevWork& 
                             int nthreads) {
   const int lslot = slot4(step), nslot = slot4(step + 1), cs = slot4(step), set = static_cast<int>(step & 1);
   LayerStat* g = W.stat + static_cast<size_t>(cs) * kMaxActive;
-  const int* list = W.ilist[lslot];
+  const int* list = pick4(W.ilist, lslot);
   const int lane = threadIdx.x & 31;
   const int rank = static_cast<int>(threadIdx.x) - t0;
   const int trip = (n + gridDim.x * nthreads - 1) / (gridDim.x * nthreads);
@@ -1801,7 +1925,6 @@ __device__ void phase_stats(const DevMesh& M, const FieldBuf& F, const DevWork& 
     const double X4[4] = {x01.x, x01.y, x23.x, x23.y};
     const unsigned long long P4[4] = {p01.x, p01.y, p23.x, p23.y};
     const bool live = v >= 0 && inter_v;
-    if (live) INSTR_CP(8, tE);
     if (compact) {
       // Survivors go straight to the next band list, one atomic per warp
       // (the list's order does not matter), so no flush is left for the end
@@ -1812,7 +1935,7 @@ __device__ void phase_stats(const DevMesh& M, const FieldBuf& F, const DevWork& 
         int base = 0;
         if (lane == leader) base = atomicAdd(&W.ctl->ilcount[nslot], __popc(lm));
         base = __shfl_sync(0xffffffffu, base, leader);
-        if (live) W.ilist[nslot][base + __popc(lm & ((1u << lane) - 1u))] = v;
+        if (live) pick4(W.ilist, nslot)[base + __popc(lm & ((1u << lane) - 1u))] = v;
       }
     }
     const int cv = live ? cnt_v : 0;
@@ -1830,7 +1953,6 @@ __device__ void phase_stats(const DevMesh& M, const FieldBuf& F, const DevWork& 
       }
     }
     const long long px = live ? fxv : 0, py = live ? fyv : 0, pz = live ? fzv : 0;
-    if (live) INSTR_CP(9, tE);
     bool cand = false;
     int nkappa = 0;  // active layers at or above the collision threshold
     // The base owner (layer 0, always slot 0) contributes nothing below, so
@@ -1895,10 +2017,10 @@ __device__ void phase_stats(const DevMesh& M, const FieldBuf& F, const DevWork& 
           }
           if (band) {
             if (pos < seg) {
-              W.bandpairs[set][static_cast<size_t>(blockIdx.x) * W.bp_seg + pos] = make_int2(v, a);
+              pick2(W.bandpairs, set)[static_cast<size_t>(blockIdx.x) * W.bp_seg + pos] = make_int2(v, a);
             } else {
               const int o = obase + __popc(om & ((1u << lane) - 1u));
-              if (o < W.bandpair_cap) W.bp_ovf[set][o] = make_int2(v, a);
+              if (o < W.bandpair_cap) pick2(W.bp_ovf, set)[o] = make_int2(v, a);
               else {
                 W.ctl->bandpair_overflow = 1;  // the trail snap would miss items: a capacity error
                 raise_error(W.ctl, kDevCapacity, v, false);
@@ -1907,36 +2029,43 @@ __device__ void phase_stats(const DevMesh& M, const FieldBuf& F, const DevWork& 
           }
         }
       }
-      const unsigned peers = __match_any_sync(0xffffffffu, a);
-      const int nunsat = __reduce_add_sync(peers, unsat ? 1 : 0);
-      const int nband = __reduce_add_sync(peers, band ? 1 : 0);
-      const int nroot = __reduce_add_sync(peers, root ? 1 : 0);
-      const long long sx = seg_sum_fx(peers, band ? px : 0);
-      const long long sy = seg_sum_fx(peers, band ? py : 0);
-      const long long sz = seg_sum_fx(peers, band ? pz : 0);
-      if (a >= 0 && lane == __ffs(peers) - 1) {
-        if (a < kSmemLayers) {
-          if (nunsat) atomicAdd(&S.cnt[a][2], nunsat);
+      // One round per distinct layer of the warp (usually one), with
+      // full-warp votes and reductions: a partial-mask reduction costs ~10x
+      // a full-mask one on sm_100a (tools/fp64_lat.cu).
+      for (unsigned todo = __ballot_sync(0xffffffffu, a >= 0); todo;) {
+        const int ldr = __ffs(todo) - 1;
+        const int key = __shfl_sync(0xffffffffu, a, ldr);
+        const bool mine = a == key;
+        todo &= ~__ballot_sync(0xffffffffu, mine);
+        const int nunsat = __popc(__ballot_sync(0xffffffffu, mine && unsat));
+        const int nband = __popc(__ballot_sync(0xffffffffu, mine && band));
+        const int nroot = __popc(__ballot_sync(0xffffffffu, mine && root));
+        const bool mb = mine && band;
+        const long long sx = warp_sum_fx(mb ? px : 0);
+        const long long sy = warp_sum_fx(mb ? py : 0);
+        const long long sz = warp_sum_fx(mb ? pz : 0);
+        if (lane != ldr) continue;
+        if (key < kSmemLayers) {
+          if (nunsat) atomicAdd(&S.cnt[key][2], nunsat);
           if (nband) {
-            atomicAdd(&S.cnt[a][1], nband);
-            atomicAdd(reinterpret_cast<unsigned long long*>(&S.sum[a][0]), static_cast<unsigned long long>(sx));
-            atomicAdd(reinterpret_cast<unsigned long long*>(&S.sum[a][1]), static_cast<unsigned long long>(sy));
-            atomicAdd(reinterpret_cast<unsigned long long*>(&S.sum[a][2]), static_cast<unsigned long long>(sz));
+            atomicAdd(&S.cnt[key][1], nband);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&S.sum[key][0]), static_cast<unsigned long long>(sx));
+            atomicAdd(reinterpret_cast<unsigned long long*>(&S.sum[key][1]), static_cast<unsigned long long>(sy));
+            atomicAdd(reinterpret_cast<unsigned long long*>(&S.sum[key][2]), static_cast<unsigned long long>(sz));
           }
-          if (nroot) atomicAdd(&S.cnt[a][0], nroot);
+          if (nroot) atomicAdd(&S.cnt[key][0], nroot);
         } else {
-          if (nunsat) atomicAdd(&g[a].nunsat, nunsat);
+          if (nunsat) atomicAdd(&g[key].nunsat, nunsat);
           if (nband) {
-            atomicAdd(&g[a].nband, nband);
-            atomicAdd(reinterpret_cast<unsigned long long*>(&g[a].sx), static_cast<unsigned long long>(sx));
-            atomicAdd(reinterpret_cast<unsigned long long*>(&g[a].sy), static_cast<unsigned long long>(sy));
-            atomicAdd(reinterpret_cast<unsigned long long*>(&g[a].sz), static_cast<unsigned long long>(sz));
+            atomicAdd(&g[key].nband, nband);
+            atomicAdd(reinterpret_cast<unsigned long long*>(&g[key].sx), static_cast<unsigned long long>(sx));
+            atomicAdd(reinterpret_cast<unsigned long long*>(&g[key].sy), static_cast<unsigned long long>(sy));
+            atomicAdd(reinterpret_cast<unsigned long long*>(&g[key].sz), static_cast<unsigned long long>(sz));
           }
-          if (nroot) atomicAdd(&g[a].ncomp, nroot);
+          if (nroot) atomicAdd(&g[key].ncomp, nroot);
         }
       }
     }
-    if (live) INSTR_CP(10, tE);
     if (cand && nkappa >= 2 && !(base > P.coll_base_limit)) {  // a pair needs two such layers
       int first = -1;
       for (int k = 0; k < cv; ++k) {
@@ -1948,7 +2077,6 @@ __device__ void phase_stats(const DevMesh& M, const FieldBuf& F, const DevWork& 
       }
     }
     INSTR_REC(2, t0, live);
-    if (live) INSTR_CP(11, tE);
   }
 }
 
@@ -1981,9 +2109,14 @@ __device__ void snap_list(const DevMesh& M, LayerStat* g, const int2* items, int
       const double d2 = dx * dx + dy * dy + dz * dz;
       key = (static_cast<unsigned long long>(__double_as_longlong(d2)) & ~kVertMask) | static_cast<unsigned long long>(v);
     }
-    const unsigned peers = __match_any_sync(0xffffffffu, a);
-    const unsigned long long kmin = seg_min_u64(peers, key);
-    if (a >= 0 && lane == __ffs(peers) - 1) atomicMin(&g[a].snap, kmin);
+    for (unsigned todo = __ballot_sync(0xffffffffu, a >= 0); todo;) {  // full-warp rounds per layer
+      const int ldr = __ffs(todo) - 1;
+      const int k = __shfl_sync(0xffffffffu, a, ldr);
+      const bool mine = a == k;
+      todo &= ~__ballot_sync(0xffffffffu, mine);
+      const unsigned long long kmin = seg_min_u64(0xffffffffu, mine ? key : ~0ull);
+      if (lane == ldr) atomicMin(&g[k].snap, kmin);
+    }
   }
 }
 
@@ -1996,9 +2129,9 @@ __device__ void phase_snap(const DevMesh& M, const DevWork& W, long long step, i
   const int set = static_cast<int>(step & 1);
   const int rank = static_cast<int>(threadIdx.x) - t0;
   for (int c = blockIdx.x; c < W.bp_nseg; c += gridDim.x)
-    snap_list(M, g, W.bandpairs[set] + static_cast<size_t>(c) * W.bp_seg, min(W.bpcount[set][c], W.bp_seg), rank,
+    snap_list(M, g, pick2(W.bandpairs, set) + static_cast<size_t>(c) * W.bp_seg, min(pick2(W.bpcount, set)[c], W.bp_seg), rank,
               nthreads);
-  snap_list(M, g, W.bp_ovf[set], min(n_ovf, W.bandpair_cap), rank * static_cast<int>(gridDim.x) + blockIdx.x,
+  snap_list(M, g, pick2(W.bp_ovf, set), min(n_ovf, W.bandpair_cap), rank * static_cast<int>(gridDim.x) + blockIdx.x,
             static_cast<int>(gridDim.x) * nthreads);
 }
 
@@ -2078,8 +2211,8 @@ __device__ int decide(const DevWork& W, const StepParams& P, long long step) {
 // of `step` whose column is interesting after the step join the list of
 // step + 1 (what E's compaction does at a check).
 __device__ void carry_list(const FieldBuf& F, const DevWork& W, long long step, int n) {
-  const int* list = W.ilist[slot4(step)];
-  int* next = W.ilist[slot4(step + 1)];
+  const int* list = pick4(W.ilist, slot4(step));
+  int* next = pick4(W.ilist, slot4(step + 1));
   int* count = &W.ctl->ilcount[slot4(step + 1)];
   const int lane = threadIdx.x & 31;
   const int stride = gridDim.x * blockDim.x;
@@ -2151,7 +2284,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
     }
     grid_sync_snap(ctl, SC);
     ++ep;
-    const FieldBuf& Fc = F.b[s & 1];
+    const FieldBuf Fc = pickf(F, s);
     const int n = SC.ilcount[cs];
     phase_union(M, Fc, W, P, cs, ep, group_rank(1), gsz / kG, n);
     grid_sync(ctl);
@@ -2197,8 +2330,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       ctl->base_cum[slot4(b - 1)] = ctl->base_one;
       ctl->sum_region += static_cast<unsigned long long>(nR);
     }
-    for (int i = group_rank(2); i < nR; i += gsz / kG) update_item(M, F, W, P, b, i, false, Q);
-    bq_flush(Q, &ctl->rcount[slot4(b + 1)], W.region[slot4(b + 1)]);
+    update_items(M, F, W, P, static_cast<int>(b), nR, group_rank(2), gsz / kG, false, Q);
+    bq_flush(Q, &ctl->rcount[slot4(b + 1)], pick4(W.region, slot4(b + 1)));
     grid_sync_snap(ctl, SC);
     if (SC.error) stop = kStopError;
   }
@@ -2206,7 +2339,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
     const bool check = P.do_check && (s % P.check_interval == 0);
     const bool more = s + 1 < P.step_end;
     const int c0 = slot4(s);
-    const FieldBuf& Fs = F.b[s & 1];  // the field after step s
+    const FieldBuf Fs = pickf(F, s);  // the field after step s
     const int nR1 = more ? SC.rcount[slot4(s + 1)] : 0;  // frontier s+1, final since the last barrier
     const int nband = SC.ilcount[c0];
     const long long pslot = (s - P.step_begin) * 4;
@@ -2225,8 +2358,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       if (fl >= 0) flush_range(M, W, P, fl, t0, n);
       if (sn >= 0) phase_snap(M, W, sn, n_ovf, t0, n);
     };
-    auto run_a = [&](bool spec) {
-      for (int i = group_rank(2); i < nR1; i += gsz / kG) update_item(M, F, W, P, s + 1, i, spec, Q);
+    auto run_a = [&](bool spec) {  // by whole warps
+      update_items(M, F, W, P, static_cast<int>(s + 1), nR1, group_rank(2), gsz / kG, spec, Q);
     };
     const int q2 = slot4(s + 2);  // A(s+1) queues frontier s+2
     last_snapped = snap_step;
@@ -2235,7 +2368,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       if (more) run_a(false);
       carry_list(Fs, W, s, nband);
       side(0, nthr);
-      bq_flush(Q, &ctl->rcount[q2], W.region[q2]);
+      bq_flush(Q, &ctl->rcount[q2], pick4(W.region, q2));
       block_done(W, s - (P.step_end - 64), 1);
       grid_sync_snap(ctl, SC);
       if (prof) W.prof[pslot + 1] = W.prof[pslot + 2] = W.prof[pslot + 3] = gtimer();
@@ -2267,6 +2400,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
         const int m0 = e_warps, m1 = nwarps - a_warps;  // middle warps [m0, m1)
         if (warp < m0) {
           phase_stats(M, Fs, W, P, s, ep, true, S, nband, false, 0, m0 * 32);
+          INSTR_AT_W(8, 0);
           if (m1 == m0) {  // no middle warps: E's warps take the rest
             anchor_test(M, Fs, W, P, SC.nadded[c0], static_cast<int>(s),
                         static_cast<int>(threadIdx.x) * static_cast<int>(gridDim.x) + blockIdx.x,
@@ -2274,14 +2408,17 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
             side(0, m0 * 32);
           }
           e_flush(S, W, P.n_active, s, 1, 0, m0 * 32);
+          INSTR_AT_W(9, 0);
         } else if (warp >= m1) {
           if (more) run_a(true);
-          if (a_warps > 0) bq_flush(Q, &ctl->rcount[q2], W.region[q2], 2, m1 * 32, a_warps * 32);
+          if (a_warps > 0) bq_flush(Q, &ctl->rcount[q2], pick4(W.region, q2), 2, m1 * 32, a_warps * 32);
+          INSTR_AT_W(7, 0);
         } else {
           const int r = static_cast<int>(threadIdx.x) - m0 * 32, nm = (m1 - m0) * 32;
           anchor_test(M, Fs, W, P, SC.nadded[c0], static_cast<int>(s), r * static_cast<int>(gridDim.x) + blockIdx.x,
                       nm * static_cast<int>(gridDim.x));
           side(m0 * 32, nm);
+          INSTR_AT_W(10, 0);
         }
       } else {
         if (more) run_a(true);
@@ -2290,7 +2427,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
         side(0, nthr);
         if (P.do_hash) phase_hash(Fs, &ctl->hash_acc[c0], M.nv);
         e_flush(S, W, P.n_active, s, 0, 0, nthr);
-        bq_flush(Q, &ctl->rcount[q2], W.region[q2]);
+        bq_flush(Q, &ctl->rcount[q2], pick4(W.region, q2));
       }
       block_done(W, s - (P.step_end - 64), 1);
       grid_sync_snap(ctl, SC);
@@ -2311,7 +2448,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       phase_union(M, Fs, W, P, c0, ep, group_rank(1), gsz / kG, nband);
       side(0, nthr);
       if (P.do_hash) phase_hash(Fs, &ctl->hash_acc[c0], M.nv);
-      bq_flush(Q, &ctl->rcount[q2], W.region[q2]);
+      bq_flush(Q, &ctl->rcount[q2], pick4(W.region, q2));
       block_done(W, s - (P.step_end - 64), 0);
       grid_sync(ctl);
       if (prof) W.prof[pslot + 1] = gtimer();
@@ -2366,9 +2503,9 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
     // column step `last` changed, and every column a discarded A(last+1)
     // overwrote) copied from the field after `last`.
     {
-      const FieldBuf& A = F.b[last & 1];
-      const FieldBuf& B = F.b[(last + 1) & 1];
-      const int* list = W.region[slot4(last + 1)];
+      const FieldBuf A = pickf(F, last);
+      const FieldBuf B = pickf(F, last + 1);
+      const int* list = pick4(W.region, slot4(last + 1));
       const int n = SC.rcount[slot4(last + 1)];
       for (int i = gtid; i < n; i += gsz) {
         const int v = list[i];
@@ -2387,11 +2524,11 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       // Unclaim the frontier the discarded A(last+1) queued, then re-stamp
       // frontier last+1 (a vertex in both carried the newer stamp): the host
       // adds to frontier last+1 and the relaunch queues frontier last+2.
-      const int* list = W.region[slot4(last + 2)];
+      const int* list = pick4(W.region, slot4(last + 2));
       const int n = SC.rcount[slot4(last + 2)];
       for (int i = gtid; i < n; i += gsz) W.stamp[list[i]] = -1;
       grid_sync(ctl);
-      const int* cur = W.region[slot4(last + 1)];
+      const int* cur = pick4(W.region, slot4(last + 1));
       const int nc = SC.rcount[slot4(last + 1)];
       for (int i = gtid; i < nc; i += gsz) W.stamp[cur[i]] = static_cast<int>(last);
     }
