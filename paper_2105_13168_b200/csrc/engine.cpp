@@ -1330,6 +1330,7 @@ StepParams make_params(const DeviceField& field, const Config& cfg, const Coeffi
   p.extinct_limit = 1.0 - cfg.saturation;
   p.check_interval = cfg.check_interval;
   p.n_active = static_cast<int>(act.size());
+  p.n_layers = field.layer_count();
   p.record_trails = cfg.record_trails ? 1 : 0;
   p.do_hash = cfg.record_hashes ? 1 : 0;
   p.do_check = 1;

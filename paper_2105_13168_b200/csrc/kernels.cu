@@ -175,6 +175,11 @@ __device__ __forceinline__ void ctl_snap(const Ctl* ctl, CtlSnap& sc) {
   }
   __syncthreads();
 }
+// After the barrier that completes check `step`: the control snapshot and
+// the check's stop decision (decide(), same words) fetched in one round by
+// warp 0; the decision lands in sc.pad_[0].
+__device__ __forceinline__ void grid_sync_snap_decide(Ctl* ctl, CtlSnap& sc, const DevWork& W, const StepParams& P,
+                                                      long long step);
 __device__ __forceinline__ void grid_sync_snap(Ctl* ctl, CtlSnap& sc) {
   cooperative_groups::this_grid().sync();
   ctl_snap(ctl, sc);
@@ -290,6 +295,24 @@ __device__ __forceinline__ FieldBuf pickf(const DevField& F, long long t) {  // 
   return r;
 }
 
+// The active flags of the layers (fixed for the whole launch) as a bitmap in
+// shared memory: the update reads the activity of every layer it meets, and
+// from global memory that was one more dependent round trip per vertex.
+__shared__ unsigned s_act[(kMaxLayers + 1 + 31) / 32];
+__device__ __forceinline__ bool is_active(unsigned l) { return (s_act[l >> 5] >> (l & 31)) & 1u; }
+__device__ void load_active(const unsigned char* active, int n_layers) {
+  const int nw = (min(n_layers, kMaxLayers + 1) + 31) / 32;
+  for (int w = threadIdx.x; w < nw; w += blockDim.x) {
+    unsigned bits = 0;
+    for (int j = 0; j < 32; ++j) {
+      const int l = w * 32 + j;
+      if (l < n_layers && active[l]) bits |= 1u << j;
+    }
+    s_act[w] = bits;
+  }
+  for (int w = nw + threadIdx.x; w < (kMaxLayers + 1 + 31) / 32; w += blockDim.x) s_act[w] = 0;
+}
+
 // Dynamic shared memory: one slab per 8-lane group, used either for the fold
 // staging of the fast update or for the work arrays of the general update
 // (which would otherwise live in local memory, i.e. in L2).
@@ -402,7 +425,7 @@ __device__ Hdr update_vertex(const DevMesh& M, const FieldBuf& F, const FieldBuf
       const int l = F.lay[vb + j];
       ol[j] = static_cast<unsigned short>(l);
       ox[j] = F.val[vb + j];
-      act = l != 0 && W.active[l];
+      act = l != 0 && is_active(l);
     }
     own_act |= ((__ballot_sync(gm, act) >> (threadIdx.x & 24)) & 0xFFu) << jb;
   }
@@ -443,7 +466,7 @@ __device__ Hdr update_vertex(const DevMesh& M, const FieldBuf& F, const FieldBuf
         if (q < cu) {
           if (L[q] == 0) {
             bu = X[q];
-          } else if (W.active[L[q]]) {
+          } else if (is_active(L[q])) {
             au = au + X[q];
             amask |= 1u << q;
           }
@@ -452,7 +475,7 @@ __device__ Hdr update_vertex(const DevMesh& M, const FieldBuf& F, const FieldBuf
         const int l = F.lay[b + q];
         const double x = F.val[b + q];
         if (l == 0) bu = x;
-        else if (W.active[l]) au = au + x;
+        else if (is_active(l)) au = au + x;
       }
     }
     const int nvalid = min(kG, k1 - kb);
@@ -483,7 +506,7 @@ __device__ Hdr update_vertex(const DevMesh& M, const FieldBuf& F, const FieldBuf
           if (q < cu_) {
             l = F.lay[b + q];
             x = F.val[b + q];
-            act = l != 0 && W.active[l];
+            act = l != 0 && is_active(l);
           }
           const unsigned am = (__ballot_sync(gm, act) >> (threadIdx.x & 24)) & 0xFFu;
           const int m = min(kG, cu_ - qb);
@@ -706,7 +729,7 @@ __device__ __forceinline__ bool gather_fold(const DevMesh& M, const FieldBuf& F,
       if (q < cu) {
         if (L[q] == 0) {
           bu = X[q];
-        } else if (W.active[L[q]]) {
+        } else if (is_active(L[q])) {
           au = au + X[q];
           amask |= 1u << q;
         }
@@ -716,7 +739,7 @@ __device__ __forceinline__ bool gather_fold(const DevMesh& M, const FieldBuf& F,
   unsigned omask = 0;
 #pragma unroll
   for (int q = 0; q < kF; ++q)
-    if (q < cv && Ol[q] != 0 && W.active[Ol[q]]) omask |= 1u << q;
+    if (q < cv && Ol[q] != 0 && is_active(Ol[q])) omask |= 1u << q;
   // Candidate layers, ascending.
   nc = 0;
   unsigned last = 0;
@@ -850,7 +873,7 @@ __device__ Hdr update_vertex_single(const DevMesh& M, const FieldBuf& F, const F
   }
   // Activity of the non-base layers, looked up as soon as each is known
   // (not after the group agrees on L, which would add a dependent round).
-  const bool act_ok = (ol == 0 || W.active[ol]) && (nl == 0 || W.active[nl]);
+  const bool act_ok = (ol == 0 || is_active(ol)) && (nl == 0 || is_active(nl));
   // One common non-base layer L across v and its neighbours.
   const unsigned lo = seg_min8(min(nl ? nl : 0xFFFFFFFFu, ol ? ol : 0xFFFFFFFFu));
   const unsigned hi = seg_max8(max(nl, ol));
@@ -1129,7 +1152,7 @@ __device__ Hdr update_vertex_fast(const DevMesh& M, const FieldBuf& F, const Fie
         if (q < cu) {
           if (L[q] == 0) {
             bu = X[q];
-          } else if (W.active[L[q]]) {
+          } else if (is_active(L[q])) {
             au = au + X[q];
             amask |= 1u << q;
           }
@@ -1138,7 +1161,7 @@ __device__ Hdr update_vertex_fast(const DevMesh& M, const FieldBuf& F, const Fie
         const int l = F.lay[b + q];
         const double x = F.val[b + q];
         if (l == 0) bu = x;
-        else if (W.active[l]) au = au + x;
+        else if (is_active(l)) au = au + x;
       }
     }
     // Fold the group's neighbours in ascending column order (the reference's
@@ -1175,14 +1198,14 @@ __device__ Hdr update_vertex_fast(const DevMesh& M, const FieldBuf& F, const Fie
         const size_t b = static_cast<size_t>(u_) * kSlots;
         for (int q = kReg; q < cu_; ++q) {
           const int l_ = F.lay[b + q];
-          if (l_ != 0 && W.active[l_]) cand_add_reg(Cl, Ca, nc, over, l_, s_ * F.val[b + q]);
+          if (l_ != 0 && is_active(l_)) cand_add_reg(Cl, Ca, nc, over, l_, s_ * F.val[b + q]);
         }
       }
     }
   }
 #pragma unroll
   for (int q = 0; q < kF; ++q)  // own layers (missing diagonal; never on valid meshes)
-    if (q < cv && Ol[q] != 0 && W.active[Ol[q]]) {
+    if (q < cv && Ol[q] != 0 && is_active(Ol[q])) {
       bool found = false;
 #pragma unroll
       for (int c = 0; c < kF; ++c) found |= (c < nc && Cl[c] == Ol[q]);
@@ -1230,7 +1253,7 @@ __device__ Hdr update_vertex_fast(const DevMesh& M, const FieldBuf& F, const Fie
   unsigned amask_own = 0;
 #pragma unroll
   for (int q = 0; q < kF; ++q)
-    if (q < cv && Ol[q] != 0 && W.active[Ol[q]]) amask_own |= 1u << q;
+    if (q < cv && Ol[q] != 0 && is_active(Ol[q])) amask_own |= 1u << q;
   double cterm = 0.0;
   if (bnear && lane >= kF) {
 #pragma unroll
@@ -1572,7 +1595,7 @@ __device__ __forceinline__ void update_items(const DevMesh& M, const DevField& F
 }
 
 __device__ __forceinline__ bool is_band(const DevWork& W, const StepParams& P, int l, double x) {
-  return l != 0 && W.active[l] && x > P.band_lo && x < P.sat;
+  return l != 0 && is_active(l) && x > P.band_lo && x < P.sat;
 }
 
 __device__ __forceinline__ unsigned uf_find(unsigned long long* par, unsigned x, unsigned long long ep) {
@@ -1734,7 +1757,7 @@ __device__ void phase_union(const DevMesh& M, const FieldBuf& F, const DevWork& 
         if (!is_band(W, P, static_cast<int>(l), F.val[static_cast<size_t>(v) * kSlots + t])) continue;
         slot = t;
       }
-      if (!W.active[l]) continue;
+      if (!is_active(l)) continue;
       const unsigned item = static_cast<unsigned>(v) * kSlots + slot;
       if (trace) tr[2] = gtimer_raw();
       for (int c = c0 + lane; c < c1; c += kG) {
@@ -1753,7 +1776,6 @@ constexpr int kSmemLayers = 64;  // per-block aggregation slots for dense active
 struct BlockStats {
   int cnt[kSmemLayers][3];  // ncomp, nband, nunsat
   long long sum[kSmemLayers][3];
-  unsigned long long snap[kSmemLayers];
   unsigned long long bmax;               // max base value in (0, 1), as ordered bits
   unsigned long long wbmax[kBlock / 32];  // per-warp maxima (each warp's leader owns its slot: no atomics)
   int nbp;                                // band items appended to this CTA's segment
@@ -1763,7 +1785,6 @@ __device__ void block_stats_init(BlockStats& S) {
   for (int i = threadIdx.x; i < kSmemLayers; i += blockDim.x) {
     S.cnt[i][0] = S.cnt[i][1] = S.cnt[i][2] = 0;
     S.sum[i][0] = S.sum[i][1] = S.sum[i][2] = 0;
-    S.snap[i] = ~0ull;
   }
   if (threadIdx.x == 0) {
     S.bmax = 0;
@@ -1788,12 +1809,17 @@ __device__ void e_flush(BlockStats& S, const DevWork& W, int n_active, long long
   const int cs = slot4(step), set = static_cast<int>(step & 1);
   LayerStat* g = W.stat + static_cast<size_t>(cs) * kMaxActive;
   const int r = static_cast<int>(threadIdx.x) - t0;
+  // Each thread clears what it flushed, so S is ready for the next check
+  // (a grid barrier later) without a CTA barrier of its own.
   if (r == 0) {
     const unsigned long long m = block_bmax(S);
     if (m) atomicMax(&W.ctl->base_max_bits[cs], m);
     if (blockIdx.x < W.bp_nseg) pick2(W.bpcount, set)[blockIdx.x] = min(S.nbp, W.bp_seg);
     if (blockIdx.x == 0)  // segments of CTAs beyond the grid
       for (int c = gridDim.x; c < W.bp_nseg; ++c) pick2(W.bpcount, set)[c] = 0;
+    S.bmax = 0;
+    S.nbp = 0;
+    for (int w = 0; w < kBlock / 32; ++w) S.wbmax[w] = 0;
   }
   for (int a = r; a < n_active && a < kSmemLayers; a += nthreads) {
     if (S.cnt[a][0]) atomicAdd(&g[a].ncomp, S.cnt[a][0]);
@@ -1803,6 +1829,8 @@ __device__ void e_flush(BlockStats& S, const DevWork& W, int n_active, long long
       if (S.sum[a][c])
         atomicAdd(reinterpret_cast<unsigned long long*>(c == 0 ? &g[a].sx : (c == 1 ? &g[a].sy : &g[a].sz)),
                   static_cast<unsigned long long>(S.sum[a][c]));
+    S.cnt[a][0] = S.cnt[a][1] = S.cnt[a][2] = 0;
+    S.sum[a][0] = S.sum[a][1] = S.sum[a][2] = 0;
   }
 }
 
@@ -1848,7 +1876,7 @@ __device__ void anchor_test(const DevMesh& M, const FieldBuf& F, const DevWork& 
     const int2 a = W.added[static_cast<size_t>(cp) * W.added_cap + i];
     const int v = a.x;
     const unsigned l = static_cast<unsigned>(a.y);
-    if (!W.active[l]) continue;
+    if (!is_active(l)) continue;
     bool anchored = false;
     // u anchors v when it is a band item of l after the step and gained no
     // band item at the step.  add_stamp[u] may already carry the next step's
@@ -1876,7 +1904,7 @@ __device__ void phase_roots(const FieldBuf& F, const DevWork& W, const StepParam
     for (int k = 0; k < cv; ++k) {
       const int l = F.lay[b + k];
       const double x = F.val[b + k];
-      if (l == 0 || !W.active[l] || !(x > P.band_lo && x < P.sat)) continue;
+      if (l == 0 || !is_active(l) || !(x > P.band_lo && x < P.sat)) continue;
       const unsigned item = static_cast<unsigned>(v) * kSlots + k;
       const unsigned long long pw = W.parent[item];
       if ((pw >> 32) != ep || static_cast<unsigned>(pw) == item) atomicAdd(&g[W.aidx[l]].ncomp, 1);
@@ -1980,7 +2008,7 @@ __device__ void phase_stats(const DevMesh& M, const FieldBuf& F, const DevWork& 
           x = F.val[b + k];
           pw = W.parent[b + k];
         }
-        if (l != 0 && W.active[l]) {
+        if (l != 0 && is_active(l)) {
           a = W.aidx[l];
           unsat = x > 0.0 && x < 1.0;
           if (unsat && x >= P.kappa) cand = true;
@@ -2070,7 +2098,7 @@ __device__ void phase_stats(const DevMesh& M, const FieldBuf& F, const DevWork& 
       int first = -1;
       for (int k = 0; k < cv; ++k) {
         const int l = F.lay[b + k];
-        if (l == 0 || !W.active[l]) continue;
+        if (l == 0 || !is_active(l)) continue;
         if (F.val[b + k] < P.kappa) continue;
         if (first < 0) first = l;
         else insert_pair(W, (static_cast<unsigned>(first) << 16) | static_cast<unsigned>(l), ep, cs);
@@ -2230,6 +2258,38 @@ __device__ void carry_list(const FieldBuf& F, const DevWork& W, long long step, 
   }
 }
 
+__device__ __forceinline__ void grid_sync_snap_decide(Ctl* ctl, CtlSnap& sc, const DevWork& W, const StepParams& P,
+                                                      long long step) {
+  cooperative_groups::this_grid().sync();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const int cs = slot4(step);
+    const LayerStat* g = W.stat + static_cast<size_t>(cs) * kMaxActive;
+    int bits = 0;
+    if (lane == 0) {
+      const int4* src = reinterpret_cast<const int4*>(ctl);
+      int4* dst = reinterpret_cast<int4*>(&sc);
+#pragma unroll
+      for (int q = 0; q < 7; ++q) dst[q] = __ldcg(src + q);
+      if (__ldcg(&ctl->npairs[cs]) > 0 || __ldcg(&ctl->pair_overflow[cs])) bits |= kStopMerge;
+      const double bmax = __longlong_as_double(static_cast<long long>(__ldcg(&ctl->base_max_bits[cs])));
+      if (__ldcg(&ctl->base_cum[cs]) == 0 && bmax < P.extinct_limit) bits |= kStopExtinct;
+      if (__ldcg(&ctl->bandpair_overflow)) bits |= kStopError;
+    }
+    for (int a = lane; a < P.n_active; a += 32) {
+      const int4 c = __ldcg(reinterpret_cast<const int4*>(g + a));  // ncomp, nband, nunsat
+      if (c.x >= 2) bits |= kStopSplit;
+      if (c.y == 0 && c.z == 0) bits |= kStopVanish;
+    }
+    bits = static_cast<int>(__reduce_or_sync(kFull, static_cast<unsigned>(bits)));
+    if (lane == 0) {
+      sc.pad_[0] = bits;
+      INSTR_PHASE();
+    }
+  }
+  __syncthreads();
+}
+
 // Slot clears of the phase that starts step t (one thread; see slot4):
 // the frontier list A(t) read, the band list / change tracking / check
 // outputs of step t+2, the base delta of step t-1 (consumed), the digest of
@@ -2258,6 +2318,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
   __shared__ CtlSnap SC;
   Ctl* ctl = W.ctl;
   if (threadIdx.x == 0) Q.n = 0;
+  load_active(W.active, P.n_layers);
 #ifdef DTB_INSTR
   for (int i = threadIdx.x; i < 6 * 16; i += blockDim.x) s_hist[i / 16][i % 16] = 0;
   for (int i = threadIdx.x; i < 32; i += blockDim.x) s_cp[i / 2][i % 2] = 0;
@@ -2321,6 +2382,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
   long long snap_step = -1;    // check whose trail snap runs in the next phase
   long long flush_step = -1;   // check whose trail records are written in the next phase
   long long last_snapped = -1; // check snapped in the phase just ended
+  block_stats_init(S);  // e_flush clears it again after every check
   {  // prologue: A(step_begin), reading the field after step_begin - 1
     ctl_snap(ctl, SC);
     const long long b = P.step_begin;
@@ -2336,7 +2398,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
     if (SC.error) stop = kStopError;
   }
   for (; stop == 0 && s < P.step_end; ++s) {
-    const bool check = P.do_check && (s % P.check_interval == 0);
+    const bool check = P.do_check && (P.check_interval == 1 || s % P.check_interval == 0);
     const bool more = s + 1 < P.step_end;
     const int c0 = slot4(s);
     const FieldBuf Fs = pickf(F, s);  // the field after step s
@@ -2383,7 +2445,6 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
     }
     ++ep;
     const bool skip = !P.d_full && P.check_interval == 1 && !first_check && !SC.dchange[c0];
-    block_stats_init(S);
     if (skip) {
       // ---- certificate holds: one phase.  E on the first warps, A on the
       // last ones, the certificate and the trail work in between; each role
@@ -2430,7 +2491,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
         bq_flush(Q, &ctl->rcount[q2], pick4(W.region, q2));
       }
       block_done(W, s - (P.step_end - 64), 1);
-      grid_sync_snap(ctl, SC);
+      grid_sync_snap_decide(ctl, SC, W, P, s);
       if (prof) W.prof[pslot + 2] = gtimer();
       if (SC.anchor_fail[c0]) {  // an unanchored new band item: the union-find after all
         block_start(W, s - (P.step_end - 64), 2);
@@ -2439,6 +2500,9 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
         phase_roots(Fs, W, P, c0, c0, ep, nband);
         block_done(W, s - (P.step_end - 64), 2);
         grid_sync(ctl);
+        const int b2 = decide(W, P, s);  // the root counts changed
+        if (threadIdx.x == 0) SC.pad_[0] = b2;
+        __syncthreads();
       }
       if (prof) W.prof[pslot + 3] = gtimer();
     } else {
@@ -2456,7 +2520,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       phase_stats(M, Fs, W, P, s, ep, true, S, nband, true, 0, nthr);
       e_flush(S, W, P.n_active, s, 0, 0, nthr);
       block_done(W, s - (P.step_end - 64), 1);
-      grid_sync_snap(ctl, SC);
+      grid_sync_snap_decide(ctl, SC, W, P, s);
       if (prof) W.prof[pslot + 2] = W.prof[pslot + 3] = gtimer();
     }
     if (P.do_hash && gtid == 0) {
@@ -2464,7 +2528,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       if (slot >= 0 && slot < W.hash_cap) W.hashes[slot] = ctl->hash_acc[c0];
     }
     first_check = false;
-    int bits = decide(W, P, s);
+    int bits = SC.pad_[0];
     if (P.stop_every_check) bits |= kStopEveryCheck;
     if (bits) {
       stop = bits;

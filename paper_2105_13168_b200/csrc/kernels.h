@@ -227,6 +227,7 @@ struct StepParams {
   long long step_begin, step_end;  // execute steps [step_begin, step_end)
   int check_interval;
   int n_active;
+  int n_layers;  // layer ids in columns are below this (the active-flag table's length)
   int record_trails;
   int do_hash;
   int stop_every_check;
