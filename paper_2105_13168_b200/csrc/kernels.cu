@@ -411,7 +411,7 @@ __device__ Hdr update_vertex(const DevMesh& M, const FieldBuf& F, const FieldBuf
   unsigned short* const sl = nl + kWork;
   static_assert((kSlots + kCand + 2 * kWork) * (8 + 2) <= kSlabBytes, "the general update's arrays fit the slab");
   INSTR_C0(tU);
-  __syncwarp(gm);  // the slab may hold the fold staging of this group's previous vertex
+  __syncwarp(__activemask());  // the slab may hold the fold staging of this group's previous vertex
   const int cv = F.cnt[v];
   const size_t vb = static_cast<size_t>(v) * kSlots;
   // The column is staged lane-parallel (slot j on lane j % kG), and the
@@ -427,9 +427,9 @@ __device__ Hdr update_vertex(const DevMesh& M, const FieldBuf& F, const FieldBuf
       ox[j] = F.val[vb + j];
       act = l != 0 && is_active(l);
     }
-    own_act |= ((__ballot_sync(gm, act) >> (threadIdx.x & 24)) & 0xFFu) << jb;
+    own_act |= ((__ballot_sync(__activemask(), act) >> (threadIdx.x & 24)) & 0xFFu) << jb;
   }
-  __syncwarp(gm);
+  __syncwarp(__activemask());
   const double phib = (cv > 0 && ol[0] == 0) ? ox[0] : 0.0;
 
   int nc = 0;
@@ -480,23 +480,23 @@ __device__ Hdr update_vertex(const DevMesh& M, const FieldBuf& F, const FieldBuf
     }
     const int nvalid = min(kG, k1 - kb);
     for (int jj = 0; jj < nvalid; ++jj) {
-      const double s_ = __shfl_sync(gm, s, jj, kG);
-      const int cu_ = __shfl_sync(gm, cu, jj, kG);
-      const double bu_ = __shfl_sync(gm, bu, jj, kG);
-      const double au_ = __shfl_sync(gm, au, jj, kG);
-      const unsigned am_ = __shfl_sync(gm, amask, jj, kG);
+      const double s_ = __shfl_sync(__activemask(), s, jj, kG);
+      const int cu_ = __shfl_sync(__activemask(), cu, jj, kG);
+      const double bu_ = __shfl_sync(__activemask(), bu, jj, kG);
+      const double au_ = __shfl_sync(__activemask(), au, jj, kG);
+      const unsigned am_ = __shfl_sync(__activemask(), amask, jj, kG);
       lapb = lapb + s_ * bu_;
       lapt = lapt + s_ * au_;
       if (bu_ > 0.0) bnear = true;
 #pragma unroll
       for (int q = 0; q < kReg; ++q) {
-        const int l_ = __shfl_sync(gm, static_cast<int>(L[q]), jj, kG);
-        const double x_ = __shfl_sync(gm, X[q], jj, kG);
+        const int l_ = __shfl_sync(__activemask(), static_cast<int>(L[q]), jj, kG);
+        const double x_ = __shfl_sync(__activemask(), X[q], jj, kG);
         if (lane == 0 && ((am_ >> q) & 1)) cand_add(cl, ca, nc, overflow, l_, s_ * x_);
       }
       if (cu_ > kReg) {
         // Slots past kReg: loaded lane-parallel, added by lane 0 in slot order.
-        const int u_ = __shfl_sync(gm, u, jj, kG);
+        const int u_ = __shfl_sync(__activemask(), u, jj, kG);
         const size_t b = static_cast<size_t>(u_) * kSlots;
         for (int qb = kReg; qb < cu_; qb += kG) {
           const int q = qb + lane;
@@ -508,11 +508,11 @@ __device__ Hdr update_vertex(const DevMesh& M, const FieldBuf& F, const FieldBuf
             x = F.val[b + q];
             act = l != 0 && is_active(l);
           }
-          const unsigned am = (__ballot_sync(gm, act) >> (threadIdx.x & 24)) & 0xFFu;
+          const unsigned am = (__ballot_sync(__activemask(), act) >> (threadIdx.x & 24)) & 0xFFu;
           const int m = min(kG, cu_ - qb);
           for (int t = 0; t < m; ++t) {
-            const int l_ = __shfl_sync(gm, l, t, kG);
-            const double x_ = __shfl_sync(gm, x, t, kG);
+            const int l_ = __shfl_sync(__activemask(), l, t, kG);
+            const double x_ = __shfl_sync(__activemask(), x, t, kG);
             if (lane == 0 && ((am >> t) & 1)) cand_add(cl, ca, nc, overflow, l_, s_ * x_);
           }
         }
@@ -735,7 +735,7 @@ __device__ __forceinline__ bool gather_fold(const DevMesh& M, const FieldBuf& F,
         }
       }
   }
-  if (__any_sync(gm, cu > kReg)) return false;
+  if (seg_any8(cu > kReg)) return false;
   unsigned omask = 0;
 #pragma unroll
   for (int q = 0; q < kF; ++q)
@@ -752,7 +752,7 @@ __device__ __forceinline__ bool gather_fold(const DevMesh& M, const FieldBuf& F,
 #pragma unroll
     for (int q = 0; q < kF; ++q)
       if (((omask >> q) & 1) && static_cast<unsigned>(Ol[q]) > last) m = min(m, static_cast<unsigned>(Ol[q]));
-    m = __reduce_min_sync(gm, m);
+    m = seg_min8(m);
     if (m == 0xFFFFFFFFu) break;
     if (c == kF) return false;  // more than kF candidates
     Cl[c] = static_cast<int>(m);
@@ -775,13 +775,13 @@ __device__ __forceinline__ bool gather_fold(const DevMesh& M, const FieldBuf& F,
         present = true;
       }
     s_fold[lane * kFoldCols + c] = t;
-    pm[c] = (__ballot_sync(gm, present) >> gshift) & 0xFFu;
+    pm[c] = (__ballot_sync(__activemask(), present) >> gshift) & 0xFFu;
   }
   s_fold[lane * kFoldCols + kF] = s * bu;
   s_fold[lane * kFoldCols + kF + 1] = s * au;
-  const unsigned vm = (__ballot_sync(gm, valid) >> gshift) & 0xFFu;
-  bnear = bnear || ((__ballot_sync(gm, valid && bu > 0.0) >> gshift) & 0xFFu) != 0;
-  __syncwarp(gm);
+  const unsigned vm = (__ballot_sync(__activemask(), valid) >> gshift) & 0xFFu;
+  bnear = bnear || ((__ballot_sync(__activemask(), valid && bu > 0.0) >> gshift) & 0xFFu) != 0;
+  __syncwarp(__activemask());
   double acc = 0.0;
   if (lane < kFoldCols) {
     unsigned use = vm;
@@ -792,11 +792,11 @@ __device__ __forceinline__ bool gather_fold(const DevMesh& M, const FieldBuf& F,
     for (int jj = 0; jj < kG; ++jj)
       if ((use >> jj) & 1) acc = acc + s_fold[jj * kFoldCols + lane];
   }
-  __syncwarp(gm);  // s_fold is reused by the group's next vertex
+  __syncwarp(__activemask());  // s_fold is reused by the group's next vertex
 #pragma unroll
-  for (int c = 0; c < kF; ++c) Ca[c] = __shfl_sync(gm, acc, c, kG);
-  lapb = __shfl_sync(gm, acc, kF, kG);
-  lapt = __shfl_sync(gm, acc, kF + 1, kG);
+  for (int c = 0; c < kF; ++c) Ca[c] = __shfl_sync(__activemask(), acc, c, kG);
+  lapb = __shfl_sync(__activemask(), acc, kF, kG);
+  lapt = __shfl_sync(__activemask(), acc, kF + 1, kG);
   return true;
 }
 
@@ -1174,15 +1174,15 @@ __device__ Hdr update_vertex_fast(const DevMesh& M, const FieldBuf& F, const Fie
 #pragma unroll
     for (int jj = 0; jj < kG; ++jj) {
       if (jj >= nvalid) break;
-      const double s_ = __shfl_sync(gm, s, jj, kG);
-      const unsigned meta_ = __shfl_sync(gm, meta, jj, kG);
-      const double bu_ = __shfl_sync(gm, bu, jj, kG);
-      const double au_ = __shfl_sync(gm, au, jj, kG);
-      const unsigned l01_ = __shfl_sync(gm, l01, jj, kG);
-      const unsigned l23_ = __shfl_sync(gm, l23, jj, kG);
+      const double s_ = __shfl_sync(__activemask(), s, jj, kG);
+      const unsigned meta_ = __shfl_sync(__activemask(), meta, jj, kG);
+      const double bu_ = __shfl_sync(__activemask(), bu, jj, kG);
+      const double au_ = __shfl_sync(__activemask(), au, jj, kG);
+      const unsigned l01_ = __shfl_sync(__activemask(), l01, jj, kG);
+      const unsigned l23_ = __shfl_sync(__activemask(), l23, jj, kG);
       double x_[kReg];
 #pragma unroll
-      for (int q = 0; q < kReg; ++q) x_[q] = __shfl_sync(gm, X[q], jj, kG);
+      for (int q = 0; q < kReg; ++q) x_[q] = __shfl_sync(__activemask(), X[q], jj, kG);
       const int cu_ = static_cast<int>(meta_ & 0xFF);
       const unsigned am_ = meta_ >> 8;
       lapb = lapb + s_ * bu_;
@@ -1194,7 +1194,7 @@ __device__ Hdr update_vertex_fast(const DevMesh& M, const FieldBuf& F, const Fie
       for (int q = 0; q < kReg; ++q)
         if ((am_ >> q) & 1) cand_add_reg(Cl, Ca, nc, over, lq[q], s_ * x_[q]);
       if (cu_ > kReg) {
-        const int u_ = __shfl_sync(gm, u, jj, kG);
+        const int u_ = __shfl_sync(__activemask(), u, jj, kG);
         const size_t b = static_cast<size_t>(u_) * kSlots;
         for (int q = kReg; q < cu_; ++q) {
           const int l_ = F.lay[b + q];
@@ -1263,7 +1263,7 @@ __device__ Hdr update_vertex_fast(const DevMesh& M, const FieldBuf& F, const Fie
   double contact = 0.0;
 #pragma unroll
   for (int q = 0; q < kF; ++q) {
-    const double t = __shfl_sync(gm, cterm, kF + q, kG);
+    const double t = __shfl_sync(__activemask(), cterm, kF + q, kG);
     if ((amask_own >> q) & 1) contact = contact + t;
   }
   if (bnear && lane == kF) {
@@ -1284,7 +1284,7 @@ __device__ Hdr update_vertex_fast(const DevMesh& M, const FieldBuf& F, const Fie
       }
     }
   }
-  if (__any_sync(gm, my_blow)) {  // every path raises the same error for v
+  if (seg_any8(my_blow)) {  // every path raises the same error for v
     if (lane == 0) raise_error(W.ctl, kDevBlowup, v, spec);
     h.flag = kHandled;
     return h;
@@ -1293,11 +1293,11 @@ __device__ Hdr update_vertex_fast(const DevMesh& M, const FieldBuf& F, const Fie
   double Cn[kF];
 #pragma unroll
   for (int c = 0; c < kF; ++c) {
-    Cupd[c] = __shfl_sync(gm, my_upd, c, kG);
-    Cn[c] = __shfl_sync(gm, my_next, c, kG);
+    Cupd[c] = __shfl_sync(__activemask(), my_upd, c, kG);
+    Cn[c] = __shfl_sync(__activemask(), my_next, c, kG);
   }
-  const bool bupd = __shfl_sync(gm, my_upd, kF, kG);
-  const double bnext = __shfl_sync(gm, my_next, kF, kG);
+  const bool bupd = __shfl_sync(__activemask(), my_upd, kF, kG);
+  const double bnext = __shfl_sync(__activemask(), my_next, kF, kG);
   bool touched = bupd;
 #pragma unroll
   for (int c = 0; c < kF; ++c) touched |= Cupd[c];
@@ -1400,17 +1400,17 @@ __device__ Hdr update_vertex_fast(const DevMesh& M, const FieldBuf& F, const Fie
         ch = q != ex;
       }
       const int gshift = threadIdx.x & 24;
-      const unsigned keep = (__ballot_sync(gm, lane < n && q != 0.0) >> gshift) & 0xFFu;
-      changed = changed || ((__ballot_sync(gm, ch) >> gshift) & 0xFFu) != 0;
+      const unsigned keep = (__ballot_sync(__activemask(), lane < n && q != 0.0) >> gshift) & 0xFFu;
+      changed = changed || ((__ballot_sync(__activemask(), ch) >> gshift) & 0xFFu) != 0;
       // Lane t takes the t-th surviving entry.
       const int src = __fns(keep, 0, lane + 1);
       const int srcl = src < 0 ? 0 : src & (kG - 1);
-      const int nl = __shfl_sync(gm, el, srcl, kG);
-      const double nx = __shfl_sync(gm, q, srcl, kG);
+      const int nl = __shfl_sync(__activemask(), el, srcl, kG);
+      const double nx = __shfl_sync(__activemask(), q, srcl, kG);
 #pragma unroll
       for (int j = 0; j < kN; ++j) {
-        El[j] = __shfl_sync(gm, nl, j, kG);
-        Ex[j] = __shfl_sync(gm, nx, j, kG);
+        El[j] = __shfl_sync(__activemask(), nl, j, kG);
+        Ex[j] = __shfl_sync(__activemask(), nx, j, kG);
       }
       n = __popc(keep);
 #pragma unroll
