@@ -1565,14 +1565,13 @@ __device__ void post_update(const DevMesh& M, const DevWork& W, int v, int t, co
 // Update of frontier entry i of step t (reading the field after t-1, writing
 // the field after t) and its bookkeeping, by one 8-lane group (act false:
 // no item, no side effects).
-__device__ __forceinline__ void update_item(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P,
-                                            int t, int i, bool act, bool spec, BlockQueue& Q) {
+__device__ __forceinline__ void update_item(const DevMesh& M, const FieldBuf& Fi, const FieldBuf& Fo, const int* list,
+                                            const DevWork& W, const StepParams& P, int t, int i, bool act, bool spec,
+                                            BlockQueue& Q) {
   const int lane = threadIdx.x & (kG - 1);
   INSTR_AT(0, i);
-  const int v = act ? pick4(W.region, slot4(t))[i] : 0;
+  const int v = act ? list[i] : 0;
   INSTR_AT(1, v);
-  const FieldBuf Fi = pickf(F, t - 1);
-  const FieldBuf Fo = pickf(F, t);
   // Loads of the bookkeeping that depend only on v, issued with the update's.
   const uint4 old_bi = Fi.binfo[v];
   const bool old_inter = Fi.interest[v] != 0;
@@ -1591,7 +1590,9 @@ __device__ __forceinline__ void update_item(const DevMesh& M, const DevField& F,
 // Updates of step t for the items rank0, rank0 + stride, ... < n of this group.
 __device__ __forceinline__ void update_items(const DevMesh& M, const DevField& F, const DevWork& W, const StepParams& P,
                                              int t, int n, int rank0, int stride, bool spec, BlockQueue& Q) {
-  for (int i = rank0; i < n; i += stride) update_item(M, F, W, P, t, i, true, spec, Q);
+  const FieldBuf Fi = pickf(F, t - 1), Fo = pickf(F, t);  // the field after t-1 and after t
+  const int* list = pick4(W.region, slot4(t));
+  for (int i = rank0; i < n; i += stride) update_item(M, Fi, Fo, list, W, P, t, i, true, spec, Q);
 }
 
 __device__ __forceinline__ bool is_band(const DevWork& W, const StepParams& P, int l, double x) {
@@ -2290,6 +2291,14 @@ __device__ __forceinline__ void grid_sync_snap_decide(Ctl* ctl, CtlSnap& sc, con
   __syncthreads();
 }
 
+// ceil(n / gridDim.x) by a multiply-high with magic = ceil(2^32 / grid): exact
+// while (n + grid - 1) < 2^32 / grid (the error of the product stays below
+// 1 / grid); larger n divides.
+__device__ __forceinline__ int ceil_div_grid(int n, unsigned magic) {
+  const unsigned x = static_cast<unsigned>(n) + gridDim.x - 1;
+  return x < magic ? static_cast<int>(__umulhi(x, magic)) : static_cast<int>(x / gridDim.x);
+}
+
 // Slot clears of the phase that starts step t (one thread; see slot4):
 // the frontier list A(t) read, the band list / change tracking / check
 // outputs of step t+2, the base delta of step t-1 (consumed), the digest of
@@ -2327,6 +2336,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   const int gsz = gridDim.x * blockDim.x;
   const int nthr = static_cast<int>(blockDim.x);
+  const unsigned magicG = 0xFFFFFFFFu / gridDim.x + 1;  // ceil(2^32 / grid), see ceil_div_grid
   unsigned long long ep = static_cast<unsigned long long>(ctl->epoch);
 
   if (kMode == 1) {
@@ -2398,7 +2408,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
     if (SC.error) stop = kStopError;
   }
   for (; stop == 0 && s < P.step_end; ++s) {
-    const bool check = P.do_check && (P.check_interval == 1 || s % P.check_interval == 0);
+    const bool check = P.do_check && (P.check_interval == 1 || static_cast<int>(s) % P.check_interval == 0);
     const bool more = s + 1 < P.step_end;
     const int c0 = slot4(s);
     const FieldBuf Fs = pickf(F, s);  // the field after step s
@@ -2452,8 +2462,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       if (prof) W.prof[pslot + 1] = W.prof[pslot];
       block_start(W, s - (P.step_end - 64), 1);
       const int nwarps = nthr / 32;
-      const int e_per_cta = (nband + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x);
-      const int a_per_cta = (nR1 + static_cast<int>(gridDim.x) - 1) / static_cast<int>(gridDim.x);
+      const int e_per_cta = ceil_div_grid(nband, magicG);
+      const int a_per_cta = ceil_div_grid(nR1, magicG);
       const int e_warps = max(1, (e_per_cta + 31) / 32), a_warps = (a_per_cta + 3) / 4;
       const bool split = !P.do_hash && e_per_cta <= nthr && a_per_cta <= nthr / kG && e_warps + a_warps <= nwarps;
       if (split) {
