@@ -1514,27 +1514,22 @@ __device__ void post_update(const DevMesh& M, const DevWork& W, int v, int t, co
                             bool old_inter, int rlen, int ue, int lane, BlockQueue& Q) {
   const unsigned flag = __shfl_sync(__activemask(), h0.flag, 0, kG);  // whole groups, see seg_any8
   if (!(flag & 0x80u)) return;  // the update raised an error: the step is void
-  const int nslot = slot4(t + 1);
-  if (flag & 1u) {
-    // Claim the one-ring for frontier t+1 (lane 0: v itself, lane j: entry j-1).
-    const int u0 = lane == 0 ? v : (lane <= rlen ? ue : -1);
-    const bool first = u0 >= 0 && atomicExch(W.stamp + u0, t) != t;
-    INSTR_AT(5, first);
-    if (first) bq_push(Q, &W.ctl->rcount[nslot], pick4(W.region, nslot), u0);
-    for (int k = lane + kG; k <= rlen; k += kG)  // entries past the group: padded row, then the CSR
-      queue_region(W, k - 1 < kEll ? __ldg(M.e_col + static_cast<size_t>(v) * kEll + k - 1)
-                                   : __ldg(M.s_col + __ldg(M.s_off + v) + k - 1),
-                   t, nslot, Q);
-  }
-  if (lane != 0) return;
-  const int cp = slot4(t);
-  if (flag & 1u) {
-    // Band-item changes for the split certificate (see anchor_test): a lost
-    // band layer (or an overflowing band index) marks the step; gained layers
-    // are listed.  An unchanged column has the same band index.
+  const int nslot = slot4(t + 1), cp = slot4(t);
+  const bool changed = (flag & 1u) != 0;
+  // Lane 0's bookkeeping (band-item changes for the split certificate, see
+  // anchor_test: a lost band layer -- or an overflowing band index -- marks
+  // the step, gained layers are listed; a column that became interesting
+  // joins the band list E(t) reads; the base==1 count) issues its atomics in
+  // the same round as the one-ring claims below, so the two round trips
+  // overlap.  An unchanged column has the same band index.
+  unsigned gained[4] = {0, 0, 0, 0};
+  int ngain = 0;
+  bool lost = false;
+  const bool want_il = lane == 0 && (flag & 8u) && !old_inter;
+  if (lane == 0 && changed) {
     const uint4 bi = h0.bi;
     if (binfo_overflow(old_bi) || binfo_overflow(bi)) {
-      W.ctl->dchange[cp] = 1;
+      lost = true;
     } else {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -1545,21 +1540,50 @@ __device__ void post_update(const DevMesh& M, const DevWork& W, int v, int t, co
           lo_kept |= lo != 0 && binfo_layer(bi, r) == lo;
           ln_old |= ln != 0 && binfo_layer(old_bi, r) == ln;
         }
-        if (lo != 0 && !lo_kept) W.ctl->dchange[cp] = 1;
+        lost |= lo != 0 && !lo_kept;
         if (ln != 0 && !ln_old) {
-          W.add_stamp[v] = t;
-          const int pos = atomicAdd(&W.ctl->nadded[cp], 1);
-          if (pos < W.added_cap) W.added[static_cast<size_t>(cp) * W.added_cap + pos] = make_int2(v, static_cast<int>(ln));
-          else W.ctl->dchange[cp] = 1;
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            if (r == ngain) gained[r] = ln;
+          ++ngain;
         }
       }
     }
   }
-  // A column that became interesting joins the list E(t) reads (the check
-  // before this one carried over every column that already was).
-  if ((flag & 8u) && !old_inter) pick4(W.ilist, cp)[atomicAdd(&W.ctl->ilcount[cp], 1)] = v;
-  const int delta = static_cast<int>((flag >> 2) & 1u) - static_cast<int>((flag >> 1) & 1u);
-  if (delta) atomicAdd(&W.ctl->base_d[cp], delta);
+  int add_pos = 0, il_pos = 0;
+  if (ngain) add_pos = atomicAdd(&W.ctl->nadded[cp], ngain);
+  if (want_il) il_pos = atomicAdd(&W.ctl->ilcount[cp], 1);
+  bool first = false;
+  if (changed) {
+    // Claim the one-ring for frontier t+1 (lane 0: v itself, lane j: entry j-1).
+    const int u0 = lane == 0 ? v : (lane <= rlen ? ue : -1);
+    first = u0 >= 0 && atomicExch(W.stamp + u0, t) != t;
+  }
+  if (lane == 0) {
+    if (lost) W.ctl->dchange[cp] = 1;
+    if (ngain) {
+      W.add_stamp[v] = t;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (r < ngain) {
+          if (add_pos + r < W.added_cap)
+            W.added[static_cast<size_t>(cp) * W.added_cap + add_pos + r] = make_int2(v, static_cast<int>(gained[r]));
+          else
+            W.ctl->dchange[cp] = 1;
+        }
+    }
+    if (want_il) pick4(W.ilist, cp)[il_pos] = v;
+    const int delta = static_cast<int>((flag >> 2) & 1u) - static_cast<int>((flag >> 1) & 1u);
+    if (delta) atomicAdd(&W.ctl->base_d[cp], delta);
+  }
+  INSTR_AT(5, first);
+  if (changed) {
+    if (first) bq_push(Q, &W.ctl->rcount[nslot], pick4(W.region, nslot), lane == 0 ? v : ue);
+    for (int k = lane + kG; k <= rlen; k += kG)  // entries past the group: padded row, then the CSR
+      queue_region(W, k - 1 < kEll ? __ldg(M.e_col + static_cast<size_t>(v) * kEll + k - 1)
+                                   : __ldg(M.s_col + __ldg(M.s_off + v) + k - 1),
+                   t, nslot, Q);
+  }
 }
 
 // Update of frontier entry i of step t (reading the field after t-1, writing
