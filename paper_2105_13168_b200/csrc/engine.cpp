@@ -1007,18 +1007,20 @@ void DeviceField::init(const std::vector<Index>& seeds) {
   std::sort(sv.begin(), sv.end());
   sv.erase(std::unique(sv.begin(), sv.end()), sv.end());
   ai0.upload(sv.data(), sv.size(), s_);
+  // Union-find parents and pair keys carry the epoch of the check that wrote
+  // them: a reused workspace continues the epoch count of its earlier passes,
+  // so their tags are stale without clearing the arrays (a pooled workspace
+  // for a 5M-vertex mesh holds 1.3 GB of parents).
+  const long long epoch = read_ctl().epoch;
   ctl.zero(s_);
-  // Versioned union-find parents / pair keys restart at epoch 0, and a reused
-  // workspace may hold tags from an earlier pass: clear them.
-  parent.zero(s_);
-  pair_keys.zero(s_);
   stat.zero(s_);
   lastpos.zero(s_);
   // Step stamps of gained band items: -1 never matches a step.
-  cuda_check(cudaMemsetAsync(add_stamp.p, 0xFF, sizeof(int) * add_stamp.n, s_), "memset");
+  cuda_check(cudaMemsetAsync(add_stamp.p, 0xFF, sizeof(int) * static_cast<size_t>(nv), s_), "memset");
   ck(launch_init_field(view_, work_, static_cast<int>(nv), ai0.p, static_cast<int>(sv.size()), s_), "init field");
   Ctl c{};
   c.base_one = static_cast<int>(nv - sv.size());
+  c.epoch = epoch;
   ctl.upload(&c, 1, s_);
   sync_active();
   cuda_check(cudaStreamSynchronize(s_), "init");
