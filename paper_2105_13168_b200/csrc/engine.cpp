@@ -1614,6 +1614,7 @@ class PassEngine {
     StepParams p = make_params(*field_, cfg_, co_, dt_);
     p.stop_every_check = cfg_.on_check ? 1 : 0;
     if (const char* env = std::getenv("DTB_D_FULL"); env && env[0] == '1') p.d_full = 1;
+    if (const char* env = std::getenv("DTB_NO_WIDE"); env && env[0] == '1') p.no_wide = 1;
     return p;
   }
 

@@ -316,7 +316,7 @@ __device__ void load_active(const unsigned char* active, int n_layers) {
 // Dynamic shared memory: one slab per 8-lane group, used either for the fold
 // staging of the fast update or for the work arrays of the general update
 // (which would otherwise live in local memory, i.e. in L2).
-constexpr int kSlabBytes = 1600;
+constexpr int kSlabBytes = 2048;
 constexpr int kDynSmem = (kBlock / kG) * kSlabBytes;
 extern __shared__ double s_dyn[];
 __device__ __forceinline__ char* group_slab() {
@@ -544,6 +544,14 @@ __device__ Hdr update_vertex(const DevMesh& M, const FieldBuf& F, const FieldBuf
     raise_error(W.ctl, kDevCapacity, v, spec);
     return h;
   }
+#ifdef DTB_INSTR
+  atomicAdd(&s_hist[5][min(nc, 15)], 1u);  // candidate layers of general-path vertices
+  {
+    int nown = 0;
+    for (int j = 0; j < cv; ++j) nown += (own_act >> j) & 1;
+    atomicAdd(&s_hist[4][min(cv, 15)], 1u);  // column length
+  }
+#endif
 
   const double mass = __ldg(M.mass + v);
   const double lap_b = lapb / mass;
@@ -621,6 +629,312 @@ __device__ Hdr update_vertex(const DevMesh& M, const FieldBuf& F, const FieldBuf
     Fo.val[o + j] = nx[j];
   }
   column_header<0>(Fo, W, v, nn, nl, nx, changed, old_one, new_one, h);
+  return h;
+}
+
+// ---------------------------------------------------------------------------
+// Lane-parallel path for wide columns (many layers around v; a high-genus
+// gyroid puts 9-10 candidate layers on a third of its frontier): own column,
+// neighbour columns and candidate layers of at most kWide entries, a row of
+// at most kG entries.  The sequential general path's results, bit for bit:
+//  * every per-candidate neighbour sum adds s_j * x_j in row order (a +0.0
+//    for a neighbour without the layer is never added: the sum is the
+//    sequential path's, whose candidate order does not matter -- each layer
+//    is set once, and col_set of distinct layers commutes);
+//  * the candidate and base rates are the same expressions, one candidate
+//    per lane; the contact and total sums run in slot order on lane 0;
+//  * the new column is the merge of the own column with the updated and
+//    inserted layers (set_value: clamp above 1, prune below the epsilon);
+//  * normalisation sums in column order on lane 0 and divides per lane.
+// Not handled (flag 0, no side effects) when the case does not fit.
+constexpr int kWide = 16;
+struct WideSlab {  // one group's slab (kSlabBytes)
+  double ox[kWide];           // own column values
+  double nbx[kG][kWide];      // neighbour j's active non-base values (slot order); later the new column
+  double ca[kWide];           // per-candidate neighbour sums
+  double rn[kWide];           // per-candidate next values; contact terms
+  unsigned short ol[kWide];   // own column layers
+  unsigned short nbl[kG][kWide];
+  unsigned short cl[kWide];   // candidate layers, ascending
+  unsigned short nl2[2 * kWide + 8];  // new column layers
+  int nbn[kG];                // neighbour j's staged entries
+};
+static_assert(sizeof(WideSlab) <= kSlabBytes, "the wide path's arrays fit the slab");
+static_assert(sizeof(double) * (2 * kWide + 8) <= sizeof(double) * kG * kWide, "the new column fits the nbx area");
+
+__device__ Hdr update_vertex_wide(const DevMesh& M, const FieldBuf& F, const FieldBuf& Fo, const DevWork& W,
+                                  const StepParams& P, int v, bool spec, int lane) {
+  Hdr h;
+  h.flag = 0;
+  h.bi = make_uint4(0, 0, 0, 0);
+  WideSlab& S = *reinterpret_cast<WideSlab*>(group_slab());
+  const int cv = F.cnt[v];
+  const int k0 = __ldg(M.s_off + v), k1 = __ldg(M.s_off + v + 1);
+  const int rlen = k1 - k0;
+  if (cv > kWide || rlen > kG) return h;  // group-uniform
+  const bool valid = lane < rlen;
+  int u = 0, cu = 0;
+  double s = 0.0;
+  if (valid) {
+    u = __ldg(M.s_col + k0 + lane);
+    s = __ldg(M.s_val + k0 + lane);
+    cu = F.cnt[u];
+  }
+  if (seg_any8(cu > kWide)) return h;
+  __syncwarp(__activemask());  // the slab may hold this group's previous staging
+  // Own column, slot j on lane j % kG, with its activity bits.
+  unsigned own_act = 0;
+  const size_t vb = static_cast<size_t>(v) * kSlots;
+  for (int jb = 0; jb < cv; jb += kG) {
+    const int j = jb + lane;
+    bool act = false;
+    if (j < cv) {
+      const int l = F.lay[vb + j];
+      S.ol[j] = static_cast<unsigned short>(l);
+      S.ox[j] = F.val[vb + j];
+      act = l != 0 && is_active(l);
+    }
+    own_act |= ((__ballot_sync(__activemask(), act) >> (threadIdx.x & 24)) & 0xFFu) << jb;
+  }
+  // Neighbour j's column: base value bu, active sum au (slot order), and its
+  // active layers staged in slot (= ascending layer) order.
+  double bu = 0.0, au = 0.0;
+  int na = 0;
+  {
+    const size_t b = static_cast<size_t>(u) * kSlots;
+    const int cmax = static_cast<int>(seg_max8(static_cast<unsigned>(cu)));  // group-uniform trip count
+#pragma unroll 4
+    for (int q = 0; q < cmax; ++q) {
+      if (q < cu) {
+        const int l = F.lay[b + q];
+        const double x = F.val[b + q];
+        if (l == 0) {
+          bu = x;
+        } else if (is_active(l)) {
+          au = au + x;
+          S.nbl[lane][na] = static_cast<unsigned short>(l);
+          S.nbx[lane][na] = x;
+          ++na;
+        }
+      }
+    }
+  }
+  S.nbn[lane] = na;
+  const double phib = (cv > 0 && S.ol[0] == 0) ? S.ox[0] : 0.0;
+  // Ordered row folds of s_j * bu_j and s_j * au_j (the general path's lapb, lapt).
+  const double tb = s * bu, tt = s * au;
+  double lapb = 0.0, lapt = 0.0;
+  {
+    const unsigned am = __activemask();
+#pragma unroll
+    for (int jj = 0; jj < kG; ++jj) {
+      const double b_ = __shfl_sync(am, tb, jj, kG);
+      const double t_ = __shfl_sync(am, tt, jj, kG);
+      if (jj < rlen) {
+        lapb = lapb + b_;
+        lapt = lapt + t_;
+      }
+    }
+  }
+  const bool bnear = phib > 0.0 || seg_any8(valid && bu > 0.0);
+  __syncwarp(__activemask());
+  // Candidate layers: the ascending union of the own active layers (lane 0)
+  // and the neighbours' staged layers (lane j), one per merge round.
+  int nc = 0;
+  {
+    // Every lane walks the own column's cursor (the same on all lanes, so
+    // no lane diverges before the group reduction); lane 0 offers its head.
+    int pn = 0, po = 0;  // cursors: neighbour list, own column
+    for (;;) {
+      while (po < cv && !((own_act >> po) & 1)) ++po;
+      const unsigned oh = po < cv ? static_cast<unsigned>(S.ol[po]) : 0xFFFFFFFFu;
+      const unsigned nh = pn < na ? S.nbl[lane][pn] : 0xFFFFFFFFu;
+      const unsigned m = seg_min8(lane == 0 ? min(nh, oh) : nh);
+      if (m == 0xFFFFFFFFu) break;
+      if (nc == kWide) return h;  // too many candidates: not handled (no side effects yet)
+      if (lane == 0) S.cl[nc] = static_cast<unsigned short>(m);
+      ++nc;
+      if (pn < na && S.nbl[lane][pn] == m) ++pn;
+      if (po < cv && S.ol[po] == m) ++po;
+    }
+  }
+  __syncwarp(__activemask());
+  // Per-candidate neighbour sums in row order, candidates lane and lane + kG.
+  {
+    double acc0 = 0.0, acc1 = 0.0;
+    const unsigned l0 = lane < nc ? S.cl[lane] : 0xFFFFu, l1 = lane + kG < nc ? S.cl[lane + kG] : 0xFFFFu;
+    for (int jj = 0; jj < rlen; ++jj) {
+      // The mask is taken per round: groups with shorter rows leave the loop
+      // early, and a mask naming their lanes would wait for them forever.
+      const double s_ = __shfl_sync(__activemask(), s, jj, kG);
+      const int n_ = S.nbn[jj];
+      for (int q = 0; q < n_; ++q) {
+        const unsigned l = S.nbl[jj][q];
+        if (l == l0) acc0 = acc0 + s_ * S.nbx[jj][q];
+        if (l == l1) acc1 = acc1 + s_ * S.nbx[jj][q];
+      }
+    }
+    if (lane < nc) S.ca[lane] = acc0;
+    if (lane + kG < nc) S.ca[lane + kG] = acc1;
+  }
+  const double mass = __ldg(M.mass + v);
+  const double lap_b = lapb / mass;
+  // Candidate rates, one candidate per lane and round.
+  bool blow = false;
+  unsigned cupd = 0;  // bit c: candidate c's value moves
+  for (int cb = 0; cb < nc; cb += kG) {
+    const int c = cb + lane;
+    bool upd = false;
+    if (c < nc) {
+      const unsigned l = S.cl[c];
+      double phi = 0.0;
+      for (int j = 0; j < cv; ++j)
+        if (S.ol[j] == l) phi = S.ox[j];
+      if (!(phi == 0.0 && phib <= P.prune)) {
+        const double lap_i = S.ca[c] / mass;
+        const double inner = P.w * (phib - phi) + P.half_a2 * (lap_b - lap_i) - P.e * sqrt(max0(phi * phib));
+        const double rate = -P.mu_n * inner;
+        if (!isfinite(rate)) {
+          blow = true;
+        } else {
+          const double next = clamp01(phi + P.dt * rate);
+          if (next != phi) {
+            upd = true;
+            S.rn[c] = next;
+          }
+        }
+      }
+    }
+    cupd |= ((__ballot_sync(__activemask(), upd) >> (threadIdx.x & 24)) & 0xFFu) << cb;
+  }
+  if (seg_any8(blow)) {
+    if (lane == 0) raise_error(W.ctl, kDevBlowup, v, spec);
+    h.flag = kHandled;
+    return h;
+  }
+  __syncwarp(__activemask());
+  // Base rate: the contact terms per own slot on the lanes, the ordered sums
+  // and the rate on lane 0.
+  bool bupd = false;
+  double bnext = 0.0;
+  if (bnear) {
+    for (int j = lane; j < cv; j += kG)
+      if ((own_act >> j) & 1) S.nbx[0][j] = sqrt(max0(phib * S.ox[j]));
+    __syncwarp(__activemask());
+    if (lane == 0) {
+      double total = 0.0, contact = 0.0;
+      for (int j = 0; j < cv; ++j)
+        if ((own_act >> j) & 1) total = total + S.ox[j];
+      for (int j = 0; j < cv; ++j)
+        if ((own_act >> j) & 1) contact = contact + S.nbx[0][j];
+      const double lap_total = lapt / mass;
+      const double rate = -P.mu_n * (P.w * total + P.half_a2 * lap_total + P.e * contact) +
+                          P.m_mu_n * (P.w * phib + P.half_a2 * lap_b);
+      if (!isfinite(rate)) {
+        blow = true;
+      } else {
+        const double next = clamp01(phib + P.dt * rate);
+        if (next != phib) {
+          bupd = true;
+          bnext = next;
+        }
+      }
+    }
+    if (__shfl_sync(__activemask(), blow, 0, kG)) {
+      if (lane == 0) raise_error(W.ctl, kDevBlowup, v, spec);
+      h.flag = kHandled;
+      return h;
+    }
+    __syncwarp(__activemask());
+  }
+  h.flag = kHandled;
+  if (lane != 0) return h;  // lane 0 alone from here (the slab is its own)
+  // The new column: merge of the own column and the updated / inserted
+  // layers, set_value semantics (layer_field.hpp:102).
+  double* const nx2 = &S.nbx[0][0];
+  unsigned short* const nl2 = S.nl2;
+  bool changed = false;
+  const bool touched = cupd != 0 || bupd;
+  int nn = 0;
+  auto setv = [&](double val, double old, bool present) -> double {
+    if (val > 1.0) val = 1.0;
+    if (val < P.prune) val = 0.0;
+    if (present ? (val != old) : (val != 0.0)) changed = true;
+    return val;
+  };
+  int jo = 0, c = 0;
+  if (bupd && phib == 0.0) {  // the base enters the column (sorted first)
+    const double val = setv(bnext, 0.0, false);
+    if (val != 0.0) {
+      nl2[nn] = 0;
+      nx2[nn] = val;
+      ++nn;
+    }
+  }
+  while (jo < cv || c < nc) {
+    const unsigned lo = jo < cv ? S.ol[jo] : 0x10000u;
+    const unsigned lc = c < nc ? S.cl[c] : 0x10000u;
+    if (lo <= lc) {  // an own entry (possibly also a candidate)
+      double val = S.ox[jo];
+      if (lo == 0) {
+        if (bupd) val = setv(bnext, val, true);
+      } else if (lo == lc && ((cupd >> c) & 1)) {
+        val = setv(S.rn[c], val, true);
+      }
+      if (val != 0.0) {
+        nl2[nn] = static_cast<unsigned short>(lo);
+        nx2[nn] = val;
+        ++nn;
+      }
+      if (lo == lc) ++c;
+      ++jo;
+    } else {  // a candidate layer not in the column
+      if ((cupd >> c) & 1) {
+        const double val = setv(S.rn[c], 0.0, false);
+        if (val != 0.0) {
+          nl2[nn] = static_cast<unsigned short>(lc);
+          nx2[nn] = val;
+          ++nn;
+        }
+      }
+      ++c;
+    }
+  }
+  // Column normalisation of touched vertices (layer_field.hpp:143).
+  if (touched) {
+    double ssum = 0.0;
+    for (int j = 0; j < nn; ++j) ssum = ssum + nx2[j];
+    if (ssum <= 0.0) {
+      raise_error(W.ctl, kDevZeroColumn, v, spec);
+      return h;
+    }
+    if (!(fabs(ssum - 1.0) < 1e-15)) {
+      int m = 0;
+      for (int j = 0; j < nn; ++j) {
+        double q = nx2[j] / ssum;
+        if (q > 1.0) q = 1.0;
+        if (q < P.prune) q = 0.0;
+        if (q != nx2[j]) changed = true;
+        if (q != 0.0) {
+          nl2[m] = nl2[j];
+          nx2[m] = q;
+          ++m;
+        }
+      }
+      nn = m;
+    }
+  }
+  if (nn > kSlots) {
+    raise_error(W.ctl, kDevCapacity, v, spec);
+    return h;
+  }
+  const bool old_one = cv > 0 && S.ol[0] == 0 && S.ox[0] == 1.0;
+  const bool new_one = nn > 0 && nl2[0] == 0 && nx2[0] == 1.0;
+  for (int j = 0; j < nn; ++j) {
+    Fo.lay[vb + j] = nl2[j];
+    Fo.val[vb + j] = nx2[j];
+  }
+  column_header<0>(Fo, W, v, nn, nl2, nx2, changed, old_one, new_one, h);
   return h;
 }
 
@@ -1478,8 +1792,10 @@ __device__ __forceinline__ void bq_push(BlockQueueT<T>& q, int* gcount, T* glist
 // the whole CTA (bar 0 = __syncthreads) or the warps of one role behind a
 // named barrier, so the other roles of the phase never wait for it.  The next
 // use of the queue is after a grid barrier, so no trailing barrier is needed.
+// Non-aligned form: the threads of a warp may arrive at different times
+// (bar.sync is barrier.sync.aligned, which requires converged warps).
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 template <class T>
 __device__ void bq_flush(BlockQueueT<T>& q, int* gcount, T* glist, int bar = 0, int t0 = 0, int nthreads = 0) {
@@ -1602,9 +1918,17 @@ __device__ __forceinline__ void update_item(const DevMesh& M, const FieldBuf& Fi
   const int rlen = __ldg(M.e_len + v);
   const int ue = lane >= 1 ? __ldg(M.e_col + static_cast<size_t>(v) * kEll + lane - 1) : v;
   Hdr h = update_vertex_single(M, Fi, Fo, W, P, v, act, spec, lane);
+#ifdef DTB_INSTR
+  if (lane == 0) atomicAdd(&s_hist[3][(h.flag & kHandled) ? 0 : 1], 1u);  // single / not
+#endif
   if (act && !(h.flag & kHandled)) {
     h = update_vertex_fast(M, Fi, Fo, W, P, v, spec, lane, group_mask());
+#ifdef DTB_INSTR
+    if (lane == 0) atomicAdd(&s_hist[3][(h.flag & kHandled) ? 2 : 3], 1u);  // fast / general
+#endif
+    if (!(h.flag & kHandled) && !P.no_wide) h = update_vertex_wide(M, Fi, Fo, W, P, v, spec, lane);
     if (!(h.flag & kHandled)) h = update_vertex(M, Fi, Fo, W, P, v, spec, lane, group_mask());
+    __syncwarp(group_mask());  // the wide and general paths end on lane 0 alone: regroup
   }
   INSTR_AT(4, h.flag);
   post_update(M, W, v, t, h, old_bi, old_inter && act, rlen, ue, lane, Q);
@@ -2712,8 +3036,8 @@ void instr_report() {
 #ifdef DTB_INSTR
   unsigned long long h[6][16];
   cudaMemcpyFromSymbol(h, g_hist, sizeof(h));
-  static const char* names[6] = {"B commit", "D union", "E stats", "A fast", "A slow", "-"};
-  for (int p = 0; p < 5; ++p) {
+  static const char* names[6] = {"B commit", "D union", "E stats", "A paths(1,!1,fast,gen)", "gen cnt(v)", "gen ncand"};
+  for (int p = 0; p < 6; ++p) {
     unsigned long long n = 0;
     for (int b = 0; b < 16; ++b) n += h[p][b];
     std::fprintf(stderr, "[dtb] instr %-8s n=%10llu  buckets(128ns*2^b):", names[p], n);

@@ -233,6 +233,7 @@ struct StepParams {
   int stop_every_check;
   int do_check;  // 0: advance only (one-shot step())
   int d_full;    // diagnostics: never skip the front union-find (DTB_D_FULL=1)
+  int no_wide;   // diagnostics: no lane-parallel wide update (DTB_NO_WIDE=1)
 };
 
 // --- launchers (kernels.cu) -------------------------------------------------
