@@ -78,8 +78,8 @@ __device__ __forceinline__ void instr_rec(int ph, unsigned long long t0) {
   while (b < 15 && (128ull << b) < dt) ++b;
   atomicAdd(&s_hist[ph][b], 1u);
 }
-__device__ unsigned long long g_cp[16][2];
-__shared__ unsigned s_cp[16][2];  // 32-bit: native shared atomics (64-bit ones are CAS loops)
+__device__ unsigned long long g_cp[32][2];
+__shared__ unsigned s_cp[32][2];  // 32-bit: native shared atomics (64-bit ones are CAS loops)
 __device__ __forceinline__ void instr_cp(int idx, unsigned long long t0) {
   if ((threadIdx.x & 7) == 0) {
     atomicAdd(&s_cp[idx][0], static_cast<unsigned>((static_cast<unsigned long long>(clock64()) - t0) >> 4));
@@ -681,33 +681,47 @@ __device__ Hdr update_vertex_wide(const DevMesh& M, const FieldBuf& F, const Fie
     cu = F.cnt[u];
   }
   if (seg_any8(cu > kWide)) return h;
+  INSTR_AT(16, cu);
   __syncwarp(__activemask());  // the slab may hold this group's previous staging
   // Own column, slot j on lane j % kG, with its activity bits.
-  unsigned own_act = 0;
+  // Every load of the own column (slots lane, lane + kG) and of neighbour
+  // lane's column (its first kWide slots: in bounds, the column holds kSlots)
+  // is issued before any is used: one round trip for all of them.
   const size_t vb = static_cast<size_t>(v) * kSlots;
-  for (int jb = 0; jb < cv; jb += kG) {
-    const int j = jb + lane;
-    bool act = false;
-    if (j < cv) {
-      const int l = F.lay[vb + j];
-      S.ol[j] = static_cast<unsigned short>(l);
-      S.ox[j] = F.val[vb + j];
-      act = l != 0 && is_active(l);
+  const int ol0 = F.lay[vb + lane], ol1 = F.lay[vb + lane + kG];
+  const double ox0 = F.val[vb + lane], ox1 = F.val[vb + lane + kG];
+  const size_t b = static_cast<size_t>(u) * kSlots;
+  const uint4 lw0 = *reinterpret_cast<const uint4*>(F.lay + b), lw1 = *reinterpret_cast<const uint4*>(F.lay + b + 8);
+  double2 xw[kWide / 2];
+#pragma unroll
+  for (int k = 0; k < kWide / 2; ++k)
+    xw[k] = 2 * k < cu ? *reinterpret_cast<const double2*>(F.val + b + 2 * k) : make_double2(0.0, 0.0);
+  unsigned own_act = 0;
+  {
+    const bool a0 = lane < cv && ol0 != 0 && is_active(ol0);
+    const bool a1 = lane + kG < cv && ol1 != 0 && is_active(ol1);
+    if (lane < cv) {
+      S.ol[lane] = static_cast<unsigned short>(ol0);
+      S.ox[lane] = ox0;
     }
-    own_act |= ((__ballot_sync(__activemask(), act) >> (threadIdx.x & 24)) & 0xFFu) << jb;
+    if (lane + kG < cv) {
+      S.ol[lane + kG] = static_cast<unsigned short>(ol1);
+      S.ox[lane + kG] = ox1;
+    }
+    own_act = ((__ballot_sync(__activemask(), a0) >> (threadIdx.x & 24)) & 0xFFu) |
+              (((__ballot_sync(__activemask(), a1) >> (threadIdx.x & 24)) & 0xFFu) << kG);
   }
   // Neighbour j's column: base value bu, active sum au (slot order), and its
   // active layers staged in slot (= ascending layer) order.
   double bu = 0.0, au = 0.0;
   int na = 0;
   {
-    const size_t b = static_cast<size_t>(u) * kSlots;
-    const int cmax = static_cast<int>(seg_max8(static_cast<unsigned>(cu)));  // group-uniform trip count
-#pragma unroll 4
-    for (int q = 0; q < cmax; ++q) {
+    const unsigned lw[8] = {lw0.x, lw0.y, lw0.z, lw0.w, lw1.x, lw1.y, lw1.z, lw1.w};
+#pragma unroll
+    for (int q = 0; q < kWide; ++q) {
       if (q < cu) {
-        const int l = F.lay[b + q];
-        const double x = F.val[b + q];
+        const int l = static_cast<int>((lw[q / 2] >> (16 * (q & 1))) & 0xFFFFu);
+        const double x = (q & 1) ? xw[q / 2].y : xw[q / 2].x;
         if (l == 0) {
           bu = x;
         } else if (is_active(l)) {
@@ -720,6 +734,7 @@ __device__ Hdr update_vertex_wide(const DevMesh& M, const FieldBuf& F, const Fie
     }
   }
   S.nbn[lane] = na;
+  INSTR_AT(17, na);
   const double phib = (cv > 0 && S.ol[0] == 0) ? S.ox[0] : 0.0;
   // Ordered row folds of s_j * bu_j and s_j * au_j (the general path's lapb, lapt).
   const double tb = s * bu, tt = s * au;
@@ -759,6 +774,7 @@ __device__ Hdr update_vertex_wide(const DevMesh& M, const FieldBuf& F, const Fie
     }
   }
   __syncwarp(__activemask());
+  INSTR_AT(18, nc);
   // Per-candidate neighbour sums in row order, candidates lane and lane + kG.
   {
     double acc0 = 0.0, acc1 = 0.0;
@@ -777,6 +793,7 @@ __device__ Hdr update_vertex_wide(const DevMesh& M, const FieldBuf& F, const Fie
     if (lane < nc) S.ca[lane] = acc0;
     if (lane + kG < nc) S.ca[lane + kG] = acc1;
   }
+  INSTR_AT(19, 1u);
   const double mass = __ldg(M.mass + v);
   const double lap_b = lapb / mass;
   // Candidate rates, one candidate per lane and round.
@@ -847,6 +864,7 @@ __device__ Hdr update_vertex_wide(const DevMesh& M, const FieldBuf& F, const Fie
     }
     __syncwarp(__activemask());
   }
+  INSTR_AT(20, static_cast<unsigned>(bupd));
   h.flag = kHandled;
   if (lane != 0) return h;  // lane 0 alone from here (the slab is its own)
   // The new column: merge of the own column and the updated / inserted
@@ -900,6 +918,7 @@ __device__ Hdr update_vertex_wide(const DevMesh& M, const FieldBuf& F, const Fie
       ++c;
     }
   }
+  INSTR_AT(21, static_cast<unsigned>(nn));
   // Column normalisation of touched vertices (layer_field.hpp:143).
   if (touched) {
     double ssum = 0.0;
@@ -928,6 +947,7 @@ __device__ Hdr update_vertex_wide(const DevMesh& M, const FieldBuf& F, const Fie
     raise_error(W.ctl, kDevCapacity, v, spec);
     return h;
   }
+  INSTR_AT(22, static_cast<unsigned>(nn));
   const bool old_one = cv > 0 && S.ol[0] == 0 && S.ox[0] == 1.0;
   const bool new_one = nn > 0 && nl2[0] == 0 && nx2[0] == 1.0;
   for (int j = 0; j < nn; ++j) {
@@ -1193,7 +1213,10 @@ __device__ Hdr update_vertex_single(const DevMesh& M, const FieldBuf& F, const F
   const unsigned hi = seg_max8(max(nl, ol));
   const bool has_l = lo != 0xFFFFFFFFu;
   const bool fits = !seg_any8(bad || !act_ok) && !(has_l && lo != hi);
-  if (!fits) return h;  // this group falls back (group-uniform)
+  if (!fits) {  // this group falls back (group-uniform); hint: the widest neighbour column
+    h.bi.x = seg_max8(static_cast<unsigned>(cu));
+    return h;
+  }
   INSTR_AT(11, 1u);
   const unsigned L = has_l ? lo : 0u;
   // Ordered folds of s_j * bu_j and s_j * x_j(L) (au_j) over the row.
@@ -1391,6 +1414,7 @@ __device__ Hdr update_vertex_fast(const DevMesh& M, const FieldBuf& F, const Fie
   Hdr h;
   h.flag = 0;
   h.bi = make_uint4(0, 0, 0, 0);
+  INSTR_AT(24, v);
   INSTR_C0(tA);
   // Every load below is independent of the counts it is masked with, so the
   // column, stiffness row and neighbour columns arrive in three dependent
@@ -1746,6 +1770,7 @@ __device__ Hdr update_vertex_fast(const DevMesh& M, const FieldBuf& F, const Fie
     }
   h.flag = kHandled;
   if (lane == 0) column_header<kN>(Fo, W, v, n, El, Ex, changed, old_one, new_one, h);
+  INSTR_AT(25, n);
   return h;
 }
 
@@ -1922,7 +1947,9 @@ __device__ __forceinline__ void update_item(const DevMesh& M, const FieldBuf& Fi
   if (lane == 0) atomicAdd(&s_hist[3][(h.flag & kHandled) ? 0 : 1], 1u);  // single / not
 #endif
   if (act && !(h.flag & kHandled)) {
-    h = update_vertex_fast(M, Fi, Fo, W, P, v, spec, lane, group_mask());
+    // Neighbour columns longer than kReg mostly mean more than kF candidate
+    // layers, where the fast path would gather everything and then give up.
+    if (h.bi.x <= static_cast<unsigned>(kReg) || P.no_wide) h = update_vertex_fast(M, Fi, Fo, W, P, v, spec, lane, group_mask());
 #ifdef DTB_INSTR
     if (lane == 0) atomicAdd(&s_hist[3][(h.flag & kHandled) ? 2 : 3], 1u);  // fast / general
 #endif
@@ -2678,7 +2705,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
   load_active(W.active, P.n_layers);
 #ifdef DTB_INSTR
   for (int i = threadIdx.x; i < 6 * 16; i += blockDim.x) s_hist[i / 16][i % 16] = 0;
-  for (int i = threadIdx.x; i < 32; i += blockDim.x) s_cp[i / 2][i % 2] = 0;
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) s_cp[i / 2][i % 2] = 0;
 #endif
   __syncthreads();
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -2966,7 +2993,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
   __syncthreads();
   for (int i = threadIdx.x; i < 6 * 16; i += blockDim.x)
     if (s_hist[i / 16][i % 16]) atomicAdd(&g_hist[i / 16][i % 16], s_hist[i / 16][i % 16]);
-  for (int i = threadIdx.x; i < 32; i += blockDim.x)
+  for (int i = threadIdx.x; i < 64; i += blockDim.x)
     if (s_cp[i / 2][i % 2]) atomicAdd(&g_cp[i / 2][i % 2], static_cast<unsigned long long>(s_cp[i / 2][i % 2]));
 #endif
 }
@@ -3046,10 +3073,10 @@ void instr_report() {
   }
   std::memset(h, 0, sizeof(h));
   cudaMemcpyToSymbol(g_hist, h, sizeof(h));
-  unsigned long long c[16][2];
+  unsigned long long c[32][2];
   cudaMemcpyFromSymbol(c, g_cp, sizeof(c));
   std::fprintf(stderr, "[dtb] instr checkpoints (avg SM cycles since item start):");
-  for (int i = 0; i < 16; ++i)
+  for (int i = 0; i < 32; ++i)
     if (c[i][1]) std::fprintf(stderr, " cp%d=%.0f", i, 16.0 * static_cast<double>(c[i][0]) / c[i][1]);
   std::fprintf(stderr, "\n");
   std::memset(c, 0, sizeof(c));
