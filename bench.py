@@ -40,13 +40,13 @@ PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # Algorithmic bytes per unit of work of the persistent step kernel
 # (DESIGN.md "Roofline"): a frontier vertex reads its column (1 + 2 x 10 B),
 # its stiffness row (8 B offsets + 7 x 12 B), its mass (8 B) and its 7
-# neighbours' columns (7 x 21 B), writes a scratch column (21 B) that the
-# commit re-reads and scatters (2 x 21 B) -> 330 B.  A band vertex of the
+# neighbours' columns (7 x 21 B), and writes its new column (21 B) -> 288 B
+# (round 1 staged the column in scratch and committed it: 330 B).  A band vertex of the
 # check reads its column (21 B), its front-connectivity row (8 + 12 x 4 B),
 # the 6 higher-numbered neighbours' columns (6 x 21 B), union-find parents
 # (2 x 8 B) and its fixed-point position (24 B) -> 243 B; the band scan
 # reads one flag byte per mesh vertex.
-BYTES_PER_FRONTIER_VERTEX = 330
+BYTES_PER_FRONTIER_VERTEX = 288
 BYTES_PER_BAND_VERTEX = 243
 BYTES_PER_MESH_VERTEX_SCAN = 1
 
@@ -320,6 +320,9 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": measured_traffic(args), "traffic_unit": "DRAM bytes per launch (ncu)",
                      "peak_kind": peak_kind,
+                     "limiter": "latency: per step a chain of dependent L2 round trips (frontier list, columns, "
+                                "neighbour columns, one-ring claims) and FP64 update arithmetic, then one grid "
+                                "barrier; the working set stays in L2 (traffic vs alg_bytes_per_launch)",
                      "kernel": "k_engine<0> (persistent step kernel)",
                      "kernel_seconds": k_time, "kernel_launches": k_launches,
                      "alg_bytes_per_launch": alg_bytes / max(1, k_launches),

@@ -15,6 +15,7 @@ int main(int argc, char** argv) {
   difftopo::DiffusionConfig cfg;
   cfg.max_steps = argc > 2 ? std::atol(argv[2]) : 3000;
   try {
+    difftopo::init_work_queues(32);  // opt-in, before any CUDA use: 16 passes at once need 16+ hardware queues
     std::vector<difftopo::TriangleMesh> meshes;
     std::vector<difftopo::LaplacianOperator> ops;
     for (int i = 0; i < n; ++i) meshes.push_back(difftopo::TriangleMesh::generate("genus:" + std::to_string(1 + i % 32) + ":3"));

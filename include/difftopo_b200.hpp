@@ -365,6 +365,13 @@ inline InitialPassResult run_initial_pass(const TriangleMesh& mesh, const Laplac
   return r;
 }
 
+// Library initialisation, no reference counterpart (see difftopo_b200.h).
+// Opt-in hardware work queues for concurrent batch passes: call first thing,
+// before any CUDA use in the process.
+inline void init_work_queues(int queues = 32) { check(dtb_init_work_queues(queues)); }
+// Context creation and kernel loading outside a caller's timed region.
+inline void warmup() { check(dtb_warmup()); }
+
 // Independent passes over a batch of meshes, several at once on this GPU
 // (dtb_run_initial_pass_batch); item i equals
 // run_initial_pass_partial(*meshes[i], *ops[i], seeds[i], cfg, scheme).
