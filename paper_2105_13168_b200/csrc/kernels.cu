@@ -1237,108 +1237,63 @@ __device__ Hdr update_vertex_single(const DevMesh& M, const FieldBuf& F, const F
   const bool bnear = phib > 0.0 || seg_any8(bpos);
   h.flag = kHandled;
   if (!act) return h;
-  // ---- the sequential update (uniform across the group's lanes)
+  // ---- the sequential update (uniform across the group's lanes), written
+  // without branches so the two divisions and the square root issue
+  // together.  The candidate's lap_i and the base's lap_total are the same
+  // quotient lapt / mass.  When v holds L (ol == L, phi == ox) the
+  // candidate's contact term sqrt(phi * phib) equals the base's
+  // sqrt(phib * ox) (IEEE products commute); when it does not (ol == 0,
+  // ox == 0) both are +0.
   const double lap_b = lapb / mass;
-  bool touched = false, cupd = false, bupd = false;
-  double cn = 0.0, bnext = 0.0;
-  if (has_l) {
-    const double phi = ol == L ? ox : 0.0;
-    if (!(phi == 0.0 && phib <= P.prune)) {
-      const double lap_i = lapt / mass;
-      const double inner = P.w * (phib - phi) + P.half_a2 * (lap_b - lap_i) - P.e * sqrt(max0(phi * phib));
-      const double rate = -P.mu_n * inner;
-      if (!isfinite(rate)) {
-        if (lane == 0) raise_error(W.ctl, kDevBlowup, v, spec);
-        return h;
-      }
-      const double next = clamp01(phi + P.dt * rate);
-      if (next != phi) {
-        touched = true;
-        cupd = true;
-        cn = next;
-      }
-    }
-  }
-  INSTR_AT(12, static_cast<unsigned>(__double_as_longlong(lapt)) ^ static_cast<unsigned>(__double_as_longlong(lapb)));
-  if (bnear) {
-    double total = 0.0, contact = 0.0;
-    if (ol != 0) total = total + ox;  // ol == L, active
-    if (ol != 0) contact = contact + sqrt(max0(phib * ox));
-    const double lap_total = lapt / mass;
-    const double rate = -P.mu_n * (P.w * total + P.half_a2 * lap_total + P.e * contact) +
+  const double lap_t = lapt / mass;
+  const double sq = sqrt(max0(phib * ox));
+  const double phi = ol == L ? ox : 0.0;
+  const bool c_on = has_l && !(phi == 0.0 && phib <= P.prune);
+  const double rate_c = -P.mu_n * (P.w * (phib - phi) + P.half_a2 * (lap_b - lap_t) - P.e * sq);
+  const double total = ol != 0 ? ox : 0.0, contact = ol != 0 ? sq : 0.0;  // 0.0 + x == x (x >= 0)
+  const double rate_b = -P.mu_n * (P.w * total + P.half_a2 * lap_t + P.e * contact) +
                         P.m_mu_n * (P.w * phib + P.half_a2 * lap_b);
-    if (!isfinite(rate)) {
-      if (lane == 0) raise_error(W.ctl, kDevBlowup, v, spec);
-      return h;
-    }
-    const double next = clamp01(phib + P.dt * rate);
-    if (next != phib) {
-      touched = true;
-      bupd = true;
-      bnext = next;
-    }
+  if ((c_on && !isfinite(rate_c)) || (bnear && !isfinite(rate_b))) {
+    if (lane == 0) raise_error(W.ctl, kDevBlowup, v, spec);
+    return h;
   }
-  INSTR_AT(13, static_cast<unsigned>(__double_as_longlong(bnext)) ^ static_cast<unsigned>(__double_as_longlong(cn)));
-  // set_value into the (at most two-entry) column, sorted by layer.
+  const double next_c = clamp01(phi + P.dt * rate_c), next_b = clamp01(phib + P.dt * rate_b);
+  const bool cupd = c_on && next_c != phi, bupd = bnear && next_b != phib;
+  const bool touched = cupd || bupd;
+  INSTR_AT(13, static_cast<unsigned>(__double_as_longlong(next_b)) ^ static_cast<unsigned>(__double_as_longlong(next_c)));
+  // set_value (layer_field.hpp:102) on the base entry and the L entry
+  // (values are already at most 1; prune below the epsilon; a stored value
+  // that moves, an insertion or a removal is a change), then the column
+  // [base][, L] sorted by layer.
   bool changed = false;
+  const bool b_in = cv > 0 && o0 == 0, l_in = ol != 0;
+  double nb = phib, nlv = l_in ? ox : 0.0;
+  if (bupd) {
+    const double val = next_b < P.prune ? 0.0 : next_b;
+    changed |= b_in ? val != phib : val != 0.0;
+    nb = val;
+  }
+  if (cupd) {
+    const double val = next_c < P.prune ? 0.0 : next_c;
+    changed |= l_in ? val != ox : val != 0.0;
+    nlv = val;
+  }
   unsigned El[2] = {0, 0};
   double Ex[2] = {0.0, 0.0};
   int n = 0;
-  auto put = [&](unsigned l, double x) {
+  if (nb != 0.0) {
+    Ex[0] = nb;
+    n = 1;
+  }
+  if (nlv != 0.0) {
     if (n == 0) {
-      El[0] = l;
-      Ex[0] = x;
+      El[0] = L;
+      Ex[0] = nlv;
     } else {
-      El[1] = l;
-      Ex[1] = x;
+      El[1] = L;
+      Ex[1] = nlv;
     }
     ++n;
-  };
-  for (int q = 0; q < 2; ++q) {
-    if (q >= cv) break;
-    const unsigned lq = q == 0 ? o0 : o1;
-    const double xq = q == 0 ? own_x.x : own_x.y;
-    double val = xq;
-    bool upd = false;
-    if (lq == 0) {
-      if (bupd) {
-        val = bnext;
-        upd = true;
-      }
-    } else if (cupd) {  // lq == L
-      val = cn;
-      upd = true;
-    }
-    if (upd) {
-      if (val > 1.0) val = 1.0;
-      if (val < P.prune) val = 0.0;
-      if (val != xq) changed = true;
-    }
-    if (val != 0.0) put(lq, val);
-  }
-  if (bupd && phib == 0.0) {  // base enters the column (sorted first)
-    double val = bnext;
-    if (val > 1.0) val = 1.0;
-    if (val < P.prune) val = 0.0;
-    if (val != 0.0) {
-      if (n == 1) {
-        El[1] = El[0];
-        Ex[1] = Ex[0];
-      }
-      El[0] = 0;
-      Ex[0] = val;
-      ++n;
-      changed = true;
-    }
-  }
-  if (cupd && ol != L) {  // L enters the column (after the base)
-    double val = cn;
-    if (val > 1.0) val = 1.0;
-    if (val < P.prune) val = 0.0;
-    if (val != 0.0) {
-      put(L, val);
-      changed = true;
-    }
   }
   INSTR_AT(14, static_cast<unsigned>(__double_as_longlong(Ex[0])));
   // Column normalisation of touched vertices (layer_field.hpp:143), written
