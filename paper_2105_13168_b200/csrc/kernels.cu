@@ -1824,7 +1824,15 @@ __device__ void post_update(const DevMesh& M, const DevWork& W, int v, int t, co
   const bool want_il = lane == 0 && (flag & 8u) && !old_inter;
   if (lane == 0 && changed) {
     const uint4 bi = h0.bi;
-    if (binfo_overflow(old_bi) || binfo_overflow(bi)) {
+    if (old_bi.y == 0 && bi.y == 0 && (old_bi.x >> 16) == 0 && (bi.x >> 16) == 0) {
+      // At most one band layer before and after (a single front): compare the two.
+      const unsigned lo = old_bi.x, ln = bi.x;
+      lost = lo != 0 && lo != ln;
+      if (ln != 0 && ln != lo) {
+        gained[0] = ln;
+        ngain = 1;
+      }
+    } else if (binfo_overflow(old_bi) || binfo_overflow(bi)) {
       lost = true;
     } else {
 #pragma unroll
