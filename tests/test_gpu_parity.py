@@ -235,3 +235,18 @@ def test_gyroid_wide_columns_bit_exact(spec, steps, tmp_path):
     first_bad = next((i for i, (a, b) in enumerate(zip(mine, theirs)) if a != b), None)
     assert first_bad is None and len(mine) == len(theirs), first_bad
     parity.compare_events(res.events(), ref["events"])
+
+
+@pytest.mark.parametrize("spec,steps", [("genus:8:45", 3000), ("genus:4:45", 3000)])
+def test_bench_workload_final_state_bit_exact(spec, steps):
+    """The bench workload itself (configs[1], V = 988k; configs[3], V = 535k):
+    a full 3000-step pass ends in the reference's exact field (64-bit digest
+    of every stored value), with the same events and step count."""
+    mesh = dt.TriangleMesh.generate(spec)
+    op, _ = ref_operator(mesh, spec)
+    res = dt.run_initial_pass(mesh, op, 0, dt.default_config(max_steps=steps))
+    ref = refdata.ref_run(spec, max_steps=steps)
+    assert res.status == ("ok" if ref["status"] == "ok" else ref["error_type"])
+    assert res.steps == ref["steps"]
+    assert res.field_hash() == int(ref["final_hash"])
+    parity.compare_events(res.events(), ref["events"])
