@@ -347,6 +347,10 @@ void DeviceMesh::derive(const double* d_xyz, double maxabs, cudaStream_t s) {
   view_.c_col = c_col.p;
   view_.n_off = n_off.p;
   view_.n_col = n_col.p;
+  view_.f_off = f_off.p;
+  view_.f_col = f_col.p;
+  view_.face_edges = fe.p;
+  view_.edge_faces = ef.p;
 }
 
 std::shared_ptr<const Mesh> DeviceMesh::host_ptr() const {
@@ -949,6 +953,7 @@ void DeviceField::setup(size_t nv_cap, size_t ne_cap) {
   parent.alloc(nv * kSlots);
   added.alloc(4 * (nv / 8 + 4096));  // four step slots
   add_stamp.alloc(nv);
+  rem_stamp.alloc(nv);
   active.alloc(kMaxLayers + 1);
   aidx.alloc(kMaxLayers + 1);
   alist.alloc(kMaxActive);
@@ -982,6 +987,7 @@ void DeviceField::setup(size_t nv_cap, size_t ne_cap) {
   work_.added = added.p;
   work_.added_cap = static_cast<int>(added.n / 4);
   work_.add_stamp = add_stamp.p;
+  work_.rem_stamp = rem_stamp.p;
   work_.active = active.p;
   work_.aidx = aidx.p;
   work_.alist = alist.p;
@@ -1015,8 +1021,9 @@ void DeviceField::init(const std::vector<Index>& seeds) {
   ctl.zero(s_);
   stat.zero(s_);
   lastpos.zero(s_);
-  // Step stamps of gained band items: -1 never matches a step.
+  // Step stamps of gained / lost band items: -1 never matches a step.
   cuda_check(cudaMemsetAsync(add_stamp.p, 0xFF, sizeof(int) * static_cast<size_t>(nv), s_), "memset");
+  cuda_check(cudaMemsetAsync(rem_stamp.p, 0xFF, sizeof(int) * static_cast<size_t>(nv), s_), "memset");
   ck(launch_init_field(view_, work_, static_cast<int>(nv), ai0.p, static_cast<int>(sv.size()), s_), "init field");
   Ctl c{};
   c.base_one = static_cast<int>(nv - sv.size());
@@ -1614,6 +1621,7 @@ class PassEngine {
     StepParams p = make_params(*field_, cfg_, co_, dt_);
     p.stop_every_check = cfg_.on_check ? 1 : 0;
     if (const char* env = std::getenv("DTB_D_FULL"); env && env[0] == '1') p.d_full = 1;
+    if (const char* env = std::getenv("DTB_CERT_VERIFY"); env && env[0] == '1') p.cert_verify = 1;
     if (const char* env = std::getenv("DTB_NO_WIDE"); env && env[0] == '1') p.no_wide = 1;
     return p;
   }
@@ -1668,6 +1676,7 @@ class PassEngine {
         if (c.error == kDevZeroColumn)
           fail(kZeroColumn, "total field extinction at vertex " + std::to_string(c.error_vertex));
         if (c.bandpair_overflow) fail(kCapacityExceeded, "band item list overflow (trail snap)");
+        if (c.error == kDevCertificate) fail(kInconsistentLog, "split certificate held but the union-find split (DTB_CERT_VERIFY)");
         fail(kCapacityExceeded, "column capacity exceeded at vertex " + std::to_string(c.error_vertex));
       }
       if (c.stop_bits) {
@@ -1964,7 +1973,7 @@ class PassEngine {
   void report_phases() const {
     std::vector<unsigned long long> t = to_host(prof_, prof_.n, s_);
     double sum[3] = {0, 0, 0}, tot = 0;
-    long n = 0;
+    long n = 0, nd = 0, nx = 0;
     const size_t nstep_slots = 4 * static_cast<size_t>(std::min<long>(cfg_.max_steps, 100000));
     for (size_t i = 0; i + 4 < nstep_slots; i += 4) {
       if (!t[i] || !t[i + 3] || !t[i + 4]) continue;
@@ -1972,11 +1981,15 @@ class PassEngine {
       sum[1] += static_cast<double>(t[i + 2] - t[i + 1]);
       sum[2] += static_cast<double>(t[i + 3] - t[i + 2]);
       tot += static_cast<double>(t[i + 4] - t[i]);
+      nd += t[i + 1] > t[i];
+      nx += t[i + 3] > t[i + 2] + 1000;  // ns: the extra union-find phases, not the timer reads
       ++n;
     }
     if (n)
-      std::fprintf(stderr, "[dtb] phase us/step over %ld steps: D+A %.2f  E+A %.2f  extra %.2f  step %.2f (blocks %d)\n", n,
-                   sum[0] / n / 1e3, sum[1] / n / 1e3, sum[2] / n / 1e3, tot / n / 1e3, blocks_);
+      std::fprintf(stderr,
+                   "[dtb] phase us/step over %ld steps: D+A %.2f  E+A %.2f  extra %.2f  step %.2f (blocks %d; "
+                   "%ld steps with D+A, %ld with the extra union-find)\n",
+                   n, sum[0] / n / 1e3, sum[1] / n / 1e3, sum[2] / n / 1e3, tot / n / 1e3, blocks_, nd, nx);
     {
       const size_t tb = t.size() - 64 * 3 * static_cast<size_t>(blocks_) - 16;
       std::fprintf(stderr, "[dtb]   trace (last D item of CTA0/thread0, us from phase start): list+binfo %.2f  active %.2f  probe %.2f  unite %.2f\n",

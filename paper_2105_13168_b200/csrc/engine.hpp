@@ -287,6 +287,7 @@ class DeviceField {
   DevBuf<unsigned long long> parent, pair_keys, hashes;
   DevBuf<int2> added;   // band items gained this step (split certificate)
   DevBuf<int> add_stamp;  // per vertex: last step it gained a band item
+  DevBuf<int> rem_stamp;  // per vertex: last step it lost a band item
   DevBuf<unsigned> pairs;
   DevBuf<LayerStat> stat;
   DevBuf<TrailRec> trail;

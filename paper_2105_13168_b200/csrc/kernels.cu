@@ -1820,14 +1820,15 @@ __device__ void post_update(const DevMesh& M, const DevWork& W, int v, int t, co
   // overlap.  An unchanged column has the same band index.
   unsigned gained[4] = {0, 0, 0, 0};
   int ngain = 0;
-  bool lost = false;
+  bool lost = false;     // a lost band item the certificate does not test: the union-find runs
+  unsigned rem_l = 0;    // the band layer a single-front column lost (tested by the certificate)
   const bool want_il = lane == 0 && (flag & 8u) && !old_inter;
   if (lane == 0 && changed) {
     const uint4 bi = h0.bi;
     if (old_bi.y == 0 && bi.y == 0 && (old_bi.x >> 16) == 0 && (bi.x >> 16) == 0) {
       // At most one band layer before and after (a single front): compare the two.
       const unsigned lo = old_bi.x, ln = bi.x;
-      lost = lo != 0 && lo != ln;
+      if (lo != 0 && lo != ln) rem_l = lo;
       if (ln != 0 && ln != lo) {
         gained[0] = ln;
         ngain = 1;
@@ -1854,8 +1855,9 @@ __device__ void post_update(const DevMesh& M, const DevWork& W, int v, int t, co
       }
     }
   }
+  const int nitems = ngain + (rem_l != 0);
   int add_pos = 0, il_pos = 0;
-  if (ngain) add_pos = atomicAdd(&W.ctl->nadded[cp], ngain);
+  if (nitems) add_pos = atomicAdd(&W.ctl->nadded[cp], nitems);
   if (want_il) il_pos = atomicAdd(&W.ctl->ilcount[cp], 1);
   bool first = false;
   if (changed) {
@@ -1865,13 +1867,16 @@ __device__ void post_update(const DevMesh& M, const DevWork& W, int v, int t, co
   }
   if (lane == 0) {
     if (lost) W.ctl->dchange[cp] = 1;
-    if (ngain) {
-      W.add_stamp[v] = t;
+    if (nitems) {
+      if (ngain) W.add_stamp[v] = t;
+      if (rem_l) W.rem_stamp[v] = t;
+      int2* items = W.added + static_cast<size_t>(cp) * W.added_cap;
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
-        if (r < ngain) {
+      for (int r = 0; r < 5; ++r)
+        if (r < nitems) {
+          const int x = r < ngain ? static_cast<int>(gained[r & 3]) : static_cast<int>(rem_l) | kRemovedItem;
           if (add_pos + r < W.added_cap)
-            W.added[static_cast<size_t>(cp) * W.added_cap + add_pos + r] = make_int2(v, static_cast<int>(gained[r]));
+            items[add_pos + r] = make_int2(v, x);
           else
             W.ctl->dchange[cp] = 1;
         }
@@ -2203,29 +2208,115 @@ __device__ __forceinline__ unsigned long long seg_max_u64(unsigned peers, unsign
 
 // Split certificate (phase D is skipped when it holds).  With every check at
 // consecutive steps, the previous check left each layer's band connected (or
-// empty).  If this step removed no band item and every added item has a mesh
-// neighbour that was a band item of its layer before the step, each layer's
-// band is still connected or empty, so no split can occur and the union-find
-// is not needed.  This marks the added items that are not so anchored.
+// empty): its band triangles -- the faces with a band vertex, extract_front
+// (diffusion.hpp:398) -- form one edge-connected set T.  The step turns T
+// into T': faces whose band vertices were all lost leave, faces of gained
+// band vertices join.  T' is still connected (or empty) when
+//  * every gained item v has a mesh neighbour u that is a band item of its
+//    layer before and after the step: star(v) is edge-connected and shares
+//    the faces on edge uv with star(u), which lies in both T and T'; and
+//  * every lost item r passes the local test below.  Let Omega be star(r)
+//    plus the faces across its link edges.  If no other vertex of Omega
+//    lost a band item at the step, every maximal run of left faces on a
+//    path in T lies in star(r) and is entered and left through faces of
+//    Omega that stay in T'; so when the faces of Omega in T' are one
+//    edge-connected set (using only the edges between consecutive star
+//    faces and between a star face and the face across its link edge), a
+//    path in T between two faces of T' reroutes inside T'.
+// Then T and T' minus the left faces is connected in T', and every joined
+// face is edge-connected to it.  Items of inactive layers are not tested.
+// One 8-lane group per item; a failed item sets anchor_fail (the union-find
+// runs after all).  add_stamp / rem_stamp may already carry the next step's
+// stamp (its update runs beside this test): a stamp past `stamp` proves
+// nothing, so it never anchors and always counts as a loss (conservative).
+__device__ __forceinline__ int seg_sum8(int x) {
+  const unsigned am = __activemask();
+  x += __shfl_xor_sync(am, x, 4);
+  x += __shfl_xor_sync(am, x, 2);
+  return x + __shfl_xor_sync(am, x, 1);
+}
+__device__ bool lost_item_ok(const DevMesh& M, const FieldBuf& F, const DevWork& W, const StepParams& P, int r,
+                             unsigned l, int stamp, int lane) {
+  const int f0 = __ldg(M.f_off + r), d = __ldg(M.f_off + r + 1) - f0;
+  if (d > kG) return false;  // group-uniform
+  const bool valid = lane < d;
+  int a = -1, b = -1, w = -1;
+  if (valid) {
+    const int f = __ldg(M.f_col + f0 + lane);
+    const unsigned t0 = __ldg(M.faces + 3 * f), t1 = __ldg(M.faces + 3 * f + 1), t2 = __ldg(M.faces + 3 * f + 2);
+    const int kv = t0 == static_cast<unsigned>(r) ? 0 : (t1 == static_cast<unsigned>(r) ? 1 : 2);
+    a = static_cast<int>(kv == 0 ? t1 : (kv == 1 ? t2 : t0));  // corners kv+1, kv+2: the link edge
+    b = static_cast<int>(kv == 0 ? t2 : (kv == 1 ? t0 : t1));
+    const unsigned e = __ldg(M.face_edges + 3 * f + (kv + 1) % 3);
+    const unsigned g0 = __ldg(M.edge_faces + 2 * e), g1 = __ldg(M.edge_faces + 2 * e + 1);
+    const unsigned g = g0 == static_cast<unsigned>(f) ? g1 : g0;
+    if (g != static_cast<unsigned>(f) && g < static_cast<unsigned>(M.nf)) {  // not a boundary edge
+      const unsigned h0 = __ldg(M.faces + 3 * g), h1 = __ldg(M.faces + 3 * g + 1), h2 = __ldg(M.faces + 3 * g + 2);
+      w = static_cast<int>(h0 != static_cast<unsigned>(a) && h0 != static_cast<unsigned>(b)
+                               ? h0
+                               : (h1 != static_cast<unsigned>(a) && h1 != static_cast<unsigned>(b) ? h1 : h2));
+    }
+  }
+  bool bad = false, fp = false;
+  if (valid) {
+    const bool in_a = band_slot_of(F, W, P, a, l) >= 0, in_b = band_slot_of(F, W, P, b, l) >= 0;
+    const bool in_w = w >= 0 && band_slot_of(F, W, P, w, l) >= 0;
+    fp = in_a || in_b;
+    bad = (in_w && !fp) ||  // the face across the link edge would hang off a left face
+          W.rem_stamp[a] >= stamp || W.rem_stamp[b] >= stamp || (w >= 0 && W.rem_stamp[w] >= stamp);
+  }
+  // Present star faces sharing an edge r-x: counted once from each side.
+  int occ_a = 0, occ_b = 0, shared = 0;
+  {
+    const unsigned am = __activemask();  // whole groups
+#pragma unroll
+    for (int j = 0; j < kG; ++j) {
+      const int aj = __shfl_sync(am, a, j, kG), bj = __shfl_sync(am, b, j, kG);
+      const bool pj = __shfl_sync(am, fp, j, kG);
+      if (j != lane && j < d) {
+        const int ha = aj == a || bj == a, hb = aj == b || bj == b;
+        occ_a += ha;
+        occ_b += hb;
+        if (pj && fp) shared += ha + hb;
+      }
+    }
+  }
+  bad |= valid && (occ_a > 1 || occ_b > 1);  // not a manifold star: no claim
+  const int np = __popc((__ballot_sync(__activemask(), fp) >> (threadIdx.x & 24)) & 0xFFu);
+  const int ns = seg_sum8(shared);  // twice the shared edges
+  // The present star faces form np - ns/2 runs around r (a cycle or a fan).
+  return !seg_any8(bad) && 2 * np - ns <= 2;
+}
+
 __device__ void anchor_test(const DevMesh& M, const FieldBuf& F, const DevWork& W, const StepParams& P, int nadded,
-                            int stamp, int rank, int stride) {
+                            int stamp, int g0, int ng) {
   const int cp = slot4(stamp);
   const int n = min(nadded, W.added_cap);
-  for (int i = rank; i < n; i += stride) {
+  const int lane = threadIdx.x & (kG - 1);
+  for (int i = g0; i < n; i += ng) {  // group-uniform
     const int2 a = W.added[static_cast<size_t>(cp) * W.added_cap + i];
     const int v = a.x;
-    const unsigned l = static_cast<unsigned>(a.y);
+    const unsigned l = static_cast<unsigned>(a.y) & 0xFFFFu;
     if (!is_active(l)) continue;
-    bool anchored = false;
-    // u anchors v when it is a band item of l after the step and gained no
-    // band item at the step.  add_stamp[u] may already carry the next step's
-    // (its update runs beside this test): a stamp past `stamp` proves
-    // nothing, so it does not anchor (conservative, never a wrong skip).
-    for (int o = M.n_off[v]; o < M.n_off[v + 1] && !anchored; ++o) {
-      const int u = M.n_col[o];
-      anchored = W.add_stamp[u] < stamp && band_slot_of(F, W, P, u, l) >= 0;
+    bool ok;
+    if (a.y & kRemovedItem) {
+      ok = lost_item_ok(M, F, W, P, v, l, stamp, lane);
+    } else {
+      // u anchors v when it is a band item of l after the step and gained
+      // no band item at the step.
+      const int o0 = __ldg(M.n_off + v), o1 = __ldg(M.n_off + v + 1);
+      bool anchored = false;
+      for (int ob = o0; ob < o1; ob += kG) {  // group-uniform rounds
+        const int o = ob + lane;
+        if (o < o1) {
+          const int u = __ldg(M.n_col + o);
+          anchored |= W.add_stamp[u] < stamp && band_slot_of(F, W, P, u, l) >= 0;
+        }
+        if (seg_any8(anchored)) break;
+      }
+      ok = seg_any8(anchored);
     }
-    if (!anchored) W.ctl->anchor_fail[cp] = 1;
+    if (!ok && lane == 0) W.ctl->anchor_fail[cp] = 1;
   }
 }
 
@@ -2812,8 +2903,8 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
           INSTR_AT_W(8, 0);
           if (m1 == m0) {  // no middle warps: E's warps take the rest
             anchor_test(M, Fs, W, P, SC.nadded[c0], static_cast<int>(s),
-                        static_cast<int>(threadIdx.x) * static_cast<int>(gridDim.x) + blockIdx.x,
-                        m0 * 32 * static_cast<int>(gridDim.x));
+                        static_cast<int>(threadIdx.x) / kG * static_cast<int>(gridDim.x) + blockIdx.x,
+                        m0 * 32 / kG * static_cast<int>(gridDim.x));
             side(0, m0 * 32);
           }
           e_flush(S, W, P.n_active, s, 1, 0, m0 * 32);
@@ -2824,15 +2915,15 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
           INSTR_AT_W(7, 0);
         } else {
           const int r = static_cast<int>(threadIdx.x) - m0 * 32, nm = (m1 - m0) * 32;
-          anchor_test(M, Fs, W, P, SC.nadded[c0], static_cast<int>(s), r * static_cast<int>(gridDim.x) + blockIdx.x,
-                      nm * static_cast<int>(gridDim.x));
+          anchor_test(M, Fs, W, P, SC.nadded[c0], static_cast<int>(s),
+                      r / kG * static_cast<int>(gridDim.x) + blockIdx.x, nm / kG * static_cast<int>(gridDim.x));
           side(m0 * 32, nm);
           INSTR_AT_W(10, 0);
         }
       } else {
         if (more) run_a(true);
         phase_stats(M, Fs, W, P, s, ep, true, S, nband, false, 0, nthr);
-        anchor_test(M, Fs, W, P, SC.nadded[c0], static_cast<int>(s), gtid, gsz);
+        anchor_test(M, Fs, W, P, SC.nadded[c0], static_cast<int>(s), gtid / kG, gsz / kG);
         side(0, nthr);
         if (P.do_hash) phase_hash(Fs, &ctl->hash_acc[c0], M.nv);
         e_flush(S, W, P.n_active, s, 0, 0, nthr);
@@ -2841,14 +2932,19 @@ __global__ void __launch_bounds__(kBlock, 1) k_engine(DevMesh M, DevField F, Dev
       block_done(W, s - (P.step_end - 64), 1);
       grid_sync_snap_decide(ctl, SC, W, P, s);
       if (prof) W.prof[pslot + 2] = gtimer();
-      if (SC.anchor_fail[c0]) {  // an unanchored new band item: the union-find after all
+      if (SC.anchor_fail[c0] || P.cert_verify) {  // an item failed its test: the union-find after all
         block_start(W, s - (P.step_end - 64), 2);
         phase_union(M, Fs, W, P, c0, ep, group_rank(1), gsz / kG, nband);
         grid_sync(ctl);
         phase_roots(Fs, W, P, c0, c0, ep, nband);
         block_done(W, s - (P.step_end - 64), 2);
         grid_sync(ctl);
-        const int b2 = decide(W, P, s);  // the root counts changed
+        int b2 = decide(W, P, s);  // the root counts changed
+        if (P.cert_verify && !SC.anchor_fail[c0] && (b2 & kStopSplit)) {  // the certificate held wrongly
+          b2 |= kStopError;
+          if (gtid == 0) raise_error(ctl, kDevCertificate, -1, false);
+        }
+        __syncthreads();
         if (threadIdx.x == 0) SC.pad_[0] = b2;
         __syncthreads();
       }

@@ -75,6 +75,7 @@ constexpr int kPairCap = 1 << 16;  // collision pair hash table slots
 constexpr int kTrailCap = 1 << 20; // device trail ring capacity (records)
 constexpr int kBlock = 512;        // threads per CTA for all engine kernels
 constexpr int kEll = 8;            // padded stiffness row width (= 8-lane group)
+constexpr int kRemovedItem = 1 << 30;  // layer-word flag of a lost band item in DevWork::added
 
 // Error codes raised by device code (mirrored in mesh.hpp ErrorCode).
 enum DevError : int {
@@ -82,6 +83,7 @@ enum DevError : int {
   kDevBlowup = 10,    // NumericalBlowup (diffusion.hpp:315)
   kDevZeroColumn = 7, // ZeroColumn (layer_field.hpp:148)
   kDevCapacity = 101, // column or candidate capacity exceeded
+  kDevCertificate = 102,  // diagnostics (DTB_CERT_VERIFY=1): the split certificate held but the union-find split
 };
 
 // Stop reasons of the persistent step kernel.
@@ -111,6 +113,8 @@ struct DevMesh {
   const double* e_val = nullptr;
   const int *c_off = nullptr, *c_col = nullptr;                   // front connectivity
   const int *n_off = nullptr, *n_col = nullptr;                   // mesh neighbours
+  const int *f_off = nullptr, *f_col = nullptr;                   // incident faces (v2f CSR)
+  const unsigned *face_edges = nullptr, *edge_faces = nullptr;    // 3F (edge k joins corners k, k+1), 2E
 };
 
 // Per-step rotating slots.  The step loop runs E(s) (the check of step s)
@@ -200,9 +204,12 @@ struct DevWork {
   int2 *bp_ovf[2] = {nullptr, nullptr};
   int bandpair_cap = 0;                 // capacity of each bp_ovf
   unsigned long long *parent = nullptr; // nv * kSlots versioned UF parents
-  int2 *added = nullptr;                // 4 x added_cap band items (vertex, layer) gained, by slot4(step)
+  // 4 x added_cap band items (vertex, layer) gained -- or, with kRemovedItem
+  // in the layer word, lost -- by slot4(step) (the split certificate's items)
+  int2 *added = nullptr;
   int added_cap = 0;
   int *add_stamp = nullptr;             // per vertex: last step at which it gained a band item
+  int *rem_stamp = nullptr;             // per vertex: last step at which it lost a band item
   unsigned char *active = nullptr;      // kMaxLayers + 1
   int *aidx = nullptr;                  // layer -> dense active index or -1
   int *alist = nullptr;                 // dense active index -> layer
@@ -234,6 +241,7 @@ struct StepParams {
   int do_check;  // 0: advance only (one-shot step())
   int d_full;    // diagnostics: never skip the front union-find (DTB_D_FULL=1)
   int no_wide;   // diagnostics: no lane-parallel wide update (DTB_NO_WIDE=1)
+  int cert_verify;  // diagnostics: run the union-find after a held certificate too, error if it splits
 };
 
 // --- launchers (kernels.cu) -------------------------------------------------
