@@ -250,3 +250,23 @@ def test_bench_workload_final_state_bit_exact(spec, steps):
     assert res.steps == ref["steps"]
     assert res.field_hash() == int(ref["final_hash"])
     parity.compare_events(res.events(), ref["events"])
+
+
+@pytest.mark.parametrize("spec,steps", [("genus:8:45", 3000), ("gyroid:2:26:0.3:1.0", 1500),
+                                        ("torus:96:32:3:1.0", 2000), ("limbstar:2:3:3", 2000),
+                                        ("plate:2:20:0.5", 2000)])
+def test_split_certificate_never_hides_a_split(spec, steps, monkeypatch):
+    """DTB_CERT_VERIFY=1 runs the union-find after every check whose split
+    certificate held (gained items anchored, lost items' stars connected)
+    and fails the pass if it finds two components there; the pass must
+    finish as the plain one does, in the same field state."""
+    mesh = dt.TriangleMesh.generate(spec)
+    op = dt.assemble_laplacian(mesh)
+    cfg = dt.default_config(max_steps=steps)
+    plain = dt.run_initial_pass(mesh, op, 0, cfg)
+    monkeypatch.setenv("DTB_CERT_VERIFY", "1")
+    checked = dt.run_initial_pass(mesh, op, 0, cfg)
+    assert checked.status == plain.status and checked.steps == plain.steps
+    assert checked.field_hash() == plain.field_hash()
+    assert [(e.kind, e.step, e.layers) for e in checked.events()] == [(e.kind, e.step, e.layers)
+                                                                       for e in plain.events()]
