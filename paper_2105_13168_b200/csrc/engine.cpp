@@ -967,6 +967,10 @@ void DeviceField::setup(size_t nv_cap, size_t ne_cap) {
   while (tcap < 8 * nv && tcap < static_cast<size_t>(kTrailCap)) tcap <<= 1;
   trail.alloc(tcap);
   ctl.alloc(1);
+  // The device seed Dijkstra's distances: all "far" between calls (the
+  // kernel resets what it touched), so a pass neither allocates nor clears them.
+  seed_dist.alloc(nv);
+  cuda_check(cudaMemsetAsync(seed_dist.p, 0x7F, sizeof(unsigned long long) * nv, s_), "memset");
   parent.zero(s_);
   pair_keys.zero(s_);
   stat.zero(s_);
@@ -1506,14 +1510,15 @@ class PassEngine {
     res_.seed_vertex = seed;
     const double radius =
         cfg_.seed_radius > 0 ? cfg_.seed_radius : 1.5 * (co_.gradient_energy / std::sqrt(co_.penalty));
-    // A device-built mesh runs the Dijkstra on the device rather than
-    // downloading its host copy; capacity overflow falls back to the host.
+    // The Dijkstra runs on the device (a device-built mesh has no host copy
+    // to download); capacity overflow falls back to the host.
     std::vector<Index> seeds;
     bool seeded = false;
-    if (!dm_->has_host()) {
+    {
       std::vector<unsigned> buf(8192);
       int n = 0;
-      ck(launch_seed_region(dm_->view(), seed, radius, buf.data(), static_cast<int>(buf.size()), &n, s_),
+      ck(launch_seed_region(dm_->view(), seed, radius, buf.data(), static_cast<int>(buf.size()), &n, s_,
+                            field_->seed_dist.p),
          "seed region");
       if (n >= 0) {
         seeds.assign(buf.begin(), buf.begin() + n);
@@ -2028,6 +2033,32 @@ class PassEngine {
       std::sort(lat.begin(), lat.end());
       std::fprintf(stderr, "[dtb]   phase %d CTA done after start (us): min %.2f p50 %.2f p90 %.2f max %.2f\n", ph,
                    lat.front(), lat[lat.size() / 2], lat[lat.size() * 9 / 10], lat.back());
+      // Per step: the slowest CTA (what the barrier waits for) against the median one.
+      double smax = 0, smed = 0;
+      int ns = 0;
+      for (long st = 8; st < 64; ++st) {
+        const unsigned long long t0 = off >= 0 ? t[4 * (off + st) + ph] : 0;
+        if (!t0) continue;
+        std::vector<double> d;
+        for (int b = 0; b < blocks_; ++b) {
+          const unsigned long long tb = t[base + (st * 3 + ph) * blocks_ + b];
+          if (tb > t0) d.push_back(static_cast<double>(tb - t0) / 1e3);
+        }
+        if (d.size() < 2) continue;
+        if (ph == 1) {
+          int am = 0;
+          for (int b = 1; b < static_cast<int>(d.size()); ++b)
+            if (d[b] > d[am]) am = b;
+          std::fprintf(stderr, "%d:%.1f ", am, d[am]);
+        }
+        std::sort(d.begin(), d.end());
+        smax += d.back();
+        smed += d[d.size() / 2];
+        ++ns;
+      }
+      if (ns)
+        std::fprintf(stderr, "[dtb]   phase %d per step: slowest CTA %.2f us, median CTA %.2f us (mean over %d steps)\n",
+                     ph, smax / ns, smed / ns, ns);
     }
   }
 

@@ -288,6 +288,7 @@ class DeviceField {
   DevBuf<int2> added;   // band items gained this step (split certificate)
   DevBuf<int> add_stamp;  // per vertex: last step it gained a band item
   DevBuf<int> rem_stamp;  // per vertex: last step it lost a band item
+  DevBuf<unsigned long long> seed_dist;  // seed Dijkstra distances, kept "far" between calls
   DevBuf<unsigned> pairs;
   DevBuf<LayerStat> stat;
   DevBuf<TrailRec> trail;

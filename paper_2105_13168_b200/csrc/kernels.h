@@ -298,7 +298,9 @@ int launch_positions(const double* xyz, int nv, double scale, double* px, double
                      long long* fy, long long* fz, void* stream);
 void instr_report();
 // seed_region on the device: *n = -1 when a capacity is exceeded (use the host).
-int launch_seed_region(const DevMesh& m, unsigned seed, double radius, unsigned* out, int cap, int* n, void* stream);  // -DDTB_INSTR builds: latency histograms
+// dist: nv words all 0x7F7F7F7F7F7F7F7F, left so (or null: a scratch copy is allocated).
+int launch_seed_region(const DevMesh& m, unsigned seed, double radius, unsigned* out, int cap, int* n, void* stream,
+                       unsigned long long* dist = nullptr);  // -DDTB_INSTR builds: latency histograms
 // Device mesh construction (csrc/meshbuild.cu).  Returns 0 when the soup is a
 // valid closed, connected, consistently oriented manifold without unused
 // vertices (outputs filled, ne = 3nf/2), 1 when the host must build it (any

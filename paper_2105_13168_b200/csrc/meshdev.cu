@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
+#include <cstring>
+#include <vector>
 
 #include "kernels.h"
 
@@ -97,39 +99,44 @@ __global__ void k_front_fill(FrontBuild B, const int* off, int* col) {
 // what Dijkstra computes).  One CTA reaches the same fixed point by
 // frontier-based Bellman-Ford relaxation with atomicMin on the distance bits
 // (non-negative doubles order like their bit patterns); relaxations beyond the
-// radius are skipped since they cannot lead back inside it.  Overflowing a
-// capacity reports -1 and the caller uses the host.
-constexpr int kSeedCap = 1 << 15;  // touched vertices / frontier entries
+// radius are skipped since they cannot lead back inside it.  The frontier
+// lives in shared memory and each entry's row is relaxed by 8 lanes at once
+// (one round of loads per level instead of one per neighbour).  Overflowing
+// a capacity reports -1 and the caller uses the host.
+constexpr int kSeedCap = 1 << 15;   // touched vertices
+constexpr int kSeedFront = 4096;    // frontier entries per level (shared memory)
 constexpr unsigned long long kFar = 0x7F7F7F7F7F7F7F7Full;  // 3.4e306, the memset pattern
 struct SeedScratch {
-  int front[2][kSeedCap];
   int touched[kSeedCap];
-  int nfront[2], ntouched, overflow;
 };
 
 __global__ void __launch_bounds__(1024) k_seed_region(const int* off, const int* col, const double* px,
                                                       const double* py, const double* pz, unsigned seed, double radius,
                                                       unsigned long long* dist, SeedScratch* S, unsigned* out,
                                                       int cap, int* out_n) {
+  __shared__ int front[2][kSeedFront];
+  __shared__ int nfront[2], ntouched, overflow;
   if (threadIdx.x == 0) {
     dist[seed] = static_cast<unsigned long long>(__double_as_longlong(0.0));
-    S->front[0][0] = static_cast<int>(seed);
-    S->nfront[0] = 1;
-    S->nfront[1] = 0;
+    front[0][0] = static_cast<int>(seed);
+    nfront[0] = 1;
+    nfront[1] = 0;
     S->touched[0] = static_cast<int>(seed);
-    S->ntouched = 1;
-    S->overflow = 0;
+    ntouched = 1;
+    overflow = 0;
   }
   __syncthreads();
+  const int lane = threadIdx.x & 7, g0 = threadIdx.x >> 3, ng = blockDim.x >> 3;
   int cur = 0;
   while (true) {
-    const int n = S->nfront[cur];
-    if (n == 0 || S->overflow) break;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const int v = S->front[cur][i];
+    const int n = nfront[cur];
+    if (n == 0 || overflow) break;
+    for (int i = g0; i < n; i += ng) {
+      const int v = front[cur][i];
       const double dv = __longlong_as_double(static_cast<long long>(__ldcg(dist + v)));
       const double vx = px[v], vy = py[v], vz = pz[v];
-      for (int o = off[v]; o < off[v + 1]; ++o) {
+      const int o1 = off[v + 1];
+      for (int o = off[v] + lane; o < o1; o += 8) {
         const int u = col[o];
         const double dx = vx - px[u], dy = vy - py[u], dz = vz - pz[u];
         const double nd = dv + sqrt(dx * dx + dy * dy + dz * dz);
@@ -138,29 +145,34 @@ __global__ void __launch_bounds__(1024) k_seed_region(const int* off, const int*
         const unsigned long long old = atomicMin(dist + u, bits);
         if (bits < old) {
           if (old == kFar) {
-            const int t = atomicAdd(&S->ntouched, 1);
+            const int t = atomicAdd(&ntouched, 1);
             if (t < kSeedCap) S->touched[t] = u;
-            else S->overflow = 1;
+            else overflow = 1;
           }
-          const int q = atomicAdd(&S->nfront[cur ^ 1], 1);
-          if (q < kSeedCap) S->front[cur ^ 1][q] = u;
-          else S->overflow = 1;
+          const int q = atomicAdd(&nfront[cur ^ 1], 1);
+          if (q < kSeedFront) front[cur ^ 1][q] = u;
+          else overflow = 1;
         }
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0) S->nfront[cur] = 0;
+    if (threadIdx.x == 0) nfront[cur] = 0;
     cur ^= 1;
     __syncthreads();
   }
   // Every touched vertex ended at d <= radius (only such values are stored).
-  const int nt = min(S->ntouched, kSeedCap);
-  for (int i = threadIdx.x; i < nt && i < cap; i += blockDim.x) out[i] = static_cast<unsigned>(S->touched[i]);
-  for (int i = threadIdx.x; i < nt; i += blockDim.x) dist[S->touched[i]] = kFar;  // reset for the next call
-  if (threadIdx.x == 0) *out_n = (S->overflow || nt > cap) ? -1 : nt;
+  // out[0] = count (or -1), out[1..] = the vertices; dist back to "far".
+  const int nt = min(ntouched, kSeedCap);
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+    const int u = S->touched[i];
+    if (i < cap) out[1 + i] = static_cast<unsigned>(u);
+    dist[u] = kFar;
+  }
+  if (threadIdx.x == 0) *out_n = (overflow || nt > cap) ? -1 : nt;
 }
 
-int launch_seed_region(const DevMesh& m, unsigned seed, double radius, unsigned* out, int cap, int* n, void* stream) {
+int launch_seed_region(const DevMesh& m, unsigned seed, double radius, unsigned* out, int cap, int* n, void* stream,
+                       unsigned long long* dist) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (!(radius >= 0.0)) {  // NaN radius: the reference's loop breaks at once... let the host decide
     *n = -1;
@@ -168,23 +180,28 @@ int launch_seed_region(const DevMesh& m, unsigned seed, double radius, unsigned*
   }
   static_assert(kFar == 0x7F7F7F7F7F7F7F7Full, "distance reset value is a memset byte pattern");
   const size_t dbytes = sizeof(unsigned long long) * static_cast<size_t>(m.nv);
-  unsigned long long* dist = static_cast<unsigned long long*>(dev_alloc(dbytes));
-  SeedScratch* S = static_cast<SeedScratch*>(dev_alloc(sizeof(SeedScratch)));
-  unsigned* dout = static_cast<unsigned*>(dev_alloc(sizeof(unsigned) * (cap > 0 ? cap : 1)));
-  int* dn = static_cast<int*>(dev_alloc(sizeof(int)));
-  cudaMemsetAsync(dist, 0x7F, dbytes, s);
-  k_seed_region<<<1, 1024, 0, s>>>(m.n_off, m.n_col, m.px, m.py, m.pz, seed, radius, dist, S, dout, cap, dn);
-  note_launch();
-  cudaMemcpyAsync(n, dn, sizeof(int), cudaMemcpyDeviceToHost, s);
-  cudaError_t e = cudaStreamSynchronize(s);
-  if (e == cudaSuccess && *n > 0) {
-    cudaMemcpyAsync(out, dout, sizeof(unsigned) * (*n), cudaMemcpyDeviceToHost, s);
-    e = cudaStreamSynchronize(s);
+  const bool own = dist == nullptr;
+  if (own) {
+    dist = static_cast<unsigned long long*>(dev_alloc(dbytes));
+    cudaMemsetAsync(dist, 0x7F, dbytes, s);
   }
-  dev_free(dn, sizeof(int));
-  dev_free(dout, sizeof(unsigned) * (cap > 0 ? cap : 1));
+  cap = max(0, min(cap, kSeedCap));
+  SeedScratch* S = static_cast<SeedScratch*>(dev_alloc(sizeof(SeedScratch)));
+  const size_t obytes = sizeof(unsigned) * (static_cast<size_t>(cap) + 1);
+  unsigned* dout = static_cast<unsigned*>(dev_alloc(obytes));  // count, then the vertices
+  k_seed_region<<<1, 1024, 0, s>>>(m.n_off, m.n_col, m.px, m.py, m.pz, seed, radius, dist, S, dout, cap,
+                                   reinterpret_cast<int*>(dout));
+  note_launch();
+  // One read-back of count and list (the list is at most cap words).
+  std::vector<unsigned> h(static_cast<size_t>(cap) + 1);
+  cudaMemcpyAsync(h.data(), dout, obytes, cudaMemcpyDeviceToHost, s);
+  const cudaError_t e = cudaStreamSynchronize(s);
+  *n = static_cast<int>(h[0]);
+  if (e == cudaSuccess && *n > 0) std::memcpy(out, h.data() + 1, sizeof(unsigned) * static_cast<size_t>(*n));
+  if (*n < 0 && !own) cudaMemsetAsync(dist, 0x7F, dbytes, s);  // touched vertices may have gone unrecorded
+  dev_free(dout, obytes);
   dev_free(S, sizeof(SeedScratch));
-  dev_free(dist, dbytes);
+  if (own) dev_free(dist, dbytes);
   return static_cast<int>(e);
 }
 

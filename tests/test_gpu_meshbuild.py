@@ -112,3 +112,18 @@ def test_device_seed_region_matches_host(spec):
             finally:
                 del os.environ["DTB_SEED_DEVICE"]
             np.testing.assert_array_equal(dev, host)
+
+
+def test_device_seed_region_large_matches_host():
+    """The bench mesh (V = 988k) at the default seed radius and at a radius
+    whose region holds tens of thousands of vertices (wide frontiers)."""
+    m = dt.TriangleMesh.generate("genus:8:45")
+    for seed, r in [(0, 0.6708203932499369), (12345, 1.5), (987000, 0.2)]:
+        host = m.seed_region(seed, r)
+        os.environ["DTB_SEED_DEVICE"] = "1"
+        try:
+            dev = m.seed_region(seed, r)
+        finally:
+            del os.environ["DTB_SEED_DEVICE"]
+        assert len(host) > 0
+        np.testing.assert_array_equal(dev, host)
