@@ -113,11 +113,7 @@ __device__ __forceinline__ unsigned fkey(unsigned x) {
   x *= 0x85EBCA77u;
   return x ^ (x >> 13);
 }
-__global__ void k_face_union(const unsigned* partner, int ns, unsigned* p) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= ns) return;
-  unsigned a = static_cast<unsigned>(s) / 3, b = partner[s] / 3;
-  if (a >= b) return;  // each face pair once per shared edge
+__device__ __forceinline__ void funite(unsigned* p, unsigned a, unsigned b) {
   while (true) {
     a = froot(p, a);
     b = froot(p, b);
@@ -130,6 +126,28 @@ __global__ void k_face_union(const unsigned* partner, int ns, unsigned* p) {
     }
     if (atomicCAS(p + b, b, a) == b) return;
   }
+}
+// Afforest-style connectivity: link every face to its partner across edge
+// k (k = 0, then 1) with the trees flattened after each round; most faces
+// then share one component, and the last pass unites all three edges only
+// for faces outside the component of face 0.  Skipping an edge whose two
+// faces are both already in that component loses nothing, so the final
+// forest has exactly the components of the face graph.
+__global__ void k_face_link(const unsigned* partner, int nf, unsigned* p, int k) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  funite(p, static_cast<unsigned>(f), partner[3 * f + k] / 3);
+}
+__global__ void k_face_flatten(unsigned* p, int nf) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < nf) p[f] = froot(p, static_cast<unsigned>(f));
+}
+__global__ void k_face_link_rest(const unsigned* partner, int nf, unsigned* p) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  const unsigned c = froot(p, 0u);
+  if (froot(p, static_cast<unsigned>(f)) == c) return;
+  for (int k = 0; k < 3; ++k) funite(p, static_cast<unsigned>(f), partner[3 * f + k] / 3);
 }
 __global__ void k_face_roots(const unsigned* p, int nf, int* nroots) {
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
@@ -342,7 +360,11 @@ int build_mesh(MeshBuild& b, void* stream) {
   if (hbad) return 1;
   k_orient_check<<<nblk(ns), kT, 0, s>>>(b.soup, partner, ns, bad);
   k_face_init<<<nblk(nf), kT, 0, s>>>(fpar, nf);
-  k_face_union<<<nblk(ns), kT, 0, s>>>(partner, ns, fpar);
+  for (int e = 0; e < 2; ++e) {
+    k_face_link<<<nblk(nf), kT, 0, s>>>(partner, nf, fpar, e);
+    k_face_flatten<<<nblk(nf), kT, 0, s>>>(fpar, nf);
+  }
+  k_face_link_rest<<<nblk(nf), kT, 0, s>>>(partner, nf, fpar);
   k_face_roots<<<nblk(nf), kT, 0, s>>>(fpar, nf, bad + 1);
   k_geometry<<<gblocks, kT, 0, s>>>(b.xyz, nv, b.soup, nf, term, part, bad);
   k_finish<<<1, kT, 0, s>>>(part, gblocks, red);
@@ -430,7 +452,7 @@ int build_mesh(MeshBuild& b, void* stream) {
     if (!tmp6) return static_cast<int>(cudaErrorMemoryAllocation);
     cub::DeviceScan::ExclusiveSum(tmp6, tmp_bytes, cnt, b.v2v_off, nv + 1, s);
   }
-  note_launch(20);
+  note_launch(24);
   cudaMemcpyAsync(hb, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
   e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return static_cast<int>(e);
