@@ -72,14 +72,61 @@ __device__ double diagonal(const LapBuild& B, int v, bool& bad) {
   return sum;
 }
 
+// Row v of the stiffness matrix in one pass over v's faces (v2f order):
+// each corner edge (a, b) of a face that contains v adds -w to the diagonal
+// (faces in order, corner edges k = 0, 1, 2 within a face: the reference's
+// triplet order before its sort) and w to the off-diagonal of the other end,
+// whose two faces therefore add in face order, 0 + w1 + w2 -- term for term
+// the reference's triplet sums.  half_cot is symmetric in (a, b) bit for bit
+// (the products commute and the cross product only changes sign), so one
+// value serves both entries.  acc[j] belongs to the j-th neighbour of the
+// sorted row; returns the row length, or -1 above kMaxValence (then
+// diagonal / offdiag give the same values entry by entry).
+constexpr int kMaxValence = 32;
+__device__ int row_values(const LapBuild& B, int v, bool& bad, int* nbr, double* acc, double& diag) {
+  const int q0 = B.v2v_off[v], deg = B.v2v_off[v + 1] - q0;
+  if (deg > kMaxValence) return -1;  // the caller takes the entries one by one
+  for (int j = 0; j < deg; ++j) {
+    nbr[j] = B.v2v[q0 + j];
+    acc[j] = 0.0;
+  }
+  double d = 0.0;
+  for (int q = B.v2f_off[v]; q < B.v2f_off[v + 1]; ++q) {
+    const int f = B.v2f[q];
+    const unsigned t[3] = {B.faces[3 * f], B.faces[3 * f + 1], B.faces[3 * f + 2]};
+    for (int k = 0; k < 3; ++k) {
+      const unsigned a = t[k], b = t[(k + 1) % 3], c = t[(k + 2) % 3];
+      if (a != (unsigned)v && b != (unsigned)v) continue;
+      const double h = half_cot(B, a, b, c, bad);
+      d = d + (-h);
+      const int u = static_cast<int>(a == (unsigned)v ? b : a);
+      for (int j = 0; j < deg; ++j)
+        if (nbr[j] == u) {
+          acc[j] = acc[j] + h;
+          break;
+        }
+    }
+  }
+  diag = d;
+  return deg;
+}
+
 __global__ void k_row_count(LapBuild B, int* counts, int* bad_flag) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= B.nv) return;
   bool bad = false;
+  int nbr[kMaxValence];
+  double acc[kMaxValence], d;
+  const int deg = row_values(B, v, bad, nbr, acc, d);
   int n = 0;
-  if (diagonal(B, v, bad) != 0.0) ++n;
-  for (int q = B.v2v_off[v]; q < B.v2v_off[v + 1]; ++q)
-    if (offdiag(B, v, B.v2v[q], bad) != 0.0) ++n;
+  if (deg >= 0) {
+    n = d != 0.0 ? 1 : 0;
+    for (int j = 0; j < deg; ++j) n += acc[j] != 0.0;
+  } else {
+    if (diagonal(B, v, bad) != 0.0) ++n;
+    for (int q = B.v2v_off[v]; q < B.v2v_off[v + 1]; ++q)
+      if (offdiag(B, v, B.v2v[q], bad) != 0.0) ++n;
+  }
   counts[v] = n;
   if (bad) atomicExch(bad_flag, 1);
 }
@@ -88,7 +135,11 @@ __global__ void k_row_fill(LapBuild B) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= B.nv) return;
   bool bad = false;
-  const double d = diagonal(B, v, bad);
+  int nbr[kMaxValence];
+  double acc[kMaxValence], d;
+  const int deg = row_values(B, v, bad, nbr, acc, d);
+  const bool wide = deg < 0;
+  if (wide) d = diagonal(B, v, bad);
   int o = B.s_off[v];
   bool diag_done = false;
   double gersh = 0.0;
@@ -98,13 +149,14 @@ __global__ void k_row_fill(LapBuild B) {
     ++o;
     gersh = gersh + fabs(x);
   };
-  for (int q = B.v2v_off[v]; q < B.v2v_off[v + 1]; ++q) {
-    const int u = B.v2v[q];
+  const int q0 = B.v2v_off[v], n = B.v2v_off[v + 1] - q0;
+  for (int j = 0; j < n; ++j) {
+    const int u = wide ? B.v2v[q0 + j] : nbr[j];
     if (!diag_done && u > v) {
       if (d != 0.0) emit(v, d);
       diag_done = true;
     }
-    const double w = offdiag(B, v, u, bad);
+    const double w = wide ? offdiag(B, v, u, bad) : acc[j];
     if (w != 0.0) emit(u, w);
   }
   if (!diag_done && d != 0.0) emit(v, d);
