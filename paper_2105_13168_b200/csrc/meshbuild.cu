@@ -268,27 +268,40 @@ __global__ void k_edges(const unsigned* faces, const unsigned* pf, const int* ei
   fe[s] = static_cast<unsigned>(e);
   fe[q] = static_cast<unsigned>(e);
 }
-__global__ void k_corner_keys(const unsigned* faces, int ns, unsigned* key, unsigned* val, int* cnt) {
+// Adjacency rows by counting: per-vertex counts, an exclusive scan into the
+// row offsets, an atomic scatter into the rows, then each row sorted on its
+// own (rows hold at most a few dozen entries).  Same rows as a stable sort of
+// the (vertex, face) corners / (vertex, other end) half-edges.
+__global__ void k_count_corners(const unsigned* faces, int ns, int* cnt) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= ns) return;
-  key[s] = faces[s];
-  val[s] = static_cast<unsigned>(s);
-  atomicAdd(cnt + faces[s], 1);
+  if (s < ns) atomicAdd(cnt + faces[s], 1);
 }
-__global__ void k_slot_to_face(const unsigned* sval, int ns, int* v2f) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < ns) v2f[i] = static_cast<int>(sval[i] / 3);
+__global__ void k_scatter_corners(const unsigned* faces, int ns, int* cur, int* v2f) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < ns) v2f[atomicAdd(cur + faces[s], 1)] = s / 3;
 }
-__global__ void k_half_keys(const unsigned* edges, int nh, unsigned long long nv, unsigned long long* key, int* cnt) {
+__global__ void k_count_half(const unsigned* edges, int nh, int* cnt) {
   const int h = blockIdx.x * blockDim.x + threadIdx.x;
-  if (h >= nh) return;
-  const unsigned v = edges[h], o = edges[h ^ 1];
-  key[h] = static_cast<unsigned long long>(v) * nv + o;
-  atomicAdd(cnt + v, 1);
+  if (h < nh) atomicAdd(cnt + edges[h], 1);
 }
-__global__ void k_key_to_other(const unsigned long long* key, int nh, unsigned long long nv, int* v2v) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < nh) v2v[i] = static_cast<int>(key[i] % nv);
+__global__ void k_scatter_half(const unsigned* edges, int nh, int* cur, int* v2v) {
+  const int h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h < nh) v2v[atomicAdd(cur + edges[h], 1)] = static_cast<int>(edges[h ^ 1]);
+}
+__global__ void k_sort_rows(const int* off, int nv, int* col) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  int* r = col + off[v];
+  const int n = off[v + 1] - off[v];
+  for (int i = 1; i < n; ++i) {  // insertion sort of a short row
+    const int x = r[i];
+    int j = i - 1;
+    while (j >= 0 && r[j] > x) {
+      r[j + 1] = r[j];
+      --j;
+    }
+    r[j + 1] = x;
+  }
 }
 
 int bits_for(unsigned long long x) {
@@ -406,53 +419,31 @@ int build_mesh(MeshBuild& b, void* stream) {
   if (!tmp2) return static_cast<int>(cudaErrorMemoryAllocation);
   cub::DeviceScan::ExclusiveSum(tmp2, tmp_bytes, open, eid, ns, s);
   k_edges<<<nblk(ns), kT, 0, s>>>(b.faces, pf, eid, ns, b.edges, b.edge_faces, b.face_edges);
-  // vertex -> faces: stable sort of the corner slots by vertex.
+  // vertex -> faces (face order) and vertex -> vertices (ascending): rows by
+  // counting, then each row sorted (k_sort_rows).
   {
-    unsigned* ck0 = reinterpret_cast<unsigned*>(key0);
-    unsigned* ck1 = ck0 + ns;
-    unsigned* cv0 = partner;  // partner is no longer needed after k_final_partner
-    unsigned* cv1 = sc.get<unsigned>(ns);
     int* cnt = sc.get<int>(nv + 1);
-    if (!cv1 || !cnt) return static_cast<int>(cudaErrorMemoryAllocation);
-    cudaMemsetAsync(cnt, 0, sizeof(int) * (nv + 1), s);
-    k_corner_keys<<<nblk(ns), kT, 0, s>>>(b.faces, ns, ck0, cv0, cnt);
-    cub::DoubleBuffer<unsigned> ck(ck0, ck1), cvv(cv0, cv1);
-    const int vbits = bits_for(static_cast<unsigned long long>(nv));
-    tmp_bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, ck, cvv, ns, 0, vbits, s);
-    void* tmp3 = sc.get<char>(tmp_bytes);
-    if (!tmp3) return static_cast<int>(cudaErrorMemoryAllocation);
-    cub::DeviceRadixSort::SortPairs(tmp3, tmp_bytes, ck, cvv, ns, 0, vbits, s);
-    k_slot_to_face<<<nblk(ns), kT, 0, s>>>(cvv.Current(), ns, b.v2f);
-    tmp_bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, b.v2f_off, nv + 1, s);
-    void* tmp4 = sc.get<char>(tmp_bytes);
-    if (!tmp4) return static_cast<int>(cudaErrorMemoryAllocation);
-    cub::DeviceScan::ExclusiveSum(tmp4, tmp_bytes, cnt, b.v2f_off, nv + 1, s);
-  }
-  // vertex -> vertices: sort the 2E half-edges by (vertex, other end).
-  {
+    if (!cnt) return static_cast<int>(cudaErrorMemoryAllocation);
     const int nh = 2 * ne;
-    unsigned long long* hk0 = sc.get<unsigned long long>(nh);
-    unsigned long long* hk1 = sc.get<unsigned long long>(nh);
-    int* cnt = sc.get<int>(nv + 1);
-    if (!hk0 || !hk1 || !cnt) return static_cast<int>(cudaErrorMemoryAllocation);
-    cudaMemsetAsync(cnt, 0, sizeof(int) * (nv + 1), s);
-    k_half_keys<<<nblk(nh), kT, 0, s>>>(b.edges, nh, static_cast<unsigned long long>(nv), hk0, cnt);
-    cub::DoubleBuffer<unsigned long long> hk(hk0, hk1);
-    tmp_bytes = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, hk, nh, 0, kbits, s);
-    void* tmp5 = sc.get<char>(tmp_bytes);
-    if (!tmp5) return static_cast<int>(cudaErrorMemoryAllocation);
-    cub::DeviceRadixSort::SortKeys(tmp5, tmp_bytes, hk, nh, 0, kbits, s);
-    k_key_to_other<<<nblk(nh), kT, 0, s>>>(hk.Current(), nh, static_cast<unsigned long long>(nv), b.v2v);
-    tmp_bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, b.v2v_off, nv + 1, s);
-    void* tmp6 = sc.get<char>(tmp_bytes);
-    if (!tmp6) return static_cast<int>(cudaErrorMemoryAllocation);
-    cub::DeviceScan::ExclusiveSum(tmp6, tmp_bytes, cnt, b.v2v_off, nv + 1, s);
+    for (int pass = 0; pass < 2; ++pass) {
+      const int n = pass == 0 ? ns : nh;
+      int* off = pass == 0 ? b.v2f_off : b.v2v_off;
+      int* col = pass == 0 ? b.v2f : b.v2v;
+      cudaMemsetAsync(cnt, 0, sizeof(int) * (nv + 1), s);
+      if (pass == 0) k_count_corners<<<nblk(n), kT, 0, s>>>(b.faces, n, cnt);
+      else k_count_half<<<nblk(n), kT, 0, s>>>(b.edges, n, cnt);
+      tmp_bytes = 0;
+      cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, off, nv + 1, s);
+      void* tmp = sc.get<char>(tmp_bytes);
+      if (!tmp) return static_cast<int>(cudaErrorMemoryAllocation);
+      cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, off, nv + 1, s);
+      cudaMemcpyAsync(cnt, off, sizeof(int) * nv, cudaMemcpyDeviceToDevice, s);  // row cursors
+      if (pass == 0) k_scatter_corners<<<nblk(n), kT, 0, s>>>(b.faces, n, cnt, col);
+      else k_scatter_half<<<nblk(n), kT, 0, s>>>(b.edges, n, cnt, col);
+      k_sort_rows<<<nblk(nv), kT, 0, s>>>(off, nv, col);
+    }
   }
-  note_launch(24);
+  note_launch(26);
   cudaMemcpyAsync(hb, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
   e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return static_cast<int>(e);
