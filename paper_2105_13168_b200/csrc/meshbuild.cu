@@ -58,29 +58,64 @@ __global__ void k_unused(const unsigned char* used, int nv, int* bad) {
 }
 
 // Slot s = 3f + k is the directed edge corner k -> corner k+1 of input face f.
-__global__ void k_slot_keys(const unsigned* soup, int ns, unsigned long long nv, unsigned long long* key,
-                            unsigned* val) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= ns) return;
+// Pairing by counting: the slots are bucketed by the lower end of their
+// vertex pair (count, scan, scatter); each bucket -- a few dozen slots at
+// most -- pairs its slots by the upper end.  Every unordered pair must be
+// used by exactly two slots (closed manifold).  Slots of an invalid soup
+// (flagged by k_soup_check) are left out.
+__device__ __forceinline__ bool slot_ends(const unsigned* soup, int s, unsigned nv, unsigned& lo, unsigned& hi) {
   const int f = s / 3, k = s % 3;
   const unsigned a = soup[3 * f + k], b = soup[3 * f + (k + 1) % 3];
-  key[s] = static_cast<unsigned long long>(min(a, b)) * nv + max(a, b);
-  val[s] = static_cast<unsigned>(s);
+  lo = min(a, b);
+  hi = max(a, b);
+  return hi < nv;
+}
+__global__ void k_count_lo(const unsigned* soup, int ns, unsigned nv, int* cnt) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned lo, hi;
+  if (s < ns && slot_ends(soup, s, nv, lo, hi)) atomicAdd(cnt + lo, 1);
+}
+__global__ void k_scatter_lo(const unsigned* soup, int ns, unsigned nv, int* cur, unsigned* rows) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned lo, hi;
+  if (s < ns && slot_ends(soup, s, nv, lo, hi)) rows[atomicAdd(cur + lo, 1)] = static_cast<unsigned>(s);
+}
+__global__ void k_pair_rows(const unsigned* soup, const int* off, const unsigned* rows, int nv, unsigned* partner,
+                            int* bad) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  const int o0 = off[v], n = off[v + 1] - o0;
+  constexpr int kCap = 64;
+  unsigned hs[kCap];
+  unsigned lo, hi;
+  if (n <= kCap)
+    for (int i = 0; i < n; ++i) {
+      slot_ends(soup, static_cast<int>(rows[o0 + i]), static_cast<unsigned>(nv), lo, hi);
+      hs[i] = hi;
+    }
+  for (int i = 0; i < n; ++i) {
+    unsigned hi_i;
+    if (n <= kCap) hi_i = hs[i];
+    else slot_ends(soup, static_cast<int>(rows[o0 + i]), static_cast<unsigned>(nv), lo, hi_i);
+    int m = 0, mate = -1;
+    for (int j = 0; j < n; ++j) {
+      if (j == i) continue;
+      unsigned hi_j;
+      if (n <= kCap) hi_j = hs[j];
+      else slot_ends(soup, static_cast<int>(rows[o0 + j]), static_cast<unsigned>(nv), lo, hi_j);
+      if (hi_j == hi_i) {
+        ++m;
+        mate = j;
+      }
+    }
+    if (m != 1) {
+      atomicOr(bad, kBadPairing);
+      return;
+    }
+    partner[rows[o0 + i]] = rows[o0 + mate];
+  }
 }
 
-// Every unordered pair must be used by exactly two slots (closed manifold).
-__global__ void k_pair(const unsigned long long* key, const unsigned* val, int ns, unsigned* partner, int* bad) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= ns || (i > 0 && key[i - 1] == key[i])) return;
-  const bool two = i + 1 < ns && key[i + 1] == key[i];
-  const bool three = two && i + 2 < ns && key[i + 2] == key[i];
-  if (!two || three) {
-    atomicOr(bad, kBadPairing);
-    return;
-  }
-  partner[val[i]] = val[i + 1];
-  partner[val[i + 1]] = val[i];
-}
 
 // Consistent orientation: the partner slot traverses the edge the other way.
 __global__ void k_orient_check(const unsigned* soup, const unsigned* partner, int ns, int* bad) {
@@ -304,11 +339,6 @@ __global__ void k_sort_rows(const int* off, int nv, int* col) {
   }
 }
 
-int bits_for(unsigned long long x) {
-  int b = 1;
-  while (b < 64 && (1ull << b) <= x) ++b;
-  return b;
-}
 
 // Scratch from the engine's caching allocator (engine.cpp dev_alloc); every
 // exit of build_mesh synchronizes the stream first, so blocks go back to the
@@ -338,7 +368,6 @@ int build_mesh(MeshBuild& b, void* stream) {
   Scratch sc{s, {}};
   int* bad = sc.get<int>(2);
   unsigned char* used = sc.get<unsigned char>(nv);
-  unsigned long long* key0 = sc.get<unsigned long long>(ns);
   unsigned long long* key1 = sc.get<unsigned long long>(ns);
   unsigned* val0 = sc.get<unsigned>(ns);
   unsigned* val1 = sc.get<unsigned>(ns);
@@ -348,24 +377,30 @@ int build_mesh(MeshBuild& b, void* stream) {
   const int gblocks = 148 * 4;
   Red* part = sc.get<Red>(gblocks);
   Red* red = sc.get<Red>(1);
-  if (!bad || !used || !key0 || !key1 || !val0 || !val1 || !partner || !fpar || !term || !part || !red)
+  if (!bad || !used || !key1 || !val0 || !val1 || !partner || !fpar || !term || !part || !red)
     return static_cast<int>(cudaErrorMemoryAllocation);
   cudaMemsetAsync(bad, 0, 2 * sizeof(int), s);
   cudaMemsetAsync(used, 0, nv, s);
   k_soup_check<<<nblk(nf), kT, 0, s>>>(b.soup, nf, nv, used, bad);
   k_unused<<<nblk(nv), kT, 0, s>>>(used, nv, bad);
   // Pair the slots by their unordered vertex pair.
-  k_slot_keys<<<nblk(ns), kT, 0, s>>>(b.soup, ns, static_cast<unsigned long long>(nv), key0, val0);
-  const int kbits = bits_for(static_cast<unsigned long long>(nv) * static_cast<unsigned long long>(nv));
   size_t tmp_bytes = 0;
-  cub::DoubleBuffer<unsigned long long> dk(key0, key1);
-  cub::DoubleBuffer<unsigned> dv(val0, val1);
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, dk, dv, ns, 0, kbits, s);
-  void* tmp = sc.get<char>(tmp_bytes);
-  if (!tmp) return static_cast<int>(cudaErrorMemoryAllocation);
-  cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, dk, dv, ns, 0, kbits, s);
-  cudaMemsetAsync(partner, 0, sizeof(unsigned) * ns, s);
-  k_pair<<<nblk(ns), kT, 0, s>>>(dk.Current(), dv.Current(), ns, partner, bad);
+  {
+    int* cnt = sc.get<int>(nv + 1);
+    int* off = sc.get<int>(nv + 1);
+    unsigned* rows = val0;
+    if (!cnt || !off) return static_cast<int>(cudaErrorMemoryAllocation);
+    cudaMemsetAsync(cnt, 0, sizeof(int) * (nv + 1), s);
+    k_count_lo<<<nblk(ns), kT, 0, s>>>(b.soup, ns, static_cast<unsigned>(nv), cnt);
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, off, nv + 1, s);
+    void* tmp = sc.get<char>(tmp_bytes);
+    if (!tmp) return static_cast<int>(cudaErrorMemoryAllocation);
+    cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, off, nv + 1, s);
+    cudaMemcpyAsync(cnt, off, sizeof(int) * nv, cudaMemcpyDeviceToDevice, s);  // bucket cursors
+    k_scatter_lo<<<nblk(ns), kT, 0, s>>>(b.soup, ns, static_cast<unsigned>(nv), cnt, rows);
+    cudaMemsetAsync(partner, 0, sizeof(unsigned) * ns, s);
+    k_pair_rows<<<nblk(nv), kT, 0, s>>>(b.soup, off, rows, nv, partner, bad);
+  }
   int hbad = 0;
   cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
   cudaError_t e = cudaStreamSynchronize(s);
@@ -443,7 +478,7 @@ int build_mesh(MeshBuild& b, void* stream) {
       k_sort_rows<<<nblk(nv), kT, 0, s>>>(off, nv, col);
     }
   }
-  note_launch(26);
+  note_launch(27);
   cudaMemcpyAsync(hb, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
   e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return static_cast<int>(e);
