@@ -69,6 +69,9 @@ def test_fallbacks_raise_host_errors():
     cases = {
         "open": (v, f[:-1]),
         "out of range": (v, np.vstack([f, [[0, 1, len(v) + 5]]]).astype(np.uint32)),
+        "out of range, even": (v, np.vstack([f, [[0, 1, len(v) + 5], [1, 0, len(v) + 7]]]).astype(np.uint32)),
+        "edge in four faces": (v, np.vstack([f, f[:2]]).astype(np.uint32)),
+        "hole and extra": (v, np.vstack([f[2:], [[0, 1, 2], [2, 1, 3]]]).astype(np.uint32)),
     }
     for name, (vv, ff) in cases.items():
         with pytest.raises(dt.DiffTopoError) as dev_err:
