@@ -254,10 +254,39 @@ std::shared_ptr<DeviceMesh> DeviceMesh::from_soup(const double* xyz, size_t nv, 
   if (nv == 0 || nf == 0 || nv >= (1u << 31) || 3 * nf >= (1u << 31)) return nullptr;
   StageTimer tm(s);
   std::shared_ptr<DeviceMesh> d(new DeviceMesh());
-  d->xyz_.alloc(3 * nv);
-  d->xyz_.upload(xyz, 3 * nv, s);
+  // The faces go first (the build starts with them); the positions follow on
+  // a side stream and land while the faces are paired (first read: the
+  // geometry pass, which waits on their event).
+  struct SideStream {
+    cudaStream_t st = nullptr;
+    cudaEvent_t faces_in = nullptr, xyz_in = nullptr;
+    SideStream() {
+      cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&faces_in, cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&xyz_in, cudaEventDisableTiming);
+    }
+  };
+  thread_local SideStream side;
   DevBuf<unsigned> in(3 * nf);
   in.upload(soup, 3 * nf, s);
+  d->xyz_.alloc(3 * nv);
+  const bool overlap = side.st && side.faces_in && side.xyz_in;
+  if (overlap) {
+    cuda_check(cudaEventRecord(side.faces_in, s), "event record");
+    cuda_check(cudaStreamWaitEvent(side.st, side.faces_in, 0), "stream wait");
+    d->xyz_.upload(xyz, 3 * nv, side.st);
+    cuda_check(cudaEventRecord(side.xyz_in, side.st), "event record");
+  } else {
+    d->xyz_.upload(xyz, 3 * nv, s);
+  }
+  // Every exit (early returns, errors) waits for the side copy before the
+  // buffers it writes can be freed; destroyed before `in` and `d`.
+  struct CopyDone {
+    cudaEvent_t ev;
+    ~CopyDone() {
+      if (ev) cudaEventSynchronize(ev);
+    }
+  } copy_done{overlap ? side.xyz_in : nullptr};
   const size_t ne = 3 * nf / 2;
   d->faces.alloc(3 * nf);
   d->edges.alloc(2 * ne);
@@ -272,6 +301,7 @@ std::shared_ptr<DeviceMesh> DeviceMesh::from_soup(const double* xyz, size_t nv, 
   b.nv = static_cast<int>(nv);
   b.nf = static_cast<int>(nf);
   b.xyz = d->xyz_.p;
+  b.xyz_ready = overlap ? side.xyz_in : nullptr;
   b.soup = in.p;
   b.faces = d->faces.p;
   b.edges = d->edges.p;

@@ -308,6 +308,7 @@ int launch_seed_region(const DevMesh& m, unsigned seed, double radius, unsigned*
 struct MeshBuild {
   int nv = 0, nf = 0, ne = 0;
   const double* xyz = nullptr;     // 3nv, device
+  void* xyz_ready = nullptr;       // cudaEvent_t the stream waits on before reading xyz (or null)
   const unsigned* soup = nullptr;  // 3nf input faces, device
   unsigned *faces = nullptr, *edges = nullptr, *edge_faces = nullptr, *face_edges = nullptr;  // 3F, 2E, 2E, 3F
   int *v2f_off = nullptr, *v2f = nullptr, *v2v_off = nullptr, *v2v = nullptr;              // V+1, 3F, V+1, 2E

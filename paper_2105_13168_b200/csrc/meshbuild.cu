@@ -414,6 +414,7 @@ int build_mesh(MeshBuild& b, void* stream) {
   }
   k_face_link_rest<<<nblk(nf), kT, 0, s>>>(partner, nf, fpar);
   k_face_roots<<<nblk(nf), kT, 0, s>>>(fpar, nf, bad + 1);
+  if (b.xyz_ready) cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(b.xyz_ready), 0);  // positions uploaded
   k_geometry<<<gblocks, kT, 0, s>>>(b.xyz, nv, b.soup, nf, term, part, bad);
   k_finish<<<1, kT, 0, s>>>(part, gblocks, red);
   int hb[2] = {0, 0};
