@@ -59,10 +59,15 @@ __device__ __forceinline__ void refresh_interest(const FieldBuf& F, const DevWor
 __global__ void k_init(DevField F, DevWork W, int nv) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= nv) return;
+  // Whole 32-byte sectors (slots 0..15 of the layer ids, 0..3 of the values):
+  // a partial sector write costs the memory system a read to merge it.
   for (int q = 0; q < 2; ++q) {
     F.b[q].cnt[v] = 1;
-    F.b[q].lay[static_cast<size_t>(v) * kSlots] = 0;
-    F.b[q].val[static_cast<size_t>(v) * kSlots] = 1.0;
+    uint4* l = reinterpret_cast<uint4*>(F.b[q].lay + static_cast<size_t>(v) * kSlots);
+    l[0] = make_uint4(0, 0, 0, 0);
+    l[1] = make_uint4(0, 0, 0, 0);
+    double4* x = reinterpret_cast<double4*>(F.b[q].val + static_cast<size_t>(v) * kSlots);
+    x[0] = make_double4(1.0, 0.0, 0.0, 0.0);
     F.b[q].interest[v] = 0;
     F.b[q].binfo[v] = make_uint4(0, 0, 0, 0);
   }
