@@ -257,16 +257,22 @@ std::shared_ptr<DeviceMesh> DeviceMesh::from_soup(const double* xyz, size_t nv, 
   // The faces go first (the build starts with them); the positions follow on
   // a side stream and land while the faces are paired (first read: the
   // geometry pass, which waits on their event).
+  // One side stream and its two events per host thread and device (streams
+  // belong to the device current when they were created).
   struct SideStream {
     cudaStream_t st = nullptr;
     cudaEvent_t faces_in = nullptr, xyz_in = nullptr;
-    SideStream() {
+    void create() {
       cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
       cudaEventCreateWithFlags(&faces_in, cudaEventDisableTiming);
       cudaEventCreateWithFlags(&xyz_in, cudaEventDisableTiming);
     }
   };
-  thread_local SideStream side;
+  thread_local std::map<int, SideStream> sides;
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "device");
+  SideStream& side = sides[dev];
+  if (!side.st) side.create();
   DevBuf<unsigned> in(3 * nf);
   in.upload(soup, 3 * nf, s);
   d->xyz_.alloc(3 * nv);
