@@ -252,10 +252,12 @@ def test_bench_workload_final_state_bit_exact(spec, steps):
     parity.compare_events(res.events(), ref["events"])
 
 
-@pytest.mark.parametrize("spec,steps", [("genus:8:45", 3000), ("gyroid:2:26:0.3:1.0", 1500),
-                                        ("torus:96:32:3:1.0", 2000), ("limbstar:2:3:3", 2000),
-                                        ("plate:2:20:0.5", 2000)])
-def test_split_certificate_never_hides_a_split(spec, steps, monkeypatch):
+@pytest.mark.parametrize("spec,steps,seed", [("genus:8:45", 3000, 0), ("gyroid:2:26:0.3:1.0", 1500, 0),
+                                             ("torus:96:32:3:1.0", 2000, 0), ("limbstar:2:3:3", 2000, 0),
+                                             ("plate:2:20:0.5", 2000, 0), ("plate:2:20:0.5", 2000, 30000),
+                                             ("torus_irr:40:20:2:0.6:0.2:0.05:7", 2000, 11),
+                                             ("icosphere:3:2.0", 600, 5), ("genus:2:3", 2000, 100)])
+def test_split_certificate_never_hides_a_split(spec, steps, seed, monkeypatch):
     """DTB_CERT_VERIFY=1 runs the union-find after every check whose split
     certificate held (gained items anchored, lost items' stars connected)
     and fails the pass if it finds two components there; the pass must
@@ -263,9 +265,9 @@ def test_split_certificate_never_hides_a_split(spec, steps, monkeypatch):
     mesh = dt.TriangleMesh.generate(spec)
     op = dt.assemble_laplacian(mesh)
     cfg = dt.default_config(max_steps=steps)
-    plain = dt.run_initial_pass(mesh, op, 0, cfg)
+    plain = dt.run_initial_pass(mesh, op, seed, cfg)
     monkeypatch.setenv("DTB_CERT_VERIFY", "1")
-    checked = dt.run_initial_pass(mesh, op, 0, cfg)
+    checked = dt.run_initial_pass(mesh, op, seed, cfg)
     assert checked.status == plain.status and checked.steps == plain.steps
     assert checked.field_hash() == plain.field_hash()
     assert [(e.kind, e.step, e.layers) for e in checked.events()] == [(e.kind, e.step, e.layers)
