@@ -327,6 +327,15 @@ def main():
     achieved = alg_bytes / k_time / 1e9
     peak, peak_kind = peaks()
 
+    # ---- the full-mesh operator sweep (what a dense formulation reads every step)
+    sw = op.sweep_bench(10)
+    dense = {"kernel": "k_spmv_ell (y = M^-1 S x over all V rows, padded 8-entry rows)",
+             "us_per_sweep": 1e6 * sw["seconds"], "achieved": sw["gbs"], "peak": peak, "unit": "GB/s",
+             "frac": sw["gbs"] / peak, "alg_bytes_per_sweep": sw["bytes"],
+             "frontier_us_per_step": 1e6 * total / args.steps / args.pass_steps,
+             "note": "each sweep after a 256 MiB L2-evicting read; a dense step would pay at least this "
+                     "every step, the frontier step touches ~0.6 % of V"}
+
     # ---- end-to-end through the C ABI from host buffers
     e2e = None
     if not args.no_e2e:
@@ -379,6 +388,7 @@ def main():
                      "avg_band_vertices_per_step": sum_band / (args.pass_steps * args.steps)},
         "clocks": clocks.summary(),
         "e2e": e2e,
+        "dense_sweep": dense,
     }
     if rank == 0 and world == 1:
         S = args.pass_steps

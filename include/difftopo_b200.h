@@ -117,6 +117,10 @@ int dtb_laplacian_info(const dtb_laplacian* op, int64_t* nnz, double* gershgorin
 int dtb_laplacian_csr(const dtb_laplacian* op, int32_t* off, int32_t* col, double* val, double* mass);
 /* LaplacianOperator::apply (operators.hpp:27): y = M^-1 S x. */
 int dtb_laplacian_apply(const dtb_laplacian* op, const double* x, double* y);
+/* Diagnostics (no reference counterpart): a full-mesh sweep of the operator
+ * (the padded-row SpMV apply uses), timed on the device after an L2 flush;
+ * mean seconds per sweep and algorithmic bytes per sweep. */
+int dtb_laplacian_sweep_bench(const dtb_laplacian* op, int32_t reps, double* seconds, double* bytes);
 /* stable_time_step (diffusion.hpp:58). */
 int dtb_stable_time_step(const dtb_laplacian* op, const dtb_coefficients* c, double* dt);
 

@@ -94,6 +94,7 @@ def load_library(path: str = LIB_PATH):
         "dtb_laplacian_info": (C.c_int, [P, pI64, pD]),
         "dtb_laplacian_csr": (C.c_int, [P, pI32, pI32, pD, pD]),
         "dtb_laplacian_apply": (C.c_int, [P, pD, pD]),
+        "dtb_laplacian_sweep_bench": (C.c_int, [P, C.c_int32, pD, pD]),
         "dtb_stable_time_step": (C.c_int, [P, C.POINTER(Coefficients), pD]),
         "dtb_run_initial_pass": (C.c_int, [P, P, U32, C.POINTER(Config), C.POINTER(Coefficients), pP]),
         "dtb_run_initial_pass_batch": (C.c_int, [pP, pP, pU32, C.c_int32, C.POINTER(Config),
@@ -355,6 +356,14 @@ class LaplacianOperator:
         y = np.empty_like(x)
         _check(_lib.dtb_laplacian_apply(self._h, _ptr(x, C.c_double), _ptr(y, C.c_double)))
         return y
+
+    def sweep_bench(self, reps: int = 10) -> dict:
+        """Diagnostics: one full-mesh sweep of the operator (the padded-row
+        SpMV ``apply`` runs) timed on the device after an L2 flush; mean
+        seconds and algorithmic bytes per sweep."""
+        sec, nbytes = C.c_double(), C.c_double()
+        _check(_lib.dtb_laplacian_sweep_bench(self._h, int(reps), C.byref(sec), C.byref(nbytes)))
+        return {"seconds": sec.value, "bytes": nbytes.value, "gbs": nbytes.value / sec.value / 1e9}
 
 
 def assemble_laplacian(mesh: TriangleMesh) -> LaplacianOperator:

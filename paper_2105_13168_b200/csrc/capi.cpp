@@ -482,6 +482,16 @@ int dtb_laplacian_apply(const dtb_laplacian* op, const double* x, double* y) {
   });
 }
 
+int dtb_laplacian_sweep_bench(const dtb_laplacian* op, int32_t reps, double* seconds, double* bytes) {
+  return guard([&] {
+    need(op, "op");
+    need(seconds, "seconds");
+    need(bytes, "bytes");
+    if (reps < 1) fail(kInvalidParameter, "reps must be positive");
+    op->op->sweep_bench(reps, op->stream, seconds, bytes);
+  });
+}
+
 int dtb_stable_time_step(const dtb_laplacian* op, const dtb_coefficients* c, double* dt) {
   return guard([&] {
     need(op, "op");

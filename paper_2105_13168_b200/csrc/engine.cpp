@@ -516,9 +516,50 @@ void DeviceLaplacian::apply(const double* xh, double* yh, cudaStream_t s) const 
   const int nv = static_cast<int>(dm_->nv());
   DevBuf<double> x(nv), y(nv);
   x.upload(xh, nv, s);
-  ck(launch_spmv(nv, off.p, col.p, val.p, mass.p, x.p, y.p, s), "spmv");
+  ck(launch_spmv_ell(nv, e_len.p, e_col.p, e_val.p, off.p, col.p, val.p, mass.p, x.p, y.p, s), "spmv");
   y.download(yh, nv, s);
   cuda_check(cudaStreamSynchronize(s), "spmv sync");
+}
+
+// A full-mesh sweep of the operator (what a dense formulation of the step
+// would read every step), timed on the device.  Every sweep follows a
+// 256 MiB read that evicts L2; `reps` (flush, sweep) pairs and `reps`
+// flushes alone are timed as two event-bracketed batches and the difference
+// is the sweeps' time (no per-launch event overhead in it).  Algorithmic
+// bytes per sweep: the padded rows (8 x 12 B + 1 B length), the mass, x once
+// and y once per vertex.
+void DeviceLaplacian::sweep_bench(int reps, cudaStream_t s, double* seconds, double* bytes) const {
+  const int nv = static_cast<int>(dm_->nv());
+  DevBuf<double> x(nv), y(nv);
+  cuda_check(cudaMemsetAsync(x.p, 0, sizeof(double) * nv, s), "memset");
+  DevBuf<char> flush(256u << 20);
+  DevBuf<int> sink(1);
+  cuda_check(cudaMemsetAsync(flush.p, 0, flush.n, s), "memset");
+  struct Events {
+    cudaEvent_t a = nullptr, b = nullptr;
+    ~Events() {
+      if (a) cudaEventDestroy(a);
+      if (b) cudaEventDestroy(b);
+    }
+  } ev;
+  cuda_check(cudaEventCreate(&ev.a), "event");
+  cuda_check(cudaEventCreate(&ev.b), "event");
+  auto batch = [&](bool sweep) {
+    cuda_check(cudaEventRecord(ev.a, s), "event");
+    for (int r = 0; r < reps; ++r) {
+      ck(launch_read_all(flush.p, flush.n, sink.p, s), "L2 eviction");
+      if (sweep) ck(launch_spmv_ell(nv, e_len.p, e_col.p, e_val.p, off.p, col.p, val.p, mass.p, x.p, y.p, s), "spmv");
+    }
+    cuda_check(cudaEventRecord(ev.b, s), "event");
+    cuda_check(cudaEventSynchronize(ev.b), "event");
+    float ms = 0;
+    cuda_check(cudaEventElapsedTime(&ms, ev.a, ev.b), "elapsed");
+    return 1e-3 * ms;
+  };
+  batch(true);  // warm-up
+  const double with = batch(true), without = batch(false);
+  *seconds = std::max(0.0, with - without) / std::max(1, reps);
+  *bytes = static_cast<double>(nv) * (kEll * 12.0 + 1.0 + 8.0 + 8.0 + 8.0);
 }
 
 DevMesh DeviceLaplacian::view() const {

@@ -134,6 +134,7 @@ class DeviceLaplacian {
   void download(std::vector<int>& off, std::vector<int>& col, std::vector<double>& val, std::vector<double>& mass,
                 cudaStream_t s) const;
   void apply(const double* x_host, double* y_host, cudaStream_t s) const;
+  void sweep_bench(int reps, cudaStream_t s, double* seconds, double* bytes) const;
   std::shared_ptr<DeviceMesh> mesh() const { return dm_; }
   DevMesh view() const;
   void build_ell(cudaStream_t s);

@@ -323,6 +323,11 @@ int launch_front_count(const FrontBuild& b, int* c_off, int* nnz, void* stream);
 int launch_front_fill(const FrontBuild& b, const int* c_off, int* c_col, void* stream);
 int launch_ell(int nv, const int* off, const int* col, const double* val, unsigned char* e_len, int* e_col,
                double* e_val, void* stream);
+// Reads `bytes` of device memory (an L2 eviction without dirty lines); writes *sink only in theory.
+int launch_read_all(const void* p, size_t bytes, int* sink, void* stream);
+// y = M^-1 S x over the padded rows (DevMesh::e_*), CSR for longer rows; the same sums as launch_spmv.
+int launch_spmv_ell(int nv, const unsigned char* e_len, const int* e_col, const double* e_val, const int* off,
+                    const int* col, const double* val, const double* mass, const double* x, double* y, void* stream);
 int launch_spmv(int nv, const int* off, const int* col, const double* val, const double* mass,
                 const double* x, double* y, void* stream);
 

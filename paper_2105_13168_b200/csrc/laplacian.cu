@@ -239,6 +239,50 @@ __global__ void k_ell(int nv, const int* off, const int* col, const double* val,
     e_val[static_cast<size_t>(v) * kEll + j] = ok ? val[k0 + j] : 0.0;
   }
 }
+// The same sums over the padded rows: one thread per row reads its 8 columns
+// and 8 values with six 16-byte loads, rows longer than kEll take the CSR.
+// Summation order and rounding are k_spmv's.
+__global__ void k_spmv_ell(int nv, const unsigned char* e_len, const int* e_col, const double* e_val, const int* off,
+                           const int* col, const double* val, const double* mass, const double* x, double* y) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  const int n = e_len[v];
+  double acc = 0.0;
+  if (n <= kEll) {
+    const size_t b = static_cast<size_t>(v) * kEll;
+    const int4 c0 = __ldg(reinterpret_cast<const int4*>(e_col + b));
+    const int4 c1 = __ldg(reinterpret_cast<const int4*>(e_col + b + 4));
+    const double2 w0 = __ldg(reinterpret_cast<const double2*>(e_val + b));
+    const double2 w1 = __ldg(reinterpret_cast<const double2*>(e_val + b + 2));
+    const double2 w2 = __ldg(reinterpret_cast<const double2*>(e_val + b + 4));
+    const double2 w3 = __ldg(reinterpret_cast<const double2*>(e_val + b + 6));
+    const int cs[kEll] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    const double ws[kEll] = {w0.x, w0.y, w1.x, w1.y, w2.x, w2.y, w3.x, w3.y};
+    double xs[kEll];
+#pragma unroll
+    for (int j = 0; j < kEll; ++j) xs[j] = j < n ? __ldg(x + cs[j]) : 0.0;
+#pragma unroll
+    for (int j = 0; j < kEll; ++j)
+      if (j < n) acc = acc + ws[j] * xs[j];
+  } else {
+    for (int k = off[v]; k < off[v + 1]; ++k) acc = acc + val[k] * x[col[k]];
+  }
+  y[v] = acc / mass[v];
+}
+
+// Reads n 16-byte words (an L2 eviction that leaves clean lines behind, so
+// the next kernel does not pay for write-backs); writes only if a word holds
+// an impossible value.
+__global__ void k_read_all(const int4* p, size_t n, int* sink) {
+  int acc = 0;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int4 q = __ldcs(p + i);
+    acc ^= q.x ^ q.y ^ q.z ^ q.w;
+  }
+  if (acc == 0x7A5E1234) *sink = acc;
+}
+
 }  // namespace
 
 int launch_ell(int nv, const int* off, const int* col, const double* val, unsigned char* e_len, int* e_col,
@@ -253,6 +297,21 @@ int launch_spmv(int nv, const int* off, const int* col, const double* val, const
   const int threads = 256;
   k_spmv<<<(nv + threads - 1) / threads, threads, 0, static_cast<cudaStream_t>(stream)>>>(nv, off, col, val, mass, x,
                                                                                            y);
+  note_launch();
+  return static_cast<int>(cudaGetLastError());
+}
+
+int launch_read_all(const void* p, size_t bytes, int* sink, void* stream) {
+  k_read_all<<<148 * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const int4*>(p), bytes / 16, sink);
+  note_launch();
+  return static_cast<int>(cudaGetLastError());
+}
+
+int launch_spmv_ell(int nv, const unsigned char* e_len, const int* e_col, const double* e_val, const int* off,
+                    const int* col, const double* val, const double* mass, const double* x, double* y, void* stream) {
+  const int threads = 256;
+  k_spmv_ell<<<(nv + threads - 1) / threads, threads, 0, static_cast<cudaStream_t>(stream)>>>(
+      nv, e_len, e_col, e_val, off, col, val, mass, x, y);
   note_launch();
   return static_cast<int>(cudaGetLastError());
 }
