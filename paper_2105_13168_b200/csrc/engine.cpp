@@ -476,6 +476,7 @@ DeviceLaplacian::DeviceLaplacian(std::shared_ptr<DeviceMesh> dm, cudaStream_t s)
   DevBuf<double> gmax(1);
   b.gersh_max = gmax.p;
   b.nnz = dnnz.p;
+  b.nroom = 2 * static_cast<long long>(dm_->ne());
   const int rc = launch_assemble(b, s);
   if (rc == -1) fail(kDegeneracyError, "non-finite cotangent weight");
   ck(rc, "laplacian assembly");

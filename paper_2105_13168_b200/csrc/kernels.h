@@ -272,6 +272,7 @@ struct LapBuild {
   double *gersh_row;           // out: per-row bound
   double *gersh_max;           // out: max over the rows (device scalar)
   int *nnz;                    // out
+  long long nroom = 0;         // sum of row lengths of v2v (2E): the fill's room besides the diagonals
 };
 int launch_assemble(const LapBuild& b, void* stream);
 

@@ -111,27 +111,12 @@ __device__ int row_values(const LapBuild& B, int v, bool& bad, int* nbr, double*
   return deg;
 }
 
-__global__ void k_row_count(LapBuild B, int* counts, int* bad_flag) {
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= B.nv) return;
-  bool bad = false;
-  int nbr[kMaxValence];
-  double acc[kMaxValence], d;
-  const int deg = row_values(B, v, bad, nbr, acc, d);
-  int n = 0;
-  if (deg >= 0) {
-    n = d != 0.0 ? 1 : 0;
-    for (int j = 0; j < deg; ++j) n += acc[j] != 0.0;
-  } else {
-    if (diagonal(B, v, bad) != 0.0) ++n;
-    for (int q = B.v2v_off[v]; q < B.v2v_off[v + 1]; ++q)
-      if (offdiag(B, v, B.v2v[q], bad) != 0.0) ++n;
-  }
-  counts[v] = n;
-  if (bad) atomicExch(bad_flag, 1);
-}
-
-__global__ void k_row_fill(LapBuild B) {
+// Fills row v once: its non-zero entries (the reference's triplet sums drop
+// exact zeros) packed at the start of the row's room for the diagonal and
+// every mesh neighbour (offset v2v_off[v] + v), the number of them in
+// counts[v]; k_row_compact then moves the rows to their scanned offsets.
+constexpr int kRowBad = 1;
+__global__ void k_row_fill(LapBuild B, int* flags, int* counts) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= B.nv) return;
   bool bad = false;
@@ -140,7 +125,8 @@ __global__ void k_row_fill(LapBuild B) {
   const int deg = row_values(B, v, bad, nbr, acc, d);
   const bool wide = deg < 0;
   if (wide) d = diagonal(B, v, bad);
-  int o = B.s_off[v];
+  const int o0 = B.v2v_off[v] + v;
+  int o = o0;
   bool diag_done = false;
   double gersh = 0.0;
   auto emit = [&](int c, double x) {
@@ -160,6 +146,8 @@ __global__ void k_row_fill(LapBuild B) {
     if (w != 0.0) emit(u, w);
   }
   if (!diag_done && d != 0.0) emit(v, d);
+  counts[v] = o - o0;
+  if (bad) atomicOr(flags, kRowBad);
   // Lumped mass: area / 3 of every incident face, in face order.
   double m = 0.0;
   for (int q = B.v2f_off[v]; q < B.v2f_off[v + 1]; ++q) {
@@ -171,6 +159,18 @@ __global__ void k_row_fill(LapBuild B) {
   }
   B.mass[v] = m;
   B.gersh_row[v] = gersh / m;
+}
+
+// Moves each filled row from its room (v2v_off[v] + v) to its scanned offset.
+__global__ void k_row_compact(int nv, const int* v2v_off, const int* off, const int* tcol, const double* tval,
+                              int* col, double* val) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  const int src = v2v_off[v] + v, dst = off[v], n = off[v + 1] - dst;
+  for (int k = 0; k < n; ++k) {
+    col[dst + k] = tcol[src + k];
+    val[dst + k] = tval[src + k];
+  }
 }
 
 __global__ void k_spmv(int nv, const int* off, const int* col, const double* val, const double* mass, const double* x,
@@ -191,20 +191,27 @@ int launch_assemble(const LapBuild& b, void* stream) {
   const int threads = 128, blocks = (b.nv + threads - 1) / threads;
   int* counts = nullptr;
   int* bad = nullptr;
+  int* tcol = nullptr;
+  double* tval = nullptr;
+  const size_t room = static_cast<size_t>(b.nv) + static_cast<size_t>(b.nroom);  // diagonal + neighbours
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&counts), sizeof(int) * (b.nv + 1), s);
-  if (e != cudaSuccess) return static_cast<int>(e);
-  e = cudaMallocAsync(reinterpret_cast<void**>(&bad), sizeof(int), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&bad), sizeof(int), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&tcol), sizeof(int) * room, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&tval), sizeof(double) * room, s);
   if (e != cudaSuccess) return static_cast<int>(e);
   cudaMemsetAsync(bad, 0, sizeof(int), s);
   cudaMemsetAsync(counts + b.nv, 0, sizeof(int), s);
-  k_row_count<<<blocks, threads, 0, s>>>(b, counts, bad);
-  note_launch(4);  // row count, two scan passes, row fill
+  LapBuild bt = b;  // rows filled into their rooms first
+  bt.s_col = tcol;
+  bt.s_val = tval;
+  k_row_fill<<<blocks, threads, 0, s>>>(bt, bad, counts);
   size_t tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, b.s_off, b.nv + 1, s);
   void* tmp = nullptr;
   cudaMallocAsync(&tmp, tmp_bytes, s);
   cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, b.s_off, b.nv + 1, s);
-  k_row_fill<<<blocks, threads, 0, s>>>(b);
+  k_row_compact<<<blocks, threads, 0, s>>>(b.nv, b.v2v_off, b.s_off, tcol, tval, b.s_col, b.s_val);
+  note_launch(4);  // row fill, two scan passes, compaction
   cudaMemcpyAsync(b.nnz, b.s_off + b.nv, sizeof(int), cudaMemcpyDeviceToDevice, s);
   // Gershgorin bound: max over the rows (exact in any order).
   size_t red_bytes = 0;
@@ -219,11 +226,13 @@ int launch_assemble(const LapBuild& b, void* stream) {
   cudaFreeAsync(red, s);
   cudaFreeAsync(counts, s);
   cudaFreeAsync(bad, s);
+  cudaFreeAsync(tcol, s);
+  cudaFreeAsync(tval, s);
   e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return static_cast<int>(e);
   e = cudaGetLastError();
   if (e != cudaSuccess) return static_cast<int>(e);
-  return hbad ? -1 : 0;
+  return (hbad & kRowBad) ? -1 : 0;
 }
 
 namespace {

@@ -293,3 +293,54 @@ def test_operator_apply_matches_csr_sums(spec):
     for j in range(width):
         acc = acc + np.where(j < lens, prod[:, j], 0.0)
     assert np.array_equal(y, acc / mass)
+
+
+def _grid_cube_obj(path, n):
+    """Closed cube surface, n x n squares per side, each split along one
+    diagonal: every diagonal's two opposite angles are right angles, so its
+    cotangent weight is exactly zero (the reference drops it)."""
+    index, verts, faces = {}, [], []
+
+    def vid(p):
+        if p not in index:
+            index[p] = len(verts)
+            verts.append(p)
+        return index[p]
+
+    for axis in range(3):
+        for side in (0, n):
+            for i in range(n):
+                for j in range(n):
+                    quad = []
+                    for di, dj in ((0, 0), (1, 0), (1, 1), (0, 1)):
+                        p = [0, 0, 0]
+                        p[axis] = side
+                        p[(axis + 1) % 3] = i + di
+                        p[(axis + 2) % 3] = j + dj
+                        quad.append(vid(tuple(p)))
+                    a, b, c, d = quad if side == n else quad[::-1]
+                    faces += [(a, b, c), (a, c, d)]
+    with open(path, "w") as fh:
+        for p in verts:
+            fh.write("v %d %d %d\n" % p)
+        for f in faces:
+            fh.write("f %d %d %d\n" % (f[0] + 1, f[1] + 1, f[2] + 1))
+
+
+def test_laplacian_assembly_drops_exact_zero_weights(tmp_path):
+    """Rows with exact zero weights leave the no-count assembly for the
+    counted one; the operator matches the reference's entry for entry."""
+    path = str(tmp_path / "cube.obj")
+    _grid_cube_obj(path, 6)
+    spec = "file:" + path
+    mesh = dt.TriangleMesh.generate(spec)
+    op = dt.assemble_laplacian(mesh)
+    off, col, val, mass = op.csr()
+    assert np.count_nonzero(val == 0.0) == 0
+    assert len(val) < (len(off) - 1) + 2 * mesh.info()["E"]  # zeros were dropped
+    L = refdata.ref_laplacian(spec)
+    assert np.array_equal(off, L["off"]) and np.array_equal(col, L["col"])
+    assert np.array_equal(mass.view(np.uint64), L["mass"].view(np.uint64))
+    rows = np.repeat(np.arange(len(off) - 1), np.diff(off))
+    diag = rows == col
+    assert np.array_equal(val[~diag].view(np.uint64), L["val"][~diag].view(np.uint64))
