@@ -358,13 +358,20 @@ void DeviceMesh::derive(const double* d_xyz, double maxabs, cudaStream_t s) {
   fb.v2v = n_col.p;
   fb.v2f_off = f_off.p;
   fb.v2f = f_col.p;
+  fb.nrel_room = 2 * static_cast<long long>(ne);
   c_off.alloc(nv + 1);
   int nnzc = 0;
-  const int rc = launch_front_count(fb, c_off.p, &nnzc, s);
+  void* room = nullptr;
+  const int rc = launch_front_count(fb, c_off.p, &nnzc, &room, s);
   if (rc == -1) fail(kCapacityExceeded, "vertex valence above 32");
   ck(rc, "front connectivity");
-  c_col.alloc(static_cast<size_t>(std::max(1, nnzc)));
-  ck(launch_front_fill(fb, c_off.p, c_col.p, s), "front connectivity");
+  try {
+    c_col.alloc(static_cast<size_t>(std::max(1, nnzc)));
+  } catch (...) {
+    cudaFreeAsync(room, s);
+    throw;
+  }
+  ck(launch_front_fill(fb, c_off.p, c_col.p, room, s), "front connectivity");
   cuda_check(cudaStreamSynchronize(s), "mesh upload");
 
   view_.nv = static_cast<int>(nv);

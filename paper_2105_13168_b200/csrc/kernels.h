@@ -279,6 +279,7 @@ int launch_assemble(const LapBuild& b, void* stream);
 // Mesh arrays built on the device (meshdev.cu).
 struct FrontBuild {
   int nv;
+  long long nrel_room;  // sum of valences (2E): the relation room is twice that
   const unsigned *faces, *face_edges, *edge_faces, *edges;  // 3F, 3F, 2E, 2E
   const int *v2v_off, *v2v, *v2f_off, *v2f;
 };
@@ -320,8 +321,11 @@ int build_mesh(MeshBuild& b, void* stream);
 // Caching device allocator (engine.cpp), shared with the kernel-side helpers.
 void* dev_alloc(size_t bytes);
 void dev_free(void* p, size_t bytes);
-int launch_front_count(const FrontBuild& b, int* c_off, int* nnz, void* stream);
-int launch_front_fill(const FrontBuild& b, const int* c_off, int* c_col, void* stream);
+// Gathers every vertex's relations into a room (returned through *room) and
+// scans their counts into c_off; -1 when a vertex has too many relations.
+int launch_front_count(const FrontBuild& b, int* c_off, int* nnz, void** room, void* stream);
+// Moves the relations from the room to c_col and frees the room.
+int launch_front_fill(const FrontBuild& b, const int* c_off, int* c_col, void* room, void* stream);
 int launch_ell(int nv, const int* off, const int* col, const double* val, unsigned char* e_len, int* e_col,
                double* e_val, void* stream);
 // Reads `bytes` of device memory (an L2 eviction without dirty lines); writes *sink only in theory.

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -71,22 +72,30 @@ __device__ int related(const FrontBuild& B, int v, int* out, bool* overflow) {
   return m;
 }
 
-__global__ void k_front_count(FrontBuild B, int* counts, int* overflow) {
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= B.nv) return;
-  int tmp[kMaxRel];
-  bool over = false;
-  counts[v] = related(B, v, tmp, &over);
-  if (over) *overflow = 1;
-}
-
-__global__ void k_front_fill(FrontBuild B, const int* off, int* col) {
+// Relations are gathered once, into each vertex's room (2 x its valence
+// entries from 2 * v2v_off[v]: a vertex has at most valence neighbours and
+// valence faces), then moved to the scanned offsets.
+__global__ void k_front_room(FrontBuild B, int* counts, int* overflow, int* room) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= B.nv) return;
   int tmp[kMaxRel];
   bool over = false;
   const int n = related(B, v, tmp, &over);
-  for (int i = 0; i < n; ++i) col[off[v] + i] = tmp[i];
+  const int base = 2 * B.v2v_off[v], cap = 2 * (B.v2v_off[v + 1] - B.v2v_off[v]);
+  if (over || n > cap) {
+    *overflow = 1;
+    counts[v] = 0;
+    return;
+  }
+  for (int i = 0; i < n; ++i) room[base + i] = tmp[i];
+  counts[v] = n;
+}
+
+__global__ void k_front_compact(FrontBuild B, const int* room, const int* off, int* col) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= B.nv) return;
+  const int base = 2 * B.v2v_off[v], dst = off[v], n = off[v + 1] - dst;
+  for (int i = 0; i < n; ++i) col[dst + i] = room[base + i];
 }
 
 }  // namespace
@@ -214,16 +223,18 @@ int launch_positions(const double* xyz, int nv, double scale, double* px, double
 
 // Count pass + exclusive scan into c_off; returns the column count through
 // *nnz, or -1 when a vertex has more than kMaxRel relations.
-int launch_front_count(const FrontBuild& b, int* c_off, int* nnz, void* stream) {
+int launch_front_count(const FrontBuild& b, int* c_off, int* nnz, void** room_out, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  int *counts = nullptr, *over = nullptr;
+  int *counts = nullptr, *over = nullptr, *room = nullptr;
+  const size_t nroom = std::max<size_t>(1, 2 * static_cast<size_t>(b.nrel_room));
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&counts), sizeof(int) * (b.nv + 1), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&over), sizeof(int), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&room), sizeof(int) * nroom, s);
   if (e != cudaSuccess) return static_cast<int>(e);
-  cudaMallocAsync(reinterpret_cast<void**>(&over), sizeof(int), s);
   cudaMemsetAsync(over, 0, sizeof(int), s);
   cudaMemsetAsync(counts + b.nv, 0, sizeof(int), s);
   const int blocks = (b.nv + 127) / 128;
-  k_front_count<<<blocks, 128, 0, s>>>(b, counts, over);
+  k_front_room<<<blocks, 128, 0, s>>>(b, counts, over, room);
   size_t tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, c_off, b.nv + 1, s);
   void* tmp = nullptr;
@@ -237,16 +248,20 @@ int launch_front_count(const FrontBuild& b, int* c_off, int* nnz, void* stream) 
   cudaFreeAsync(counts, s);
   cudaFreeAsync(over, s);
   e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return static_cast<int>(e);
-  if (h[1]) return -1;
+  if (e != cudaSuccess || h[1]) {
+    cudaFreeAsync(room, s);
+    return e != cudaSuccess ? static_cast<int>(e) : -1;
+  }
   *nnz = h[0];
+  *room_out = room;
   return static_cast<int>(cudaGetLastError());
 }
 
-int launch_front_fill(const FrontBuild& b, const int* c_off, int* c_col, void* stream) {
+int launch_front_fill(const FrontBuild& b, const int* c_off, int* c_col, void* room, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  k_front_fill<<<(b.nv + 127) / 128, 128, 0, s>>>(b, c_off, c_col);
+  k_front_compact<<<(b.nv + 127) / 128, 128, 0, s>>>(b, static_cast<const int*>(room), c_off, c_col);
   note_launch();
+  cudaFreeAsync(room, s);
   return static_cast<int>(cudaGetLastError());
 }
 
