@@ -365,12 +365,16 @@ void DeviceMesh::derive(const double* d_xyz, double maxabs, cudaStream_t s) {
   const int rc = launch_front_count(fb, c_off.p, &nnzc, &room, s);
   if (rc == -1) fail(kCapacityExceeded, "vertex valence above 32");
   ck(rc, "front connectivity");
-  try {
-    c_col.alloc(static_cast<size_t>(std::max(1, nnzc)));
-  } catch (...) {
-    cudaFreeAsync(room, s);
-    throw;
-  }
+  struct RoomGuard {  // freed once the stream has finished with it (every exit syncs first)
+    void* p;
+    size_t bytes;
+    cudaStream_t s;
+    ~RoomGuard() {
+      cudaStreamSynchronize(s);
+      dev_free(p, bytes);
+    }
+  } room_guard{room, front_room_bytes(fb), s};
+  c_col.alloc(static_cast<size_t>(std::max(1, nnzc)));
   ck(launch_front_fill(fb, c_off.p, c_col.p, room, s), "front connectivity");
   cuda_check(cudaStreamSynchronize(s), "mesh upload");
 

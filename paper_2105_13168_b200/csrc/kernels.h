@@ -324,8 +324,12 @@ void dev_free(void* p, size_t bytes);
 // Gathers every vertex's relations into a room (returned through *room) and
 // scans their counts into c_off; -1 when a vertex has too many relations.
 int launch_front_count(const FrontBuild& b, int* c_off, int* nnz, void** room, void* stream);
-// Moves the relations from the room to c_col and frees the room.
+// Moves the relations from the room to c_col; the caller frees the room
+// (dev_free(room, front_room_bytes(b))) once the stream is done with it.
 int launch_front_fill(const FrontBuild& b, const int* c_off, int* c_col, void* room, void* stream);
+inline size_t front_room_bytes(const FrontBuild& b) {
+  return sizeof(int) * (b.nrel_room > 0 ? 2 * static_cast<size_t>(b.nrel_room) : 1);
+}
 int launch_ell(int nv, const int* off, const int* col, const double* val, unsigned char* e_len, int* e_col,
                double* e_val, void* stream);
 // Reads `bytes` of device memory (an L2 eviction without dirty lines); writes *sink only in theory.

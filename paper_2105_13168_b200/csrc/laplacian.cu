@@ -194,11 +194,22 @@ int launch_assemble(const LapBuild& b, void* stream) {
   int* tcol = nullptr;
   double* tval = nullptr;
   const size_t room = static_cast<size_t>(b.nv) + static_cast<size_t>(b.nroom);  // diagonal + neighbours
+  // The row rooms come from the library's caching allocator (a stream-ordered
+  // pool allocation of this size is mapped anew after every synchronisation
+  // and serialises concurrent batch lanes); freed after the closing sync.
+  tcol = static_cast<int*>(dev_alloc(sizeof(int) * room));
+  tval = static_cast<double*>(dev_alloc(sizeof(double) * room));
+  auto release = [&]() {
+    dev_free(tcol, sizeof(int) * room);
+    dev_free(tval, sizeof(double) * room);
+  };
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&counts), sizeof(int) * (b.nv + 1), s);
   if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&bad), sizeof(int), s);
-  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&tcol), sizeof(int) * room, s);
-  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&tval), sizeof(double) * room, s);
-  if (e != cudaSuccess) return static_cast<int>(e);
+  if (e != cudaSuccess) {
+    cudaStreamSynchronize(s);
+    release();
+    return static_cast<int>(e);
+  }
   cudaMemsetAsync(bad, 0, sizeof(int), s);
   cudaMemsetAsync(counts + b.nv, 0, sizeof(int), s);
   LapBuild bt = b;  // rows filled into their rooms first
@@ -226,9 +237,8 @@ int launch_assemble(const LapBuild& b, void* stream) {
   cudaFreeAsync(red, s);
   cudaFreeAsync(counts, s);
   cudaFreeAsync(bad, s);
-  cudaFreeAsync(tcol, s);
-  cudaFreeAsync(tval, s);
   e = cudaStreamSynchronize(s);
+  release();
   if (e != cudaSuccess) return static_cast<int>(e);
   e = cudaGetLastError();
   if (e != cudaSuccess) return static_cast<int>(e);

@@ -225,12 +225,17 @@ int launch_positions(const double* xyz, int nv, double scale, double* px, double
 // *nnz, or -1 when a vertex has more than kMaxRel relations.
 int launch_front_count(const FrontBuild& b, int* c_off, int* nnz, void** room_out, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  int *counts = nullptr, *over = nullptr, *room = nullptr;
-  const size_t nroom = std::max<size_t>(1, 2 * static_cast<size_t>(b.nrel_room));
+  int *counts = nullptr, *over = nullptr;
+  // The room comes from the library's caching allocator (see launch_assemble);
+  // the caller frees it with dev_free(room, front_room_bytes(b)) after the
+  // stream has finished with it.
+  int* room = static_cast<int*>(dev_alloc(front_room_bytes(b)));
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&counts), sizeof(int) * (b.nv + 1), s);
   if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&over), sizeof(int), s);
-  if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&room), sizeof(int) * nroom, s);
-  if (e != cudaSuccess) return static_cast<int>(e);
+  if (e != cudaSuccess) {
+    dev_free(room, front_room_bytes(b));
+    return static_cast<int>(e);
+  }
   cudaMemsetAsync(over, 0, sizeof(int), s);
   cudaMemsetAsync(counts + b.nv, 0, sizeof(int), s);
   const int blocks = (b.nv + 127) / 128;
@@ -249,7 +254,7 @@ int launch_front_count(const FrontBuild& b, int* c_off, int* nnz, void** room_ou
   cudaFreeAsync(over, s);
   e = cudaStreamSynchronize(s);
   if (e != cudaSuccess || h[1]) {
-    cudaFreeAsync(room, s);
+    dev_free(room, front_room_bytes(b));
     return e != cudaSuccess ? static_cast<int>(e) : -1;
   }
   *nnz = h[0];
@@ -261,7 +266,6 @@ int launch_front_fill(const FrontBuild& b, const int* c_off, int* c_col, void* r
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   k_front_compact<<<(b.nv + 127) / 128, 128, 0, s>>>(b, static_cast<const int*>(room), c_off, c_col);
   note_launch();
-  cudaFreeAsync(room, s);
   return static_cast<int>(cudaGetLastError());
 }
 
